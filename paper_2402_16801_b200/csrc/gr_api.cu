@@ -1,0 +1,571 @@
+// gr_api.cu -- the C ABI (include/gridrogue_b200.h): device state
+// ownership, the per-step launch sequence, and the reference-layout state
+// channel.
+//
+// One step (BatchEnv.step, bindings/.../__init__.py:63-84) on the handle's
+// stream:
+//   k_step        game logic for every env, rewards/done/info, per-block
+//                 done counts, batch-wide flags             (gr_step.cu)
+//   k_scan        exclusive scan of done counts -> local done ranks
+//   [all-gather of the 4 x int32 exchange record -- multi-GPU only]
+//   k_finish_info global rank offset, OR of flags, pool size for this step
+//   k_worldgen    fresh worlds for the pool slots this shard consumes
+//   k_install_pool  EpisodeStats + install_worlds for done envs
+//   k_symbolic / k_pixels  post-reset observation
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <cstdarg>
+#include <string>
+#include <vector>
+#include <algorithm>
+#include <cuda_runtime.h>
+
+#include "gr_device.cuh"
+#include "gr_state.cuh"
+#include "gr_kernels.cuh"
+
+namespace gr {
+void launch_scan(const int32_t* block_done, int32_t* block_off, int nb, const uint32_t* cur_flags, int32_t* exchange,
+                 cudaStream_t st);
+void launch_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t step_key, StepInfo* info,
+                        uint32_t* flags_out, cudaStream_t st);
+void launch_install_initial(bool ext, const DS& S, const WBuf& wb, int64_t n, cudaStream_t st);
+void launch_install_pool(bool ext, const DS& S, const InstallArgs& a, const int32_t* block_off, cudaStream_t st);
+
+// policies.RandomPolicy.actions (policies.py:31-37)
+__global__ void k_random_actions(int64_t* out, int64_t n, int64_t env0, uint32_t key, int na) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float u = u32f(key, (uint32_t)(env0 + i));
+  out[i] = (int64_t)__fmul_rn(u, (float)na) % na;
+}
+
+// first invalid action (engine.py:715-717)
+__global__ void k_validate(const int64_t* a, int64_t n, int na, unsigned long long* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && (a[i] < 0 || a[i] >= na)) atomicMin(bad, (unsigned long long)i);
+}
+
+// bit2 of flags: does some env stand on a dark floor (obs.py:236)
+__global__ void k_dark(DS S, int64_t n, uint32_t* flags) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool d = i < n && C_FLOOR_AMB[GR_AT(S, GR_F_PFLOOR, uint8_t, 0, i)] < 1.0f;
+  if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(flags, 4u);
+}
+
+// apply the deferred dead-lane cooldown decrements (see gr_step.cu)
+__global__ void k_materialize(DS S, int64_t n, int F, const uint32_t* flags) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint8_t p = S.cd_pending[i];
+  if (!p) return;
+  const int pf = F > 1 ? GR_AT(S, GR_F_PFLOOR, uint8_t, 0, i) : 0;
+  const uint32_t fl = flags[0];
+  for (int l = 0; l < 3; ++l)
+    if ((fl & 1u) && ((p >> l) & 1)) {
+      uint8_t& c = GR_AT(S, GR_F_MEL_CD, uint8_t, pf * 3 + l, i);
+      if (c > 0) c -= 1;
+    }
+  for (int l = 0; l < 2; ++l)
+    if ((fl & 2u) && ((p >> (3 + l)) & 1)) {
+      uint8_t& c = GR_AT(S, GR_F_RAN_CD, uint8_t, pf * 2 + l, i);
+      if (c > 0) c -= 1;
+    }
+  S.cd_pending[i] = 0;
+}
+
+}  // namespace gr
+
+using namespace gr;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) return fail(GR_E_CUDA, "%s: %s", #x, cudaGetErrorString(e_));   \
+  } while (0)
+
+struct gr_env {
+  gr_config cfg;
+  bool ext;
+  TierDims d;
+  int64_t n, M, nb;
+  DS S;
+  WBuf pool;
+  WMeta* init_meta = nullptr;
+  int32_t *block_done = nullptr, *block_off = nullptr, *exchange = nullptr;
+  uint32_t *cur_flags = nullptr, *prev_flags = nullptr;
+  StepInfo* info = nullptr;
+  unsigned long long* bad = nullptr;
+  unsigned long long* counters = nullptr;       // worldgen [5]
+  unsigned long long *st_episodes = nullptr, *st_steps = nullptr, *st_ach = nullptr;
+  double* st_return = nullptr;
+  uint64_t pool_key = 0, env_key = 0;
+  int64_t step_index = 0;
+  bool have_reset = false;
+  bool validate = true;
+  int64_t launches = 0;
+  int64_t last_bad_env = -1, last_bad_action = 0;
+  // e2e scratch
+  void* h_obs_dev = nullptr;
+  int64_t* h_act_dev = nullptr;
+  float* h_rew_dev = nullptr;
+  uint8_t *h_done_dev = nullptr, *h_newly_dev = nullptr, *h_floor_dev = nullptr;
+  uint32_t* h_time_dev = nullptr;
+  cudaStream_t h_stream = nullptr;
+  std::vector<void*> allocs;
+};
+
+static int64_t obs_elems_of(const gr_env* e) {
+  if (e->cfg.obs_mode == GR_OBS_SYMBOLIC) return e->ext ? 8268 : 1345;
+  if (e->cfg.obs_mode == GR_OBS_PIXELS) {
+    const int px = e->cfg.tile_px;
+    return (int64_t)(e->d.VR + 2) * px * (e->d.VC + (e->ext ? 2 : 0)) * px * 3;
+  }
+  return 0;
+}
+
+static int dev_alloc(gr_env* e, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t err = cudaMalloc(p, bytes);
+  if (err != cudaSuccess) return fail(GR_E_OOM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(err));
+  e->allocs.push_back(*p);
+  err = cudaMemset(*p, 0, bytes);
+  if (err != cudaSuccess) return fail(GR_E_CUDA, "cudaMemset: %s", cudaGetErrorString(err));
+  return GR_OK;
+}
+
+extern "C" {
+
+const char* gr_last_error(void) { return g_err.c_str(); }
+int gr_version(void) { return GR_ABI_VERSION; }
+
+int gr_field_info(int32_t tier, int32_t field, int64_t* elems_per_env, int32_t* elem_size) {
+  if (field < 0 || field >= GR_NFIELDS) return fail(GR_E_INVALID, "unknown field id %d", field);
+  if (tier != GR_TIER_CLASSIC && tier != GR_TIER_EXTENDED) return fail(GR_E_INVALID, "unknown tier %d", tier);
+  const TierDims& d = tier == GR_TIER_EXTENDED ? EXT_DIMS : CLASSIC_DIMS;
+  if (elems_per_env) *elems_per_env = ref_elems(field, d);
+  if (elem_size) *elem_size = ref_esz(field);
+  return GR_OK;
+}
+
+void gr_destroy(gr_env* e) {
+  if (!e) return;
+  cudaSetDevice(e->cfg.device);
+  for (void* p : e->allocs) cudaFree(p);
+  if (e->h_stream) cudaStreamDestroy(e->h_stream);
+  delete e;
+}
+
+int gr_create(const gr_config* cfg, gr_env** out) {
+  if (!cfg || !out) return fail(GR_E_INVALID, "null argument");
+  *out = nullptr;
+  if (cfg->tier != GR_TIER_CLASSIC && cfg->tier != GR_TIER_EXTENDED)
+    return fail(GR_E_INVALID, "unknown tier %d", cfg->tier);
+  if (cfg->obs_mode < GR_OBS_NONE || cfg->obs_mode > GR_OBS_PIXELS)
+    return fail(GR_E_INVALID, "unknown obs_mode %d", cfg->obs_mode);
+  if (cfg->obs_mode == GR_OBS_PIXELS && cfg->tile_px != 7 && cfg->tile_px != 10 && cfg->tile_px != 16)
+    return fail(GR_E_INVALID, "tile_px must be one of (7, 10, 16)");
+  if (cfg->n_envs < 1) return fail(GR_E_INVALID, "n_envs must be >= 1");
+  if (cfg->reset_ratio < 1) return fail(GR_E_INVALID, "reset_ratio must be >= 1");
+  const int64_t ng = cfg->n_envs_global > 0 ? cfg->n_envs_global : cfg->n_envs;
+  if (cfg->env_offset < 0 || cfg->env_offset + cfg->n_envs > ng)
+    return fail(GR_E_INVALID, "shard [%lld, %lld) outside the %lld-env batch", (long long)cfg->env_offset,
+                (long long)(cfg->env_offset + cfg->n_envs), (long long)ng);
+  cudaError_t ce = cudaSetDevice(cfg->device);
+  if (ce != cudaSuccess) return fail(GR_E_CUDA, "cudaSetDevice(%d): %s", cfg->device, cudaGetErrorString(ce));
+  gr_env* e = new gr_env();
+  e->cfg = *cfg;
+  e->cfg.n_envs_global = ng;
+  if (e->cfg.max_episode_length <= 0) e->cfg.max_episode_length = 100000;
+  e->ext = cfg->tier == GR_TIER_EXTENDED;
+  e->d = e->ext ? EXT_DIMS : CLASSIC_DIMS;
+  e->n = cfg->n_envs;
+  e->M = std::max<int64_t>(1, (ng + cfg->reset_ratio - 1) / cfg->reset_ratio);
+  e->nb = (e->n + 127) / 128;
+  int rc = GR_OK;
+  e->S.ns = e->n;
+  for (int f = 0; f < GR_NFIELDS && rc == GR_OK; ++f) {
+    const size_t bytes = (size_t)device_comps(f, e->d) * e->n * FIELD_TABLE[f].esz;
+    rc = dev_alloc(e, &e->S.f[f], bytes);
+  }
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.cd_pending, e->n);
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.ep_return, e->n * sizeof(double));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.ep_length, e->n * sizeof(int32_t));
+  const int64_t cap = std::min(e->n, e->M);
+  const size_t wbytes = (size_t)cap * e->d.F * e->d.H * e->d.W;
+  e->pool.cap = cap;
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->pool.blocks, wbytes);
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->pool.items, wbytes);
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->pool.meta, cap * sizeof(WMeta));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->block_done, e->nb * sizeof(int32_t));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->block_off, e->nb * sizeof(int32_t));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->exchange, 4 * sizeof(int32_t));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->cur_flags, sizeof(uint32_t));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->prev_flags, sizeof(uint32_t));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->info, sizeof(StepInfo));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->bad, sizeof(unsigned long long));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->counters, 5 * sizeof(unsigned long long));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->st_episodes, sizeof(unsigned long long));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->st_steps, sizeof(unsigned long long));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->st_ach, 67 * sizeof(unsigned long long));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->st_return, sizeof(double));
+  if (rc != GR_OK) {
+    gr_destroy(e);
+    return rc;
+  }
+  // batch.BatchState keys (batch.py:144-155)
+  const uint64_t base = mix64(cfg->seed);
+  e->pool_key = hash2(base, hash2(1, 0));
+  e->env_key = hash2(base, hash2(0, 0));
+  *out = e;
+  return GR_OK;
+}
+
+int64_t gr_obs_elems(const gr_env* e) { return e ? obs_elems_of(e) : 0; }
+int32_t gr_n_actions(const gr_env* e) { return e ? e->d.NA : 0; }
+int32_t gr_n_achievements(const gr_env* e) { return e ? e->d.A : 0; }
+int64_t gr_kernel_launches(const gr_env* e) { return e ? e->launches : 0; }
+
+int gr_set_validate(gr_env* e, int32_t on) {
+  if (!e) return fail(GR_E_INVALID, "null env");
+  e->validate = on != 0;
+  return GR_OK;
+}
+
+int gr_bad_action(const gr_env* e, int64_t* env_index, int64_t* action) {
+  if (!e) return fail(GR_E_INVALID, "null env");
+  if (env_index) *env_index = e->last_bad_env;
+  if (action) *action = e->last_bad_action;
+  return GR_OK;
+}
+
+static int observe(gr_env* e, void* obs_dev, cudaStream_t st, bool recompute_flags) {
+  if (!obs_dev || e->cfg.obs_mode == GR_OBS_NONE) return GR_OK;
+  if (recompute_flags) {
+    CK(cudaMemsetAsync(e->cur_flags, 0, sizeof(uint32_t), st));
+    k_dark<<<(unsigned)e->nb, 128, 0, st>>>(e->S, e->n, e->cur_flags);
+    e->launches++;
+  }
+  ObsArgs oa{obs_dev, e->n, recompute_flags ? e->cur_flags : e->prev_flags, e->cfg.tile_px};
+  if (e->cfg.obs_mode == GR_OBS_SYMBOLIC) launch_symbolic(e->ext, e->S, oa, st);
+  else launch_pixels(e->ext, e->S, oa, st);
+  e->launches++;
+  CK(cudaGetLastError());
+  return GR_OK;
+}
+
+int gr_reset(gr_env* e, void* obs_dev, void* stream) {
+  if (!e) return fail(GR_E_INVALID, "null env");
+  CK(cudaSetDevice(e->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!e->init_meta) {
+    int rc = dev_alloc(e, (void**)&e->init_meta, e->n * sizeof(WMeta));
+    if (rc) return rc;
+  }
+  CK(cudaMemsetAsync(e->init_meta, 0, e->n * sizeof(WMeta), st));
+  // batch_reset: world i = generate_world(make_level_params(split(env_stream, i).key))
+  WorldJob j{};
+  j.mode = 0;
+  j.count = e->n;
+  j.env_key = e->env_key;
+  j.env_offset = e->cfg.env_offset;
+  j.M = e->M;
+  j.out = WBuf{(uint8_t*)e->S.f[GR_F_BLOCKS], (uint8_t*)e->S.f[GR_F_ITEMS], e->init_meta, e->n};
+  j.counters = e->counters;
+  launch_worldgen(e->ext, j, st);
+  launch_install_initial(e->ext, e->S, j.out, e->n, st);
+  e->launches += 2;
+  CK(cudaMemsetAsync(e->prev_flags, 0, sizeof(uint32_t), st));
+  CK(cudaMemsetAsync(e->st_episodes, 0, sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(e->st_steps, 0, sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(e->st_ach, 0, 67 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(e->st_return, 0, sizeof(double), st));
+  CK(cudaGetLastError());
+  e->step_index = 0;
+  e->have_reset = true;
+  return observe(e, obs_dev, st, true);
+}
+
+int gr_random_actions(gr_env* e, uint32_t seed, uint64_t t, int64_t* actions_dev, void* stream) {
+  if (!e || !actions_dev) return fail(GR_E_INVALID, "null argument");
+  const uint32_t key = (uint32_t)((uint64_t)seed + t * 2654435761ull);
+  k_random_actions<<<(unsigned)((e->n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      actions_dev, e->n, e->cfg.env_offset, key, e->d.NA);
+  e->launches++;
+  CK(cudaGetLastError());
+  return GR_OK;
+}
+
+int gr_step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, uint8_t* done_dev, uint8_t* newly_dev,
+                  uint32_t* time_dev, uint8_t* floor_dev, int32_t* exchange_dev, void* stream) {
+  if (!e) return fail(GR_E_INVALID, "null env");
+  if (!e->have_reset) return fail(GR_E_STATE, "call reset() before step()");
+  if (!actions_dev || !reward_dev || !done_dev) return fail(GR_E_INVALID, "actions/reward/done are required");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (e->validate) {
+    CK(cudaMemsetAsync(e->bad, 0xFF, sizeof(unsigned long long), st));
+    k_validate<<<(unsigned)((e->n + 255) / 256), 256, 0, st>>>(actions_dev, e->n, e->d.NA, e->bad);
+    e->launches++;
+    unsigned long long bad = 0;
+    CK(cudaMemcpyAsync(&bad, e->bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (bad != ~0ull) {
+      int64_t a = 0;
+      CK(cudaMemcpy(&a, actions_dev + bad, sizeof(a), cudaMemcpyDeviceToHost));
+      e->last_bad_env = (int64_t)bad;
+      e->last_bad_action = a;
+      return fail(GR_E_BAD_ACTION, "invalid action %lld for env %lld", (long long)a, (long long)bad);
+    }
+  }
+  CK(cudaMemsetAsync(e->cur_flags, 0, sizeof(uint32_t), st));
+  StepArgs a{};
+  a.actions = actions_dev;
+  a.reward = reward_dev;
+  a.done = done_dev;
+  a.newly = newly_dev;
+  a.itime = time_dev;
+  a.ifloor = floor_dev;
+  a.n = e->n;
+  a.max_len = e->cfg.max_episode_length;
+  a.prev_flags = e->prev_flags;
+  a.cur_flags = e->cur_flags;
+  a.block_done = e->block_done;
+  a.bad = nullptr;
+  launch_step(e->ext, e->S, a, st);
+  launch_scan(e->block_done, e->block_off, (int)e->nb, e->cur_flags, exchange_dev ? exchange_dev : e->exchange, st);
+  e->launches += 2;
+  CK(cudaGetLastError());
+  return GR_OK;
+}
+
+int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int32_t world, void* obs_dev,
+                   void* stream) {
+  if (!e) return fail(GR_E_INVALID, "null env");
+  if (world < 1 || rank < 0 || rank >= world) return fail(GR_E_INVALID, "bad rank %d / world %d", rank, world);
+  cudaStream_t st = (cudaStream_t)stream;
+  // WorldPool(pool_key, step_index + 1, M) (batch.py:217)
+  const uint64_t step_key = hash2(e->pool_key, (uint64_t)(e->step_index + 1));
+  launch_finish_info(exchange_all_dev ? exchange_all_dev : e->exchange, rank, world, e->M, step_key, e->info,
+                     e->prev_flags, st);
+  WorldJob j{};
+  j.mode = 1;
+  j.info = e->info;
+  j.M = e->M;
+  j.out = e->pool;
+  j.counters = e->counters;
+  launch_worldgen(e->ext, j, st);
+  InstallArgs ia{};
+  ia.mode = 1;
+  ia.n = e->n;
+  ia.info = e->info;
+  ia.pool = e->pool;
+  ia.M = e->M;
+  ia.st_episodes = e->st_episodes;
+  ia.st_steps = e->st_steps;
+  ia.st_return = e->st_return;
+  ia.st_ach = e->st_ach;
+  launch_install_pool(e->ext, e->S, ia, e->block_off, st);
+  e->launches += 3;
+  CK(cudaGetLastError());
+  e->step_index += 1;
+  return observe(e, obs_dev, st, false);
+}
+
+int gr_step(gr_env* e, const int64_t* actions_dev, void* obs_dev, float* reward_dev, uint8_t* done_dev,
+            uint8_t* newly_dev, uint32_t* time_dev, uint8_t* floor_dev, void* stream) {
+  int rc = gr_step_local(e, actions_dev, reward_dev, done_dev, newly_dev, time_dev, floor_dev, nullptr, stream);
+  if (rc) return rc;
+  return gr_step_finish(e, nullptr, 0, 1, obs_dev, stream);
+}
+
+static int ensure_host_scratch(gr_env* e) {
+  if (e->h_act_dev) return GR_OK;
+  int rc = dev_alloc(e, (void**)&e->h_act_dev, e->n * sizeof(int64_t));
+  if (!rc) rc = dev_alloc(e, (void**)&e->h_rew_dev, e->n * sizeof(float));
+  if (!rc) rc = dev_alloc(e, (void**)&e->h_done_dev, e->n);
+  if (!rc) rc = dev_alloc(e, (void**)&e->h_newly_dev, e->n * e->d.A);
+  if (!rc) rc = dev_alloc(e, (void**)&e->h_time_dev, e->n * sizeof(uint32_t));
+  if (!rc) rc = dev_alloc(e, (void**)&e->h_floor_dev, e->n);
+  const int64_t ob = obs_elems_of(e) * (e->cfg.obs_mode == GR_OBS_PIXELS ? 1 : 4);
+  if (!rc) rc = dev_alloc(e, &e->h_obs_dev, (size_t)ob * e->n);
+  if (!rc) {
+    cudaError_t ce = cudaStreamCreateWithFlags(&e->h_stream, cudaStreamNonBlocking);
+    if (ce != cudaSuccess) return fail(GR_E_CUDA, "stream: %s", cudaGetErrorString(ce));
+  }
+  return rc;
+}
+
+int gr_reset_host(gr_env* e, void* obs_host) {
+  if (!e) return fail(GR_E_INVALID, "null env");
+  CK(cudaSetDevice(e->cfg.device));
+  int rc = ensure_host_scratch(e);
+  if (rc) return rc;
+  rc = gr_reset(e, obs_host ? e->h_obs_dev : nullptr, e->h_stream);
+  if (rc) return rc;
+  const int64_t ob = obs_elems_of(e) * (e->cfg.obs_mode == GR_OBS_PIXELS ? 1 : 4);
+  if (obs_host && ob)
+    CK(cudaMemcpyAsync(obs_host, e->h_obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, e->h_stream));
+  CK(cudaStreamSynchronize(e->h_stream));
+  return GR_OK;
+}
+
+int gr_step_host(gr_env* e, const int64_t* actions_host, void* obs_host, float* reward_host, uint8_t* done_host,
+                 uint8_t* newly_host, uint32_t* time_host, uint8_t* floor_host) {
+  if (!e) return fail(GR_E_INVALID, "null env");
+  if (!e->have_reset) return fail(GR_E_STATE, "call reset() before step()");
+  if (!actions_host) return fail(GR_E_INVALID, "actions are required");
+  CK(cudaSetDevice(e->cfg.device));
+  // validation on the host copy: nothing is mutated on a bad action
+  for (int64_t i = 0; i < e->n; ++i)
+    if (actions_host[i] < 0 || actions_host[i] >= e->d.NA) {
+      e->last_bad_env = i;
+      e->last_bad_action = actions_host[i];
+      return fail(GR_E_BAD_ACTION, "invalid action %lld for env %lld", (long long)actions_host[i], (long long)i);
+    }
+  int rc = ensure_host_scratch(e);
+  if (rc) return rc;
+  cudaStream_t st = e->h_stream;
+  CK(cudaMemcpyAsync(e->h_act_dev, actions_host, e->n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  const bool v = e->validate;
+  e->validate = false;
+  rc = gr_step(e, e->h_act_dev, obs_host ? e->h_obs_dev : nullptr, e->h_rew_dev, e->h_done_dev,
+               newly_host ? e->h_newly_dev : nullptr, time_host ? e->h_time_dev : nullptr,
+               floor_host ? e->h_floor_dev : nullptr, st);
+  e->validate = v;
+  if (rc) return rc;
+  const int64_t ob = obs_elems_of(e) * (e->cfg.obs_mode == GR_OBS_PIXELS ? 1 : 4);
+  if (obs_host && ob) CK(cudaMemcpyAsync(obs_host, e->h_obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, st));
+  if (reward_host) CK(cudaMemcpyAsync(reward_host, e->h_rew_dev, e->n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (done_host) CK(cudaMemcpyAsync(done_host, e->h_done_dev, e->n, cudaMemcpyDeviceToHost, st));
+  if (newly_host) CK(cudaMemcpyAsync(newly_host, e->h_newly_dev, e->n * e->d.A, cudaMemcpyDeviceToHost, st));
+  if (time_host) CK(cudaMemcpyAsync(time_host, e->h_time_dev, e->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  if (floor_host) CK(cudaMemcpyAsync(floor_host, e->h_floor_dev, e->n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return GR_OK;
+}
+
+static int materialize(gr_env* e) {
+  k_materialize<<<(unsigned)e->nb, 128>>>(e->S, e->n, e->d.F, e->prev_flags);
+  e->launches++;
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return GR_OK;
+}
+
+int gr_export_field(gr_env* e, int32_t field, void* host_dst) {
+  if (!e || !host_dst) return fail(GR_E_INVALID, "null argument");
+  if (field < 0 || field >= GR_NFIELDS) return fail(GR_E_INVALID, "unknown field id %d", field);
+  CK(cudaSetDevice(e->cfg.device));
+  int rc = materialize(e);
+  if (rc) return rc;
+  const FieldDesc& fd = FIELD_TABLE[field];
+  const int64_t comps = device_comps(field, e->d);
+  const size_t bytes = (size_t)comps * e->n * fd.esz;
+  if (fd.kind == K_MAP) {
+    CK(cudaMemcpy(host_dst, e->S.f[field], bytes, cudaMemcpyDeviceToHost));
+    return GR_OK;
+  }
+  std::vector<uint8_t> tmp(bytes);
+  CK(cudaMemcpy(tmp.data(), e->S.f[field], bytes, cudaMemcpyDeviceToHost));
+  uint8_t* dst = (uint8_t*)host_dst;
+  if (fd.kind == K_ACH) {
+    const uint32_t* w = (const uint32_t*)tmp.data();
+    for (int64_t i = 0; i < e->n; ++i)
+      for (int a = 0; a < e->d.A; ++a) dst[i * e->d.A + a] = (w[(size_t)(a >> 5) * e->n + i] >> (a & 31)) & 1u;
+    return GR_OK;
+  }
+  const int es = fd.esz;
+  for (int64_t c = 0; c < comps; ++c)
+    for (int64_t i = 0; i < e->n; ++i)
+      memcpy(dst + ((size_t)i * comps + c) * es, tmp.data() + ((size_t)c * e->n + i) * es, es);
+  return GR_OK;
+}
+
+int gr_import_field(gr_env* e, int32_t field, const void* host_src) {
+  if (!e || !host_src) return fail(GR_E_INVALID, "null argument");
+  if (field < 0 || field >= GR_NFIELDS) return fail(GR_E_INVALID, "unknown field id %d", field);
+  CK(cudaSetDevice(e->cfg.device));
+  int rc = materialize(e);
+  if (rc) return rc;
+  const FieldDesc& fd = FIELD_TABLE[field];
+  const int64_t comps = device_comps(field, e->d);
+  const size_t bytes = (size_t)comps * e->n * fd.esz;
+  e->have_reset = true;
+  if (fd.kind == K_MAP) {
+    CK(cudaMemcpy(e->S.f[field], host_src, bytes, cudaMemcpyHostToDevice));
+    return GR_OK;
+  }
+  std::vector<uint8_t> tmp(bytes);
+  const uint8_t* src = (const uint8_t*)host_src;
+  if (fd.kind == K_ACH) {
+    uint32_t* w = (uint32_t*)tmp.data();
+    memset(w, 0, bytes);
+    for (int64_t i = 0; i < e->n; ++i)
+      for (int a = 0; a < e->d.A; ++a)
+        if (src[i * e->d.A + a]) w[(size_t)(a >> 5) * e->n + i] |= 1u << (a & 31);
+  } else {
+    const int es = fd.esz;
+    for (int64_t c = 0; c < comps; ++c)
+      for (int64_t i = 0; i < e->n; ++i)
+        memcpy(tmp.data() + ((size_t)c * e->n + i) * es, src + ((size_t)i * comps + c) * es, es);
+  }
+  CK(cudaMemcpy(e->S.f[field], tmp.data(), bytes, cudaMemcpyHostToDevice));
+  return GR_OK;
+}
+
+int gr_observe(gr_env* e, void* obs_dev, void* stream) {
+  if (!e) return fail(GR_E_INVALID, "null env");
+  CK(cudaSetDevice(e->cfg.device));
+  return observe(e, obs_dev, (cudaStream_t)stream, true);
+}
+
+int gr_stats_get(gr_env* e, gr_stats* out) {
+  if (!e || !out) return fail(GR_E_INVALID, "null argument");
+  CK(cudaSetDevice(e->cfg.device));
+  CK(cudaDeviceSynchronize());
+  unsigned long long ep = 0, steps = 0, ach[67] = {0};
+  double ret = 0;
+  CK(cudaMemcpy(&ep, e->st_episodes, sizeof(ep), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&steps, e->st_steps, sizeof(steps), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&ret, e->st_return, sizeof(ret), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(ach, e->st_ach, sizeof(ach), cudaMemcpyDeviceToHost));
+  memset(out, 0, sizeof(*out));
+  out->episodes = (int64_t)ep;
+  out->total_steps = (int64_t)steps;
+  out->total_return = ret;
+  for (int a = 0; a < 67; ++a) out->ach_episodes[a] = (int64_t)ach[a];
+  return GR_OK;
+}
+
+int gr_episodes_completed(gr_env* e, int64_t* out) {
+  if (!e || !out) return fail(GR_E_INVALID, "null argument");
+  unsigned long long ep = 0;
+  CK(cudaMemcpy(&ep, e->st_episodes, sizeof(ep), cudaMemcpyDeviceToHost));
+  *out = (int64_t)ep;
+  return GR_OK;
+}
+
+int gr_level_seeds(gr_env* e, uint64_t* host_dst) { return gr_export_field(e, GR_F_PARAMS_SEED, host_dst); }
+
+int gr_worldgen_counters(gr_env* e, int64_t out[5]) {
+  if (!e || !out) return fail(GR_E_INVALID, "null argument");
+  unsigned long long c[5];
+  CK(cudaMemcpy(c, e->counters, sizeof(c), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < 5; ++k) out[k] = (int64_t)c[k];
+  return GR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// gr_kernels.cuh -- kernel argument blocks and host-side launchers.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "gr_state.cuh"
+
+namespace gr {
+
+struct StepArgs {
+  const int64_t* actions;   // int64[n]
+  float* reward;            // float32[n]
+  double* reward64;         // optional float64[n]
+  uint8_t* done;            // uint8[n]
+  uint8_t* newly;           // optional uint8[n, A]
+  uint32_t* itime;          // optional
+  uint8_t* ifloor;          // optional
+  int64_t n;
+  int64_t max_len;
+  const uint32_t* prev_flags;  // batch-wide flags of the previous step
+  uint32_t* cur_flags;         // this step: bit0 melee alive, bit1 ranged alive, bit2 dark floor
+  int32_t* block_done;         // done count per 128-env block
+  const int64_t* bad;          // >=0: validation failed, do nothing
+};
+
+// step bookkeeping shared by the post-step kernels (device memory)
+struct StepInfo {
+  int32_t k_local;      // done envs of this shard
+  int32_t offset;       // global rank of this shard's first done env
+  int32_t n_pool;       // worlds to generate = min(k_local, M)
+  int32_t pad;
+  uint32_t flags;       // OR over ranks of cur_flags
+  uint32_t pad2;
+  uint64_t step_key;    // WorldPool._step_key of the pool serving this step
+};
+
+struct WorldJob {
+  int mode;               // 0: initial reset (env-indexed seeds), 1: pool
+  int64_t count;          // worlds (mode 0: n envs; mode 1: read from info->n_pool)
+  const StepInfo* info;   // mode 1
+  uint64_t env_key;       // mode 0: split(make_stream(seed), 0).key
+  int64_t env_offset;     // mode 0: global index of env 0
+  int64_t M;              // pool size (mode 1)
+  WBuf out;
+  unsigned long long* counters;  // [5] diagnostics
+};
+
+struct InstallArgs {
+  int mode;                   // 0: initial (world w -> env w, maps already in place), 1: pool
+  int64_t n;                  // mode 0 env count
+  const int64_t* done_list;   // mode 1: env index per local done rank
+  const StepInfo* info;
+  WBuf pool;
+  int64_t M;
+  // EpisodeStats accumulators (batch.py:109-124)
+  unsigned long long* st_episodes;
+  unsigned long long* st_steps;
+  double* st_return;
+  unsigned long long* st_ach;    // [A]
+};
+
+struct ObsArgs {
+  void* out;                // float32[n, L] or uint8[n, H, W, 3]
+  int64_t n;
+  const uint32_t* flags;    // bit2: some env stands on a dark floor (glow on)
+  int tile_px;
+};
+
+void launch_step(bool ext, const DS& S, const StepArgs& a, cudaStream_t st);
+void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st);
+void launch_install(bool ext, const DS& S, const InstallArgs& a, int64_t grid_envs, cudaStream_t st);
+void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st);
+void launch_pixels(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st);
+
+}  // namespace gr

@@ -1,0 +1,398 @@
+// gr_obs.cu -- observation rendering: the symbolic one-hot vector
+// (obs.encode_symbolic_batch, obs.py:191-386) and the RGB tile frame
+// (tiles.render_tiles, tiles.py:85-186), one warp per environment.
+//
+// Per env the warp first builds the egocentric view in shared memory
+// (block / item / creature channel and light per tile: obs.view_window,
+// light_window, _creature_channel_grid) and the scaled inventory, then
+// streams the row out: each lane writes consecutive 16-byte vectors, so a
+// warp instruction covers 512 contiguous bytes and every obs byte is
+// written exactly once (write-only, no read-for-ownership of the output).
+#include <cstdint>
+#include <algorithm>
+#include "gr_device.cuh"
+#include "gr_state.cuh"
+#include "gr_kernels.cuh"
+
+namespace gr {
+
+template <bool EXT>
+struct OT {
+  static constexpr int F = EXT ? 9 : 1, H = EXT ? 48 : 64, W = H, HW = H * W;
+  static constexpr int VR = EXT ? 9 : 7, VC = EXT ? 11 : 9, T = VR * VC;
+  static constexpr int BCH = EXT ? 37 : 15, ICH = EXT ? 5 : 0, CCH = EXT ? 36 : 5;
+  static constexpr int STRIDE = BCH + ICH + CCH + 1;
+  static constexpr int L = EXT ? 8268 : 1345;
+  static constexpr int NINV = EXT ? 50 : 18;
+};
+
+constexpr int OBS_WARPS = 4;
+
+template <bool EXT>
+struct ViewSmem {
+  uint8_t blk[OT<EXT>::T];     // block id (global)
+  uint8_t itm[OT<EXT>::T];
+  uint8_t cre[OT<EXT>::T];
+  float light[OT<EXT>::T];
+  float inv[OT<EXT>::NINV];
+};
+
+// obs.daylight (obs.py:191-195): float32 with numpy's SIMD sin
+__device__ __forceinline__ float daylight(uint32_t time) {
+  float phase = __fdiv_rn((float)(time % 300u), 300.0f);
+  float m = phase < 0.5f ? phase : 0.5f;
+  float arg = __fmul_rn(__fmul_rn(3.14159274101257324f, m), 2.0f);
+  float lift = np_sincosf(arg, false);
+  return __fadd_rn(0.150000006f, __fmul_rn(0.850000024f, lift > 0.0f ? lift : 0.0f));
+}
+
+__constant__ int8_t C_CLASSIC_LOCAL[37] = {0, 0, 1, 2, 3, 4, 0, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 0, 0,
+                                           0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+
+// build the view of env i into v (whole warp); glow: batch-wide torch flag
+template <bool EXT>
+__device__ void build_view(const DS& S, int64_t i, bool glow, ViewSmem<EXT>& v) {
+  using O = OT<EXT>;
+  const int lane = threadIdx.x & 31;
+  const int pf = EXT ? GR_AT(S, GR_F_PFLOOR, uint8_t, 0, i) : 0;
+  const int pr = GR_AT(S, GR_F_PROW, int16_t, 0, i), pc = GR_AT(S, GR_F_PCOL, int16_t, 0, i);
+  const uint32_t time = GR_AT(S, GR_F_TIME, uint32_t, 0, i);
+  const bool sleeping = GR_AT(S, GR_F_SLEEPING, uint8_t, 0, i);
+  const uint8_t* blk = (const uint8_t*)S.f[GR_F_BLOCKS] + ((size_t)i * O::F + pf) * O::HW;
+  const uint8_t* itm = (const uint8_t*)S.f[GR_F_ITEMS] + ((size_t)i * O::F + pf) * O::HW;
+  const float base = pf == 0 ? daylight(time) : C_FLOOR_AMB[pf];
+  const int r0 = pr - O::VR / 2, c0 = pc - O::VC / 2;
+  for (int t = lane; t < O::T; t += 32) {
+    const int r = r0 + t / O::VC, c = c0 + t % O::VC;
+    const bool inb = r >= 0 && r < O::H && c >= 0 && c < O::W;
+    const uint8_t b = inb ? blk[r * O::W + c] : B_OOB;
+    v.blk[t] = b;
+    v.itm[t] = inb && EXT ? itm[r * O::W + c] : 0;
+    v.cre[t] = 0;
+    v.light[t] = base;
+  }
+  __syncwarp();
+  if (EXT && glow) {
+    // obs._torch_light over the (VR+6)x(VC+6) item window: each torch lights
+    // view tiles within Chebyshev 3 at 1 - d/4
+    constexpr int WR = O::VR + 6, WC = O::VC + 6;
+    for (int t = lane; t < WR * WC; t += 32) {
+      const int wr = t / WC - 3, wc = t % WC - 3;   // view coordinates
+      const int r = r0 + wr, c = c0 + wc;
+      if (r < 0 || r >= O::H || c < 0 || c >= O::W || itm[r * O::W + c] != I_TORCH) continue;
+      for (int a = max(wr - 3, 0); a <= min(wr + 3, O::VR - 1); ++a)
+        for (int b = max(wc - 3, 0); b <= min(wc + 3, O::VC - 1); ++b) {
+          const int d = max(abs(a - wr), abs(b - wc));
+          const float g = 1.0f - 0.25f * (float)d;   // exact: 1, .75, .5, .25
+          atomicMax(reinterpret_cast<int*>(&v.light[a * O::VC + b]), __float_as_int(g));
+        }
+    }
+    __syncwarp();
+  }
+  if (sleeping)
+    for (int t = lane; t < O::T; t += 32) v.light[t] = 0.0f;
+  // creature channels: later lanes overwrite earlier ones (obs.py:263-296)
+  if (lane == 0) {
+    auto paint = [&](int r, int c, bool alive, int ch) {
+      const int wr = r - r0, wc = c - c0;
+      if (alive && wr >= 0 && wr < O::VR && wc >= 0 && wc < O::VC) v.cre[wr * O::VC + wc] = (uint8_t)ch;
+    };
+    const int cls_fid[3] = {GR_F_MEL_POS, GR_F_RAN_POS, GR_F_PAS_POS};
+    const int caps[3] = {3, 2, 3};
+    for (int cls = 0; cls < 3; ++cls) {
+      const int fp = cls_fid[cls], cap = caps[cls];
+      const int fa = cls < 2 ? fp + 3 : fp + 2, ft = cls < 2 ? fp + 4 : fp + 3;
+      for (int l = 0; l < cap; ++l) {
+        const int lanei = pf * cap + l;
+        const int ty = GR_AT(S, ft, uint8_t, lanei, i);
+        int ch;
+        if (EXT) ch = ty + 1;
+        else ch = ty == 0 ? 1 : ty == 2 ? 2 : ty == 1 ? 3 : 0;
+        paint(GR_AT(S, fp, int16_t, 2 * lanei, i), GR_AT(S, fp, int16_t, 2 * lanei + 1, i),
+              GR_AT(S, fa, uint8_t, lanei, i), ch);
+      }
+    }
+    for (int l = 0; l < 3; ++l)
+      paint(GR_AT(S, GR_F_EPROJ_POS, int16_t, 2 * l, i), GR_AT(S, GR_F_EPROJ_POS, int16_t, 2 * l + 1, i),
+            GR_AT(S, GR_F_EPROJ_ALIVE, uint8_t, l, i), EXT ? GR_AT(S, GR_F_EPROJ_TYPE, uint8_t, l, i) + 20 : 4);
+    if (EXT)
+      for (int l = 0; l < 3; ++l)
+        paint(GR_AT(S, GR_F_PPROJ_POS, int16_t, 2 * l, i), GR_AT(S, GR_F_PPROJ_POS, int16_t, 2 * l + 1, i),
+              GR_AT(S, GR_F_PPROJ_ALIVE, uint8_t, l, i), GR_AT(S, GR_F_PPROJ_TYPE, uint8_t, l, i) + 20);
+  }
+  // inventory section (obs._scaled_inventory, obs.py:300-340)
+  for (int k = lane; k < O::NINV; k += 32) {
+    auto sq = [](uint8_t n) { return __fdiv_rn(__fsqrt_rn((float)n), 10.0f); };
+    auto u8 = [&](int fid, int c) { return GR_AT(S, fid, uint8_t, c, i); };
+    auto f32 = [&](int fid) { return GR_AT(S, fid, float, 0, i); };
+    const uint8_t facing = u8(GR_F_FACING, 0);
+    const float day = __fdiv_rn((float)(time % 300u), 300.0f);
+    float x = 0.0f;
+    if (!EXT) {
+      switch (k) {
+        case 0: x = sq(u8(GR_F_INV_WOOD, 0)); break;
+        case 1: x = sq(u8(GR_F_INV_STONE, 0)); break;
+        case 2: x = sq(u8(GR_F_INV_COAL, 0)); break;
+        case 3: x = sq(u8(GR_F_INV_IRON, 0)); break;
+        case 4: x = sq(u8(GR_F_INV_DIAMOND, 0)); break;
+        case 5: x = sq(u8(GR_F_INV_SAPLING, 0)); break;
+        case 6: x = __fdiv_rn((float)u8(GR_F_PICK_TIER, 0), 4.0f); break;
+        case 7: x = __fdiv_rn((float)u8(GR_F_SWORD_TIER, 0), 4.0f); break;
+        case 8: x = __fdiv_rn(f32(GR_F_HEALTH), 10.0f); break;
+        case 9: x = __fdiv_rn(f32(GR_F_FOOD), 10.0f); break;
+        case 10: x = __fdiv_rn(f32(GR_F_DRINK), 10.0f); break;
+        case 11: x = __fdiv_rn(f32(GR_F_ENERGY), 10.0f); break;
+        case 12: case 13: case 14: case 15: x = facing == k - 12 ? 1.0f : 0.0f; break;
+        case 16: x = day; break;
+        default: x = sleeping ? 1.0f : 0.0f; break;
+      }
+    } else {
+      if (k < 10) {
+        const int fids[10] = {GR_F_INV_WOOD, GR_F_INV_STONE, GR_F_INV_COAL, GR_F_INV_IRON, GR_F_INV_DIAMOND,
+                              GR_F_INV_SAPPHIRE, GR_F_INV_RUBY, GR_F_INV_SAPLING, GR_F_INV_TORCH, GR_F_INV_ARROW};
+        x = sq(u8(fids[k], 0));
+      } else if (k < 16) {
+        x = sq(u8(GR_F_INV_POTION, k - 10));
+      } else if (k == 16) {
+        x = __fdiv_rn((float)u8(GR_F_INV_BOOK, 0), 2.0f);
+      } else if (k == 17) {
+        x = __fdiv_rn((float)u8(GR_F_PICK_TIER, 0), 4.0f);
+      } else if (k == 18) {
+        x = __fdiv_rn((float)u8(GR_F_SWORD_TIER, 0), 4.0f);
+      } else if (k == 19) {
+        x = (float)u8(GR_F_SWORD_ENCH, 0);
+      } else if (k == 20) {
+        x = (float)u8(GR_F_HAS_BOW, 0);
+      } else if (k < 25) {
+        x = __fdiv_rn((float)u8(GR_F_ARMOUR, k - 21), 2.0f);
+      } else if (k < 29) {
+        x = (float)u8(GR_F_ARMOUR_ENCH, k - 25);
+      } else if (k < 34) {
+        const int fids[5] = {GR_F_HEALTH, GR_F_FOOD, GR_F_DRINK, GR_F_ENERGY, GR_F_MANA};
+        x = __fdiv_rn(f32(fids[k - 29]), 10.0f);
+      } else if (k < 38) {
+        const int fids[4] = {GR_F_XP, GR_F_DEX, GR_F_STR, GR_F_INTEL};
+        x = __fdiv_rn((float)u8(fids[k - 34], 0), 10.0f);
+      } else if (k < 42) {
+        x = facing == k - 38 ? 1.0f : 0.0f;
+      } else if (k == 42) {
+        x = day;
+      } else if (k == 43) {
+        x = sleeping ? 1.0f : 0.0f;
+      } else if (k == 44) {
+        x = (float)u8(GR_F_RESTING, 0);
+      } else if (k == 45) {
+        x = (float)u8(GR_F_LEARNED_FIRE, 0);
+      } else if (k == 46) {
+        x = (float)u8(GR_F_LEARNED_ICE, 0);
+      } else if (k == 47) {
+        x = __fdiv_rn((float)pf, 10.0f);
+      } else if (k == 48) {
+        x = (float)u8(GR_F_FLOOR_CLEARED, pf);
+      } else {
+        x = (float)u8(GR_F_BOSS_VULN, 0);
+      }
+    }
+    v.inv[k] = x;
+  }
+  __syncwarp();
+}
+
+template <bool EXT>
+__device__ __forceinline__ float sym_value(const ViewSmem<EXT>& v, int p) {
+  using O = OT<EXT>;
+  if (p < O::T * O::STRIDE) {
+    const int t = p / O::STRIDE, ch = p - t * O::STRIDE;
+    const float l = v.light[t];
+    if (ch == O::STRIDE - 1) return l;
+    const bool lit = l >= 0.05f;
+    const int bch = EXT ? v.blk[t] : C_CLASSIC_LOCAL[v.blk[t]];
+    const bool on = ch == bch || (EXT && ch == O::BCH + v.itm[t]) || ch == O::BCH + O::ICH + v.cre[t];
+    return lit && on ? 1.0f : 0.0f;
+  }
+  const int k = p - O::T * O::STRIDE;
+  return k < O::NINV ? v.inv[k] : 0.0f;
+}
+
+template <bool EXT>
+__global__ void __launch_bounds__(OBS_WARPS * 32) k_symbolic(DS S, ObsArgs a) {
+  using O = OT<EXT>;
+  __shared__ ViewSmem<EXT> views[OBS_WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ViewSmem<EXT>& v = views[warp];
+  const bool glow = EXT && a.flags && (a.flags[0] & 4u);
+  for (int64_t i = (int64_t)blockIdx.x * OBS_WARPS + warp; i < a.n; i += (int64_t)gridDim.x * OBS_WARPS) {
+    build_view<EXT>(S, i, glow, v);
+    float* row = (float*)a.out + (size_t)i * O::L;
+    if (EXT) {
+      // 8268 floats = 2067 float4, rows 16-byte aligned
+      float4* r4 = reinterpret_cast<float4*>(row);
+      for (int q = lane; q < O::L / 4; q += 32) {
+        const int p = 4 * q;
+        float4 val = make_float4(sym_value<EXT>(v, p), sym_value<EXT>(v, p + 1), sym_value<EXT>(v, p + 2),
+                                 sym_value<EXT>(v, p + 3));
+        __stcs(r4 + q, val);
+      }
+    } else {
+      for (int p = lane; p < O::L; p += 32) __stcs(row + p, sym_value<EXT>(v, p));
+    }
+    __syncwarp();
+  }
+}
+
+// ----------------------------------------------------------------- pixels
+__constant__ uint8_t C_PALETTE[37][3] = {
+    {0, 0, 0}, {10, 10, 10}, {64, 160, 66}, {48, 92, 190}, {120, 120, 120}, {28, 100, 38}, {134, 97, 55},
+    {160, 140, 110}, {60, 60, 64}, {188, 168, 152}, {130, 220, 228}, {168, 120, 50}, {150, 80, 60},
+    {216, 200, 130}, {230, 90, 16}, {96, 190, 90}, {180, 210, 70}, {84, 78, 76}, {4, 4, 4}, {86, 110, 76},
+    {142, 134, 128}, {60, 110, 230}, {210, 40, 80}, {196, 150, 40}, {110, 170, 220}, {190, 110, 40},
+    {180, 220, 240}, {100, 96, 90}, {150, 60, 20}, {140, 190, 210}, {240, 140, 90}, {150, 200, 255},
+    {90, 20, 120}, {130, 130, 140}, {118, 118, 130}, {106, 106, 120}, {200, 60, 230}};
+__constant__ uint8_t C_ITEMC[5][3] = {{255, 255, 255}, {255, 220, 90}, {20, 20, 25}, {235, 235, 240}, {70, 30, 30}};
+__constant__ uint8_t C_BARC[5][3] = {{220, 60, 60}, {220, 160, 60}, {70, 130, 230}, {240, 230, 90}, {150, 90, 220}};
+__constant__ uint8_t C_GEARC[7][3] = {{200, 200, 210}, {160, 160, 170}, {120, 140, 200}, {240, 220, 90},
+                                      {90, 220, 140}, {220, 90, 90}, {140, 120, 240}};
+
+__device__ __forceinline__ uint32_t creature_rgb(bool ext, int ch) {
+  int kind;
+  if (!ext) {
+    if (ch == 4) return 0xFAFAFAu;
+    kind = ch == 1 ? 0 : ch == 2 ? 2 : 1;
+  } else {
+    if (ch >= 20) return 0xFAFAFAu;
+    kind = ch - 1;
+  }
+  uint32_t r, g, b;
+  if (kind == 0) { r = 80; g = 200; b = 90; }
+  else if (kind == 1) { r = 230; g = 230; b = 215; }
+  else if (kind == 2) { r = 240; g = 190; b = 160; }
+  else { r = 40 + 11 * kind; g = 255 - 12 * kind; b = 60 + 9 * kind; }
+  return (r << 16) | (g << 8) | b;
+}
+
+template <bool EXT>
+struct PixSmem {
+  uint32_t tile_rgb[OT<EXT>::T];   // shaded tile colour
+  uint32_t inset_rgb[OT<EXT>::T];  // 0xFF000000 = none
+  int fill[12];                    // bar fills: 5 strip + 7 side
+};
+
+template <bool EXT>
+__global__ void __launch_bounds__(128) k_pixels(DS S, ObsArgs a) {
+  using O = OT<EXT>;
+  __shared__ ViewSmem<EXT> view;
+  __shared__ PixSmem<EXT> pm;
+  const int px = a.tile_px;
+  const int side = EXT ? 2 : 0;
+  const int FH = (O::VR + 2) * px, FW = (O::VC + side) * px;
+  const int inset = max(1, px / 4);
+  const int64_t frame = (int64_t)FH * FW * 3;
+  for (int64_t i = blockIdx.x; i < a.n; i += gridDim.x) {
+    if (threadIdx.x < 32) {
+      // render_tiles sees a one-env batch: glow iff this env's floor is dark
+      const int pf = EXT ? GR_AT(S, GR_F_PFLOOR, uint8_t, 0, i) : 0;
+      build_view<EXT>(S, i, EXT && C_FLOOR_AMB[pf] < 1.0f, view);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < O::T; t += blockDim.x) {
+      const float l = view.light[t];
+      const float sh = l < 0.0f ? 0.0f : (l > 1.0f ? 1.0f : l);
+      const bool dark = l < 0.05f;
+      const int b = view.blk[t];
+      uint32_t rgb = 0;
+      if (!dark)
+        for (int k = 0; k < 3; ++k)
+          rgb |= (uint32_t)(uint8_t)(int)__fmul_rn((float)C_PALETTE[b][k], sh) << (16 - 8 * k);
+      pm.tile_rgb[t] = rgb;
+      uint32_t ins = 0xFF000000u;
+      if (!dark) {
+        const int it = view.itm[t];
+        if (it) ins = ((uint32_t)C_ITEMC[it][0] << 16) | ((uint32_t)C_ITEMC[it][1] << 8) | C_ITEMC[it][2];
+        if (view.cre[t]) ins = creature_rgb(EXT, view.cre[t]);
+      }
+      if (t == (O::VR / 2) * O::VC + O::VC / 2) ins = 0xFA3C3Cu;   // the player
+      pm.inset_rgb[t] = ins;
+    }
+    if (threadIdx.x == 0) {
+      // vital bars (tiles.py:147-166) and gear panel (:169-186), float64
+      const float str_ = (float)GR_AT(S, GR_F_STR, uint8_t, 0, i), dex = (float)GR_AT(S, GR_F_DEX, uint8_t, 0, i);
+      const float intel = (float)GR_AT(S, GR_F_INTEL, uint8_t, 0, i);
+      const double hmax = (double)__fadd_rn(9.0f, str_), fmax = (double)__fadd_rn(12.0f, dex);
+      double st[5] = {(double)GR_AT(S, GR_F_HEALTH, float, 0, i) / hmax, (double)GR_AT(S, GR_F_FOOD, float, 0, i) / fmax,
+                      (double)GR_AT(S, GR_F_DRINK, float, 0, i) / fmax, (double)GR_AT(S, GR_F_ENERGY, float, 0, i) / fmax,
+                      EXT ? (double)GR_AT(S, GR_F_MANA, float, 0, i) / (double)__fadd_rn(16.0f, intel) : 0.0};
+      const int width = O::VC * px - 2;
+      for (int k = 0; k < 5; ++k) {
+        const double f = st[k] < 0.0 ? 0.0 : (st[k] > 1.0 ? 1.0 : st[k]);
+        pm.fill[k] = (int)rint(__dmul_rn(f, (double)width));
+      }
+      if (EXT) {
+        const int arm = GR_AT(S, GR_F_ARMOUR, uint8_t, 0, i) + GR_AT(S, GR_F_ARMOUR, uint8_t, 1, i) +
+                        GR_AT(S, GR_F_ARMOUR, uint8_t, 2, i) + GR_AT(S, GR_F_ARMOUR, uint8_t, 3, i);
+        double g[7] = {(double)GR_AT(S, GR_F_SWORD_TIER, uint8_t, 0, i) / 4.0,
+                       (double)GR_AT(S, GR_F_PICK_TIER, uint8_t, 0, i) / 4.0, (double)arm / 8.0,
+                       (double)GR_AT(S, GR_F_XP, uint8_t, 0, i) / 8.0, (double)dex / 5.0, (double)str_ / 5.0,
+                       (double)intel / 5.0};
+        for (int k = 0; k < 7; ++k) {
+          const double f = g[k] < 0.0 ? 0.0 : (g[k] > 1.0 ? 1.0 : g[k]);
+          pm.fill[5 + k] = (int)rint(__dmul_rn(f, (double)(2 * px - 2)));
+        }
+      }
+    }
+    __syncthreads();
+    uint8_t* out = (uint8_t*)a.out + (size_t)i * frame;
+    const int ns = EXT ? 5 : 4;
+    const int bar_h = max(2, (2 * px) / (ns + 1));
+    const int y0 = O::VR * px;
+    for (int64_t byte = threadIdx.x; byte < frame; byte += blockDim.x) {
+      const int p = (int)(byte / 3), ch = (int)(byte % 3);
+      const int y = p / FW, x = p % FW;
+      uint32_t rgb = 0;
+      if (y < O::VR * px && x < O::VC * px) {
+        const int t = (y / px) * O::VC + x / px, iy = y % px, ix = x % px;
+        rgb = pm.tile_rgb[t];
+        if (iy >= inset && iy < px - inset && ix >= inset && ix < px - inset && pm.inset_rgb[t] != 0xFF000000u)
+          rgb = pm.inset_rgb[t];
+      } else if (y >= y0 && x < O::VC * px) {
+        const int k = (y - y0 - 1) / bar_h, yy = (y - y0 - 1) % bar_h;
+        if (y - y0 - 1 >= 0 && k < ns && yy < bar_h - 1 && x >= 1 && x < 1 + O::VC * px - 2) {
+          rgb = x < 1 + pm.fill[k]
+                    ? ((uint32_t)C_BARC[k][0] << 16) | ((uint32_t)C_BARC[k][1] << 8) | C_BARC[k][2]
+                    : 0x1E1E1Eu;
+        }
+      } else if (EXT && x >= O::VC * px) {
+        const int k = y / px, yy = y % px, xx = x - O::VC * px;
+        if (k < 7 && k * px + px <= FH && yy >= 1 && yy < px - 1 && xx >= 1 && xx < 2 * px - 1) {
+          rgb = xx < 1 + pm.fill[5 + k]
+                    ? ((uint32_t)C_GEARC[k][0] << 16) | ((uint32_t)C_GEARC[k][1] << 8) | C_GEARC[k][2]
+                    : 0x1E1E1Eu;
+        }
+      }
+      out[byte] = (uint8_t)(rgb >> (16 - 8 * ch));
+    }
+    __syncthreads();
+  }
+}
+
+void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t need = (a.n + OBS_WARPS - 1) / OBS_WARPS;
+  const int grid = (int)std::min<int64_t>(need, (int64_t)sms * 16);
+  if (ext) k_symbolic<true><<<grid, OBS_WARPS * 32, 0, st>>>(S, a);
+  else k_symbolic<false><<<grid, OBS_WARPS * 32, 0, st>>>(S, a);
+}
+
+void launch_pixels(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>(a.n, (int64_t)sms * 16);
+  if (ext) k_pixels<true><<<grid, 128, 0, st>>>(S, a);
+  else k_pixels<false><<<grid, 128, 0, st>>>(S, a);
+}
+
+}  // namespace gr

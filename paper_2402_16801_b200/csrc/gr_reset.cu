@@ -1,0 +1,246 @@
+// gr_reset.cu -- optimistic auto-reset: done-rank scan, pool bookkeeping and
+// world install.
+//
+// batch.batch_step (batch.py:216-231): the pool serving step s is
+// WorldPool(pool_key, s + 1, M); done envs, in ascending global env order,
+// take slot rank % M; install_worlds (state.py:198-249) resets each one.
+// Worlds are generated only for the slots this shard consumes
+// (gr_world.cu); pool entry p holds slot (offset + p) % M, so the env of
+// local done rank r installs entry r % M.
+#include <cstdint>
+#include <algorithm>
+#include "gr_device.cuh"
+#include "gr_state.cuh"
+#include "gr_kernels.cuh"
+
+namespace gr {
+
+// exclusive scan of per-block done counts (one CTA), + exchange record
+__global__ void __launch_bounds__(1024) k_scan(const int32_t* block_done, int32_t* block_off, int nb,
+                                                const uint32_t* cur_flags, int32_t* exchange) {
+  __shared__ int32_t warp_tot[32];
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < nb ? block_done[i] : 0;
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) >= o) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int w = warp_tot[threadIdx.x];
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (threadIdx.x >= o) w += y;
+      }
+      warp_tot[threadIdx.x] = w;
+    }
+    __syncthreads();
+    const int wpre = (threadIdx.x >> 5) ? warp_tot[(threadIdx.x >> 5) - 1] : 0;
+    if (i < nb) block_off[i] = carry + wpre + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_tot[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    exchange[0] = carry;
+    exchange[1] = (int32_t)cur_flags[0];
+    exchange[2] = 0;
+    exchange[3] = 0;
+  }
+}
+
+// combine the all-gathered exchange records of every rank
+__global__ void k_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t step_key,
+                              StepInfo* info, uint32_t* flags_out) {
+  int off = 0;
+  uint32_t fl = 0;
+  for (int r = 0; r < world; ++r) {
+    if (r < rank) off += ex_all[4 * r];
+    fl |= (uint32_t)ex_all[4 * r + 1];
+  }
+  const int k = ex_all[4 * rank];
+  info->k_local = k;
+  info->offset = off;
+  info->n_pool = (int32_t)(k < M ? k : M);
+  info->flags = fl;
+  info->step_key = step_key;
+  *flags_out = fl;
+}
+
+// install_worlds for one env (state.py:198-249); all threads of the CTA
+template <bool EXT>
+__device__ void install_one(const DS& S, int64_t i, const WMeta& m, const uint8_t* src_blk, const uint8_t* src_itm) {
+  constexpr int F = EXT ? 9 : 1, H = EXT ? 48 : 64, W = H, HW = H * W;
+  // maps (16-byte vectors)
+  if (src_blk) {
+    uint4* db = reinterpret_cast<uint4*>((uint8_t*)S.f[GR_F_BLOCKS] + (size_t)i * F * HW);
+    uint4* di = reinterpret_cast<uint4*>((uint8_t*)S.f[GR_F_ITEMS] + (size_t)i * F * HW);
+    const uint4* sb = reinterpret_cast<const uint4*>(src_blk);
+    const uint4* si = reinterpret_cast<const uint4*>(src_itm);
+    for (int q = threadIdx.x; q < F * HW / 16; q += blockDim.x) {
+      db[q] = sb[q];
+      di[q] = si[q];
+    }
+  }
+  // per-floor lanes and chests: spread over threads
+#define Z(fid, T_, c) GR_AT(S, fid, T_, c, i) = (T_)0
+  for (int c = threadIdx.x; c < F * 6; c += blockDim.x) {
+    const int f = c / 6, j = c % 6;
+    const bool has = EXT && j < m.nch[f];
+    GR_AT(S, GR_F_CHEST_POS, int16_t, 2 * c, i) = has ? m.chest[f][j][0] : (int16_t)-1;
+    GR_AT(S, GR_F_CHEST_POS, int16_t, 2 * c + 1, i) = has ? m.chest[f][j][1] : (int16_t)-1;
+    GR_AT(S, GR_F_CHEST_LOOT, uint8_t, c, i) = has ? (uint8_t)m.chest[f][j][2] : (uint8_t)0;
+    GR_AT(S, GR_F_CHEST_QTY, uint8_t, c, i) = has ? (uint8_t)m.chest[f][j][3] : (uint8_t)0;
+    GR_AT(S, GR_F_CHEST_AUX, uint8_t, c, i) = has ? (uint8_t)(hash2(m.key, 800 + (uint64_t)c) % 6) : (uint8_t)0;
+  }
+  for (int c = threadIdx.x; c < F * 3; c += blockDim.x) {
+    Z(GR_F_MEL_POS, int16_t, 2 * c); Z(GR_F_MEL_POS, int16_t, 2 * c + 1);
+    Z(GR_F_MEL_HP, float, c); Z(GR_F_MEL_CD, uint8_t, c); Z(GR_F_MEL_ALIVE, uint8_t, c); Z(GR_F_MEL_TYPE, uint8_t, c);
+    Z(GR_F_PAS_POS, int16_t, 2 * c); Z(GR_F_PAS_POS, int16_t, 2 * c + 1);
+    Z(GR_F_PAS_HP, float, c); Z(GR_F_PAS_ALIVE, uint8_t, c); Z(GR_F_PAS_TYPE, uint8_t, c);
+  }
+  for (int c = threadIdx.x; c < F * 2; c += blockDim.x) {
+    Z(GR_F_RAN_POS, int16_t, 2 * c); Z(GR_F_RAN_POS, int16_t, 2 * c + 1);
+    Z(GR_F_RAN_HP, float, c); Z(GR_F_RAN_CD, uint8_t, c); Z(GR_F_RAN_ALIVE, uint8_t, c); Z(GR_F_RAN_TYPE, uint8_t, c);
+  }
+  for (int f = threadIdx.x; f < F; f += blockDim.x) {
+    GR_AT(S, GR_F_LADDER_DOWN, int16_t, 2 * f, i) = m.ld[f][0];
+    GR_AT(S, GR_F_LADDER_DOWN, int16_t, 2 * f + 1, i) = m.ld[f][1];
+    GR_AT(S, GR_F_LADDER_UP, int16_t, 2 * f, i) = m.lu[f][0];
+    GR_AT(S, GR_F_LADDER_UP, int16_t, 2 * f + 1, i) = m.lu[f][1];
+    GR_AT(S, GR_F_FLOORS_VISITED, uint8_t, f, i) = f == 0;
+    GR_AT(S, GR_F_FLOOR_CLEARED, uint8_t, f, i) = 0;
+  }
+  for (int l = threadIdx.x; l < 10; l += blockDim.x) {
+    Z(GR_F_PLANT_POS, int16_t, 2 * l); Z(GR_F_PLANT_POS, int16_t, 2 * l + 1);
+    Z(GR_F_PLANT_AGE, uint16_t, l); Z(GR_F_PLANT_ALIVE, uint8_t, l);
+  }
+  for (int l = threadIdx.x; l < 3; l += blockDim.x) {
+    Z(GR_F_PPROJ_POS, int16_t, 2 * l); Z(GR_F_PPROJ_POS, int16_t, 2 * l + 1);
+    Z(GR_F_PPROJ_DIR, uint8_t, l); Z(GR_F_PPROJ_TYPE, uint8_t, l); Z(GR_F_PPROJ_TTL, uint8_t, l);
+    Z(GR_F_PPROJ_ALIVE, uint8_t, l);
+    Z(GR_F_EPROJ_POS, int16_t, 2 * l); Z(GR_F_EPROJ_POS, int16_t, 2 * l + 1);
+    Z(GR_F_EPROJ_DIR, uint8_t, l); Z(GR_F_EPROJ_TYPE, uint8_t, l); Z(GR_F_EPROJ_TTL, uint8_t, l);
+    Z(GR_F_EPROJ_ALIVE, uint8_t, l);
+    for (int k = 0; k < 3; ++k) { Z(GR_F_PPROJ_DMG, float, 3 * l + k); Z(GR_F_EPROJ_DMG, float, 3 * l + k); }
+  }
+  for (int k = threadIdx.x; k < 6; k += blockDim.x) {
+    GR_AT(S, GR_F_POTION_MAP, uint8_t, k, i) = m.potion[k];
+    Z(GR_F_INV_POTION, uint8_t, k);
+    Z(GR_F_CLOCKS, uint16_t, k);
+  }
+  if (threadIdx.x == 0) {
+    GR_AT(S, GR_F_SPAWN0, int16_t, 0, i) = m.spawn[0];
+    GR_AT(S, GR_F_SPAWN0, int16_t, 1, i) = m.spawn[1];
+    GR_AT(S, GR_F_PARAMS_SEED, uint64_t, 0, i) = m.seed;
+    GR_AT(S, GR_F_PROW, int16_t, 0, i) = m.spawn[0];
+    GR_AT(S, GR_F_PCOL, int16_t, 0, i) = m.spawn[1];
+    if (EXT) {
+      GR_AT(S, GR_F_NECRO_POS, int16_t, 0, i) = (int16_t)(H / 2 - 6);
+      GR_AT(S, GR_F_NECRO_POS, int16_t, 1, i) = (int16_t)(W / 2);
+    }
+    GR_AT(S, GR_F_FACING, uint8_t, 0, i) = 3;
+    GR_AT(S, GR_F_DEX, uint8_t, 0, i) = 1;
+    GR_AT(S, GR_F_STR, uint8_t, 0, i) = 1;
+    GR_AT(S, GR_F_INTEL, uint8_t, 0, i) = 1;
+    Z(GR_F_XP, uint8_t, 0); Z(GR_F_SWORD_TIER, uint8_t, 0); Z(GR_F_PICK_TIER, uint8_t, 0);
+    Z(GR_F_HAS_BOW, uint8_t, 0); Z(GR_F_SWORD_ENCH, uint8_t, 0); Z(GR_F_BOW_ENCH, uint8_t, 0);
+    Z(GR_F_LEARNED_FIRE, uint8_t, 0); Z(GR_F_LEARNED_ICE, uint8_t, 0);
+    Z(GR_F_SLEEPING, uint8_t, 0); Z(GR_F_RESTING, uint8_t, 0);
+    for (int fid = GR_F_INV_WOOD; fid <= GR_F_INV_BOOK; ++fid) GR_AT(S, fid, uint8_t, 0, i) = 0;
+    for (int k = 0; k < 4; ++k) { Z(GR_F_ARMOUR, uint8_t, k); Z(GR_F_ARMOUR_ENCH, uint8_t, k); }
+    for (int k = 0; k < 3; ++k) Z(GR_F_ACH, uint32_t, k);
+    Z(GR_F_TIME, uint32_t, 0);
+    Z(GR_F_BOSS_WAVE, uint8_t, 0); Z(GR_F_BOSS_VULN, uint8_t, 0); Z(GR_F_BOSS_TIMER, uint8_t, 0);
+    Z(GR_F_DONE, uint8_t, 0);
+    Z(GR_F_PFLOOR, uint8_t, 0);
+    GR_AT(S, GR_F_HEALTH, float, 0, i) = 10.0f;
+    GR_AT(S, GR_F_FOOD, float, 0, i) = 13.0f;
+    GR_AT(S, GR_F_DRINK, float, 0, i) = 13.0f;
+    GR_AT(S, GR_F_ENERGY, float, 0, i) = 13.0f;
+    GR_AT(S, GR_F_MANA, float, 0, i) = 17.0f;
+    GR_AT(S, GR_F_RNG_KEY, uint64_t, 0, i) = m.key;
+    GR_AT(S, GR_F_BOSS_HP, float, 0, i) = EXT ? 60.0f : 0.0f;
+    S.cd_pending[i] = 0;
+    S.ep_return[i] = 0.0;
+    S.ep_length[i] = 0;
+  }
+#undef Z
+}
+
+// initial reset: world w was generated straight into env w's maps
+template <bool EXT>
+__global__ void __launch_bounds__(128) k_install_initial(DS S, WBuf wb, int64_t n) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) install_one<EXT>(S, i, wb.meta[i], nullptr, nullptr);
+}
+
+// auto-reset: each CTA owns 128 consecutive envs; done envs get their
+// global rank from the block scan, record EpisodeStats, then install.
+template <bool EXT>
+__global__ void __launch_bounds__(128) k_install_pool(DS S, InstallArgs a, const int32_t* block_off) {
+  constexpr int F = EXT ? 9 : 1, HW = EXT ? 48 * 48 : 64 * 64, A = EXT ? 67 : 22;
+  __shared__ int32_t list[128];
+  __shared__ int cnt;
+  const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const bool d = i < a.n && GR_AT(S, GR_F_DONE, uint8_t, 0, i);
+  const unsigned bal = __ballot_sync(0xffffffffu, d);
+  __shared__ int wcnt[4];
+  if ((threadIdx.x & 31) == 0) wcnt[threadIdx.x >> 5] = __popc(bal);
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int pre = 0;
+  for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) pre += wcnt[w];
+  const int local = pre + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
+  if (d) list[local] = threadIdx.x;
+  if (threadIdx.x == 0) cnt = wcnt[0] + wcnt[1] + wcnt[2] + wcnt[3];
+  __syncthreads();
+  const int n_here = cnt;
+  const int base_rank = block_off[blockIdx.x];
+  for (int q = 0; q < n_here; ++q) {
+    const int64_t env = (int64_t)blockIdx.x * 128 + list[q];
+    const int64_t r = base_rank + q;             // local done rank
+    const int64_t p = r % a.M;                   // pool entry
+    if (threadIdx.x == 0) {
+      atomicAdd(a.st_episodes, 1ull);
+      atomicAdd(a.st_steps, (unsigned long long)S.ep_length[env]);
+      atomicAdd(a.st_return, S.ep_return[env]);
+    }
+    for (int k = threadIdx.x; k < A; k += blockDim.x)
+      if ((GR_AT(S, GR_F_ACH, uint32_t, k >> 5, env) >> (k & 31)) & 1u) atomicAdd(&a.st_ach[k], 1ull);
+    __syncthreads();
+    install_one<EXT>(S, env, a.pool.meta[p], a.pool.blocks + (size_t)p * F * HW, a.pool.items + (size_t)p * F * HW);
+    __syncthreads();
+  }
+}
+
+void launch_scan(const int32_t* block_done, int32_t* block_off, int nb, const uint32_t* cur_flags, int32_t* exchange,
+                 cudaStream_t st) {
+  k_scan<<<1, 1024, 0, st>>>(block_done, block_off, nb, cur_flags, exchange);
+}
+
+void launch_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t step_key, StepInfo* info,
+                        uint32_t* flags_out, cudaStream_t st) {
+  k_finish_info<<<1, 1, 0, st>>>(ex_all, rank, world, M, step_key, info, flags_out);
+}
+
+void launch_install_initial(bool ext, const DS& S, const WBuf& wb, int64_t n, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>(n, 148 * 16);
+  if (grid <= 0) return;
+  if (ext) k_install_initial<true><<<grid, 128, 0, st>>>(S, wb, n);
+  else k_install_initial<false><<<grid, 128, 0, st>>>(S, wb, n);
+}
+
+void launch_install_pool(bool ext, const DS& S, const InstallArgs& a, const int32_t* block_off, cudaStream_t st) {
+  const int grid = (int)((a.n + 127) / 128);
+  if (grid <= 0) return;
+  if (ext) k_install_pool<true><<<grid, 128, 0, st>>>(S, a, block_off);
+  else k_install_pool<false><<<grid, 128, 0, st>>>(S, a, block_off);
+}
+
+}  // namespace gr

@@ -1,0 +1,884 @@
+// gr_world.cu -- procedural world generation on device, one CTA per
+// (world, floor), staged in shared memory.
+//
+// Restates worldgen.py (and perlin.py) per floor:
+//   floor 0   overworld  worldgen.py:181-327  (+ make_level_params :75-87)
+//   1, 3, 4   dungeon    worldgen.py:367-406
+//   2, 5      cave       worldgen.py:418-468  (float64 noise)
+//   6, 7      realm      worldgen.py:479-520
+//   8         graveyard  worldgen.py:523-546
+//   fallback  template   worldgen.py:549-575 after 16 failed attempts (:578-595)
+//   chests    worldgen.py:598-633, potion permutation :647-649
+// The per-tile work (noise, thresholds, sprinkles) is spread over the
+// 256 threads; every argmax/argmin of the reference becomes a block
+// reduction with numpy's first-index tie-break; the inherently sequential
+// parts (room RNG chain, L-corridors, chest picks) run on thread 0.
+#include <cstdint>
+#include <climits>
+#include <algorithm>
+#include "gr_device.cuh"
+#include "gr_state.cuh"
+#include "gr_kernels.cuh"
+
+namespace gr {
+
+constexpr int WG_THREADS = 256;
+constexpr double PI_D = 3.141592653589793;
+
+template <bool EXT>
+struct WT {
+  static constexpr int H = EXT ? 48 : 64, W = H, HW = H * W, F = EXT ? 9 : 1;
+  static constexpr int PER = (HW + WG_THREADS - 1) / WG_THREADS;   // tiles per thread
+};
+
+template <bool EXT>
+struct WSmem {
+  alignas(16) uint8_t blk[WT<EXT>::HW];
+  alignas(16) uint8_t itm[WT<EXT>::HW];
+  union {
+    float h32[WT<EXT>::HW];      // overworld height
+    double f64[EXT ? WT<EXT>::HW : 1];  // cave field
+  };
+  float u[WT<EXT>::HW];          // hashed per-tile uniforms
+  float gx[252], gy[252];        // overworld gradients
+  double dgx[EXT ? 106 : 1], dgy[EXT ? 106 : 1];  // cave gradients
+  float prof[2][8][32];          // [coarse/fine][a1..a4,b0..b3][i]
+  double dprof[EXT ? 2 : 1][8][12];
+  float ang[252];
+  // reductions
+  float rf[32];
+  double rd[32];
+  int ri[32];
+  unsigned long long ru[32];
+  int res_i;
+  unsigned long long res_u;
+  int fail;
+  int spawn;
+  int cr[8], cc[8], nrooms;
+  int rowcnt[64];
+  int tmp[8];
+};
+
+// ------------------------------------------------------- block reductions
+template <class SM>
+__device__ int block_argmax_f(SM& sm, float v, int idx) {   // idx = INT_MAX: no candidate
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_down_sync(0xffffffffu, v, o);
+    int oi = __shfl_down_sync(0xffffffffu, idx, o);
+    if (oi != INT_MAX && (idx == INT_MAX || ov > v || (ov == v && oi < idx))) { v = ov; idx = oi; }
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { sm.rf[w] = v; sm.ri[w] = idx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float bv = sm.rf[0];
+    int bi = sm.ri[0];
+    for (int k = 1; k < WG_THREADS / 32; ++k) {
+      int oi = sm.ri[k];
+      float ov = sm.rf[k];
+      if (oi != INT_MAX && (bi == INT_MAX || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+    }
+    sm.res_i = bi == INT_MAX ? -1 : bi;
+  }
+  __syncthreads();
+  int r = sm.res_i;
+  __syncthreads();
+  return r;
+}
+
+template <class SM>
+__device__ int block_argmax_d(SM& sm, double v, int idx) {
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_down_sync(0xffffffffu, v, o);
+    int oi = __shfl_down_sync(0xffffffffu, idx, o);
+    if (oi != INT_MAX && (idx == INT_MAX || ov > v || (ov == v && oi < idx))) { v = ov; idx = oi; }
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { sm.rd[w] = v; sm.ri[w] = idx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bv = sm.rd[0];
+    int bi = sm.ri[0];
+    for (int k = 1; k < WG_THREADS / 32; ++k) {
+      int oi = sm.ri[k];
+      double ov = sm.rd[k];
+      if (oi != INT_MAX && (bi == INT_MAX || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+    }
+    sm.res_i = bi == INT_MAX ? -1 : bi;
+  }
+  __syncthreads();
+  int r = sm.res_i;
+  __syncthreads();
+  return r;
+}
+
+template <class SM>
+__device__ unsigned long long block_min_u64(SM& sm, unsigned long long v) {
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long ov = __shfl_down_sync(0xffffffffu, v, o);
+    v = ov < v ? ov : v;
+  }
+  if ((threadIdx.x & 31) == 0) sm.ru[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long b = sm.ru[0];
+    for (int k = 1; k < WG_THREADS / 32; ++k) b = sm.ru[k] < b ? sm.ru[k] : b;
+    sm.res_u = b;
+  }
+  __syncthreads();
+  unsigned long long r = sm.res_u;
+  __syncthreads();
+  return r;
+}
+
+template <class SM>
+__device__ unsigned long long block_or_u64(SM& sm, unsigned long long v) {
+  for (int o = 16; o > 0; o >>= 1) v |= __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sm.ru[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long b = 0;
+    for (int k = 0; k < WG_THREADS / 32; ++k) b |= sm.ru[k];
+    sm.res_u = b;
+  }
+  __syncthreads();
+  unsigned long long r = sm.res_u;
+  __syncthreads();
+  return r;
+}
+
+template <bool EXT>
+__device__ unsigned long long census(WSmem<EXT>& sm) {
+  unsigned long long m = 0;
+  for (int t = threadIdx.x; t < WT<EXT>::HW; t += WG_THREADS) m |= 1ull << sm.blk[t];
+  return block_or_u64(sm, m);
+}
+
+__device__ __forceinline__ int cheb(int r0, int c0, int r1, int c1) { return max(abs(r0 - r1), abs(c0 - c1)); }
+
+// argmax of u over tiles satisfying pred(t) (worldgen._pick_tile)
+template <bool EXT, class P>
+__device__ int pick_u(WSmem<EXT>& sm, const float* score, P pred) {
+  float bv = 0.0f;
+  int bi = INT_MAX;
+  for (int t = threadIdx.x; t < WT<EXT>::HW; t += WG_THREADS)
+    if (pred(t) && (bi == INT_MAX || score[t] > bv)) { bv = score[t]; bi = t; }
+  return block_argmax_f(sm, bv, bi);
+}
+
+// ------------------------------------------------------------ noise
+// perlin._profiles (perlin.py:36-51) for both octave sizes, float32
+template <bool EXT>
+__device__ void build_profiles_f32(WSmem<EXT>& sm) {
+  const int H = WT<EXT>::H;
+  const int dims[2] = {H / 2, H / 8};
+  for (int k = threadIdx.x; k < 2 * 32; k += WG_THREADS) {
+    const int o = k / 32, i = k % 32, d = dims[o];
+    if (i >= d) continue;
+    float f = __fdiv_rn((float)i, (float)d);
+    float u = __fmul_rn(__fmul_rn(__fmul_rn(f, f), f),
+                        __fadd_rn(__fmul_rn(f, __fsub_rn(__fmul_rn(f, 6.0f), 15.0f)), 10.0f));
+    const float one = 1.0f, root2 = 1.41421353816986083984375f;
+    sm.prof[o][0][i] = __fsub_rn(one, u);
+    sm.prof[o][1][i] = __fmul_rn(__fsub_rn(one, u), f);
+    sm.prof[o][2][i] = u;
+    sm.prof[o][3][i] = __fmul_rn(u, __fsub_rn(f, one));
+    sm.prof[o][4][i] = __fmul_rn(__fmul_rn(__fsub_rn(one, u), f), root2);
+    sm.prof[o][5][i] = __fmul_rn(__fsub_rn(one, u), root2);
+    sm.prof[o][6][i] = __fmul_rn(__fmul_rn(u, __fsub_rn(f, one)), root2);
+    sm.prof[o][7][i] = __fmul_rn(u, root2);
+  }
+}
+
+// one octave value at tile (r, c): perlin_octave, float32, einsum order
+template <bool EXT>
+__device__ __forceinline__ float octave_at(const WSmem<EXT>& sm, int o, const float* gx, const float* gy, int res,
+                                           int r, int c) {
+  const int d = WT<EXT>::H / res;
+  const int R = r / d, i = r % d, C = c / d, j = c % d, n = res + 1;
+  const float* P = &sm.prof[o][0][0];
+  const float a1 = P[0 * 32 + i], a2 = P[1 * 32 + i], a3 = P[2 * 32 + i], a4 = P[3 * 32 + i];
+  const float b0 = P[4 * 32 + j], b1 = P[5 * 32 + j], b2 = P[6 * 32 + j], b3 = P[7 * 32 + j];
+  const int k00 = R * n + C, k10 = (R + 1) * n + C;
+  float t0 = __fadd_rn(__fmul_rn(gx[k00], a1), __fmul_rn(gx[k10], a3));
+  float t1 = __fadd_rn(__fmul_rn(gy[k00], a2), __fmul_rn(gy[k10], a4));
+  float t2 = __fadd_rn(__fmul_rn(gx[k00 + 1], a1), __fmul_rn(gx[k10 + 1], a3));
+  float t3 = __fadd_rn(__fmul_rn(gy[k00 + 1], a2), __fmul_rn(gy[k10 + 1], a4));
+  return __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(t0, b0), __fmul_rn(t1, b1)), __fmul_rn(t2, b2)), __fmul_rn(t3, b3));
+}
+
+// worldgen._overworld_blocks for one tile
+__device__ __forceinline__ uint8_t overworld_tile(float h, float forest, float special, float u) {
+  uint8_t b = B_GRASS;
+  if (h < -0.28f) b = B_WATER;
+  if (h >= -0.28f && h < -0.22f) b = B_SAND;
+  const bool mountain = h > 0.28f;
+  if (mountain) b = B_STONE;
+  if (b == B_GRASS && forest > 0.18f && u < 0.55f) b = B_TREE;
+  if (mountain && fabsf(special) < 0.06f) b = B_PATH;
+  if (mountain && special < -0.5f) b = B_LAVA;
+  if (b == B_STONE) {
+    if (u < 0.035f) b = B_COAL;
+    if (u >= 0.94f && h > 0.34f) b = B_IRON;
+    if (u >= 0.91f && u < 0.94f && h > 0.45f) b = B_DIAMOND;
+  }
+  return b;
+}
+
+// worldgen._ensure_block with a float32 score (overworld / realm)
+template <bool EXT>
+__device__ bool ensure_f32(WSmem<EXT>& sm, uint8_t block, const float* hsrc, bool low, int spawn) {
+  using T = WT<EXT>;
+  const unsigned long long present = census(sm);
+  if ((present >> block) & 1ull) return true;
+  auto score = [&](int t) { return low ? -hsrc[t] : hsrc[t]; };
+  if (!low) {
+    float bv = 0.0f;
+    int bi = INT_MAX;
+    for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
+      if (sm.blk[t] == B_STONE && (bi == INT_MAX || score(t) > bv)) { bv = score(t); bi = t; }
+    int pos = block_argmax_f(sm, bv, bi);
+    if (pos >= 0) {
+      if (threadIdx.x == 0) sm.blk[pos] = block;
+      __syncthreads();
+      return true;
+    }
+  }
+  const int sr = spawn >= 0 ? spawn / T::W : 0, sc = spawn >= 0 ? spawn % T::W : 0;
+  auto near = [&](int t) { return spawn >= 0 && t != spawn && cheb(t / T::W, t % T::W, sr, sc) <= 8; };
+  int any_near = 0, any_grass = 0;
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+    any_grass |= sm.blk[t] == B_GRASS;
+    any_near |= sm.blk[t] == B_GRASS && near(t);
+  }
+  any_near = __syncthreads_or(any_near);
+  any_grass = __syncthreads_or(any_grass);
+  float bv = 0.0f;
+  int bi = INT_MAX;
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+    const uint8_t b = sm.blk[t];
+    const bool host = any_near ? (b == B_GRASS && near(t)) : any_grass ? b == B_GRASS : (b == B_GRASS || b == B_TREE);
+    if (host && (bi == INT_MAX || score(t) > bv)) { bv = score(t); bi = t; }
+  }
+  int pos = block_argmax_f(sm, bv, bi);
+  if (pos < 0) return false;
+  if (threadIdx.x == 0) sm.blk[pos] = block;
+  __syncthreads();
+  return true;
+}
+
+// worldgen._gen_overworld (:247-327) on angles already in sm.ang.
+// Returns false for _Degenerate.  Spawn written to sm.spawn, ladder to *ld.
+template <bool EXT>
+__device__ bool gen_overworld(WSmem<EXT>& sm, uint64_t seed0, bool extended, int attempt, int* ld) {
+  using T = WT<EXT>;
+  const uint64_t key = hash2(seed0, (uint64_t)attempt);
+  const uint32_t k32 = (uint32_t)(hash2(key, 1) & 0xFFFFFFFFull);
+  // fields + sprinkles + thresholds, one pass per tile
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+    const int r = t / T::W, c = t % T::W;
+    const float coarse = octave_at<EXT>(sm, 0, sm.gx, sm.gy, 2, r, c);
+    const float f1 = octave_at<EXT>(sm, 1, sm.gx + 9, sm.gy + 9, 8, r, c);
+    const float forest = octave_at<EXT>(sm, 1, sm.gx + 90, sm.gy + 90, 8, r, c);
+    const float special = octave_at<EXT>(sm, 1, sm.gx + 171, sm.gy + 171, 8, r, c);
+    const float h = __fdiv_rn(__fadd_rn(coarse, __fmul_rn(0.35f, f1)), 1.35f);
+    const float u = u32f(k32, (uint32_t)t);
+    sm.h32[t] = h;
+    sm.u[t] = u;
+    sm.blk[t] = overworld_tile(h, forest, special, u);
+    sm.itm[t] = 0;
+  }
+  __syncthreads();
+  // spawn: first walkable tile of minimal Chebyshev distance to the centre
+  unsigned long long best = ~0ull;
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
+    if (in_set(WALK_SET, sm.blk[t])) {
+      unsigned long long k = ((unsigned long long)cheb(t / T::W, t % T::W, T::H / 2, T::W / 2) << 32) | (unsigned)t;
+      best = k < best ? k : best;
+    }
+  best = block_min_u64(sm, best);
+  if (best == ~0ull) return false;
+  const int spawn = (int)(best & 0xFFFFFFFFull);
+  if (threadIdx.x == 0) { sm.blk[spawn] = B_GRASS; sm.spawn = spawn; }
+  __syncthreads();
+  const unsigned long long cen = census(sm);
+  bool fixed_any = false;
+  const uint8_t order[6] = {B_COAL, B_IRON, B_DIAMOND, B_LAVA, B_WATER, B_SAND};
+  for (int k = 0; k < 6; ++k) {
+    if (!((cen >> order[k]) & 1ull)) {
+      if (!ensure_f32<EXT>(sm, order[k], sm.h32, k >= 4, spawn)) return false;
+      fixed_any = true;
+    }
+  }
+  bool stone_now = (census(sm) >> B_STONE) & 1ull;
+  if (!((cen >> B_STONE) & 1ull) || (fixed_any && !stone_now))
+    if (!ensure_f32<EXT>(sm, B_STONE, sm.h32, false, spawn)) return false;
+  const int sr = spawn / T::W, sc = spawn % T::W;
+  if (!((cen >> B_TREE) & 1ull)) {
+    int pos = pick_u<EXT>(sm, sm.u, [&](int t) {
+      return sm.blk[t] == B_GRASS && t != spawn && cheb(t / T::W, t % T::W, sr, sc) <= 8;
+    });
+    if (pos < 0) pos = pick_u<EXT>(sm, sm.u, [&](int t) { return sm.blk[t] == B_GRASS; });
+    if (pos < 0) return false;
+    if (threadIdx.x == 0) sm.blk[pos] = B_TREE;
+    __syncthreads();
+  }
+  *ld = -1;
+  if (extended) {
+    int pos = pick_u<EXT>(sm, sm.u, [&](int t) {
+      return in_set(WALK_SET, sm.blk[t]) && cheb(t / T::W, t % T::W, sr, sc) >= 10;
+    });
+    if (pos < 0) pos = pick_u<EXT>(sm, sm.u, [&](int t) { return in_set(WALK_SET, sm.blk[t]); });
+    if (pos < 0 || pos == spawn) return false;
+    if (threadIdx.x == 0) sm.itm[pos] = I_LADDER_DOWN;
+    __syncthreads();
+    *ld = pos;
+  }
+  return true;
+}
+
+// gradients of the 252 angles in sm.ang (numpy float32 sin/cos)
+template <bool EXT>
+__device__ void overworld_gradients(WSmem<EXT>& sm) {
+  for (int k = threadIdx.x; k < 252; k += WG_THREADS) {
+    sm.gx[k] = np_sincosf(sm.ang[k], true);
+    sm.gy[k] = np_sincosf(sm.ang[k], false);
+  }
+  __syncthreads();
+}
+
+// f32(u * 2 * pi) exactly as (flat * 2.0 * np.pi).astype(np.float32)
+__device__ __forceinline__ float angle_of(double u) { return __double2float_rn(__dmul_rn(__dmul_rn(u, 2.0), PI_D)); }
+
+struct FloorOut { int spawn, ld, lu; };
+
+// worldgen._gen_realm (:479-520)
+template <bool EXT>
+__device__ bool gen_realm(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo) {
+  using T = WT<EXT>;
+  const Stream s = Stream::raw(seed).split(3000 + (uint64_t)attempt);
+  for (int k = threadIdx.x; k < 252; k += WG_THREADS) sm.ang[k] = angle_of(s.at((uint64_t)k));
+  __syncthreads();
+  overworld_gradients<EXT>(sm);
+  int ld_unused;
+  if (!gen_overworld<EXT>(sm, hash2(seed, 4000 + (uint64_t)attempt), false, attempt, &ld_unused)) return false;
+  const uint32_t k32 = (uint32_t)(hash2(hash2(seed, 13 + (uint64_t)attempt), 6) & 0xFFFFFFFFull);
+  const uint8_t gem = floor == 6 ? B_RUBY : B_SAPPHIRE;
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+    uint8_t b = sm.blk[t], d = b;
+    if (floor == 6) {
+      if (b == B_GRASS) d = B_FIRE_GRASS; else if (b == B_TREE) d = B_FIRE_TREE;
+      else if (b == B_WATER) d = B_LAVA; else if (b == B_SAND) d = B_GRAVEL;
+    } else {
+      if (b == B_GRASS) d = B_ICE_GRASS; else if (b == B_TREE) d = B_ICE_SHRUB;
+      else if (b == B_SAND) d = B_GRAVEL; else if (b == B_LAVA) d = B_WATER;
+    }
+    const float u = u32f(k32, (uint32_t)t);
+    sm.u[t] = u;
+    if (d == B_STONE && u > 0.975f) d = gem;
+    sm.blk[t] = d;
+  }
+  __syncthreads();
+  if (!ensure_f32<EXT>(sm, gem, sm.u, false, -1)) return false;
+  unsigned long long best = ~0ull;
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
+    if (in_set(WALK_SET, sm.blk[t])) {
+      unsigned long long k = ((unsigned long long)cheb(t / T::W, t % T::W, T::H / 2, T::W / 2) << 32) | (unsigned)t;
+      best = k < best ? k : best;
+    }
+  best = block_min_u64(sm, best);
+  if (best == ~0ull) return false;
+  const int spawn = (int)(best & 0xFFFFFFFFull), sr = spawn / T::W, sc = spawn % T::W;
+  int tpos = pick_u<EXT>(sm, sm.u, [&](int t) {
+    return in_set(WALK_SET, sm.blk[t]) && cheb(t / T::W, t % T::W, sr, sc) <= 8;
+  });
+  if (tpos < 0 || tpos == spawn) return false;
+  if (threadIdx.x == 0) sm.blk[tpos] = floor == 6 ? B_ENCHANT_FIRE : B_ENCHANT_ICE;
+  __syncthreads();
+  int down = pick_u<EXT>(sm, sm.u, [&](int t) {
+    return in_set(WALK_SET, sm.blk[t]) && cheb(t / T::W, t % T::W, sr, sc) >= 10;
+  });
+  if (down < 0) {
+    // _pick_tile(out, walk, 1.0 - u)
+    float bv = 0.0f;
+    int bi = INT_MAX;
+    for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+      const float v = __fsub_rn(1.0f, sm.u[t]);
+      if (in_set(WALK_SET, sm.blk[t]) && (bi == INT_MAX || v > bv)) { bv = v; bi = t; }
+    }
+    down = block_argmax_f(sm, bv, bi);
+  }
+  if (down < 0 || down == spawn) return false;
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) sm.itm[t] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) { sm.itm[spawn] = I_LADDER_UP; sm.itm[down] = I_LADDER_DOWN; }
+  __syncthreads();
+  fo->spawn = spawn; fo->lu = spawn; fo->ld = down;
+  return true;
+}
+
+// worldgen._carve_line on thread 0
+template <bool EXT>
+__device__ void carve(WSmem<EXT>& sm, int r, int c, int tr, int tc) {
+  using T = WT<EXT>;
+  while (c != tc) { c += tc > c ? 1 : -1; sm.blk[r * T::W + c] = B_PATH; }
+  while (r != tr) { r += tr > r ? 1 : -1; sm.blk[r * T::W + c] = B_PATH; }
+}
+
+// worldgen._gen_dungeon (:367-406)
+template <bool EXT>
+__device__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo) {
+  using T = WT<EXT>;
+  if (threadIdx.x == 0) {
+    Stream s = Stream::raw(seed).split(1000 + (uint64_t)attempt);
+    const int n = s.randint(4, 8);
+    sm.nrooms = n;
+    for (int k = 0; k < n; ++k) {
+      const int rh = s.randint(5, 10), rw = s.randint(5, 10);
+      const int r0 = s.randint(2, T::H - rh - 2), c0 = s.randint(2, T::W - rw - 2);
+      sm.cr[k] = r0 + rh / 2;
+      sm.cc[k] = c0 + rw / 2;
+      // stash room rectangles in rowcnt (4 ints per room)
+      sm.rowcnt[4 * k] = r0; sm.rowcnt[4 * k + 1] = r0 + rh;
+      sm.rowcnt[4 * k + 2] = c0; sm.rowcnt[4 * k + 3] = c0 + rw;
+    }
+  }
+  __syncthreads();
+  const int n = sm.nrooms;
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+    const int r = t / T::W, c = t % T::W;
+    bool in = false;
+    for (int k = 0; k < n; ++k)
+      in |= r >= sm.rowcnt[4 * k] && r < sm.rowcnt[4 * k + 1] && c >= sm.rowcnt[4 * k + 2] && c < sm.rowcnt[4 * k + 3];
+    sm.blk[t] = in ? B_PATH : B_WALL;
+    sm.itm[t] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k + 1 < n; ++k) carve<EXT>(sm, sm.cr[k], sm.cc[k], sm.cr[k + 1], sm.cc[k + 1]);
+  __syncthreads();
+  const uint32_t k32 = (uint32_t)(hash2(hash2(seed, 7 + (uint64_t)attempt), 4) & 0xFFFFFFFFull);
+  uint8_t nb[WT<EXT>::PER];
+#pragma unroll
+  for (int q = 0; q < WT<EXT>::PER; ++q) {
+    const int t = threadIdx.x + q * WG_THREADS;
+    if (t >= T::HW) break;
+    const int r = t / T::W, c = t % T::W;
+    const float u = u32f(k32, (uint32_t)t);
+    sm.u[t] = u;
+    const uint8_t b = sm.blk[t];
+    const bool path = b == B_PATH;
+    const bool near_path = path || (r > 0 && sm.blk[t - T::W] == B_PATH) || (r < T::H - 1 && sm.blk[t + T::W] == B_PATH) ||
+                           (c > 0 && sm.blk[t - 1] == B_PATH) || (c < T::W - 1 && sm.blk[t + 1] == B_PATH);
+    uint8_t d = b;
+    if (b == B_WALL && near_path && u < 0.25f) d = B_WALL_MOSS;
+    if (floor == 3 && path && u > 0.82f) d = B_WATER;
+    if (floor == 4 && path && u > 0.85f) d = B_GRAVEL;
+    nb[q] = d;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < WT<EXT>::PER; ++q) {
+    const int t = threadIdx.x + q * WG_THREADS;
+    if (t < T::HW) sm.blk[t] = nb[q];
+  }
+  __syncthreads();
+  const int fountain = pick_u<EXT>(sm, sm.u, [&](int t) { return sm.blk[t] == B_PATH; });
+  if (fountain >= 0 && threadIdx.x == 0) sm.blk[fountain] = B_FOUNTAIN;
+  __syncthreads();
+  const int up = sm.cr[0] * T::W + sm.cc[0], down = sm.cr[n - 1] * T::W + sm.cc[n - 1];
+  if (sm.blk[up] != B_PATH || sm.blk[down] != B_PATH || up == down) return false;
+  __syncthreads();
+  if (threadIdx.x == 0) { sm.itm[up] = I_LADDER_UP; sm.itm[down] = I_LADDER_DOWN; }
+  __syncthreads();
+  fo->spawn = up; fo->lu = up; fo->ld = down;
+  return true;
+}
+
+// perlin._profiles in float64 for the cave octaves (res 4 and 8)
+template <bool EXT>
+__device__ void build_profiles_f64(WSmem<EXT>& sm) {
+  const int H = WT<EXT>::H;
+  const int dims[2] = {H / 4, H / 8};
+  for (int k = threadIdx.x; k < 2 * 12; k += WG_THREADS) {
+    const int o = k / 12, i = k % 12, d = dims[o];
+    if (i >= d) continue;
+    double f = __ddiv_rn((double)i, (double)d);
+    double u = __dmul_rn(__dmul_rn(__dmul_rn(f, f), f),
+                         __dadd_rn(__dmul_rn(f, __dsub_rn(__dmul_rn(f, 6.0), 15.0)), 10.0));
+    const double one = 1.0, root2 = 1.4142135623730951;
+    sm.dprof[o][0][i] = __dsub_rn(one, u);
+    sm.dprof[o][1][i] = __dmul_rn(__dsub_rn(one, u), f);
+    sm.dprof[o][2][i] = u;
+    sm.dprof[o][3][i] = __dmul_rn(u, __dsub_rn(f, one));
+    sm.dprof[o][4][i] = __dmul_rn(__dmul_rn(__dsub_rn(one, u), f), root2);
+    sm.dprof[o][5][i] = __dmul_rn(__dsub_rn(one, u), root2);
+    sm.dprof[o][6][i] = __dmul_rn(__dmul_rn(u, __dsub_rn(f, one)), root2);
+    sm.dprof[o][7][i] = __dmul_rn(u, root2);
+  }
+}
+
+template <bool EXT>
+__device__ __forceinline__ double octave_at_d(const WSmem<EXT>& sm, int o, const double* gx, const double* gy,
+                                              int res, int r, int c) {
+  const int d = WT<EXT>::H / res;
+  const int R = r / d, i = r % d, C = c / d, j = c % d, n = res + 1;
+  const double* P = &sm.dprof[o][0][0];
+  const double a1 = P[0 * 12 + i], a2 = P[1 * 12 + i], a3 = P[2 * 12 + i], a4 = P[3 * 12 + i];
+  const double b0 = P[4 * 12 + j], b1 = P[5 * 12 + j], b2 = P[6 * 12 + j], b3 = P[7 * 12 + j];
+  const int k00 = R * n + C, k10 = (R + 1) * n + C;
+  double t0 = __dadd_rn(__dmul_rn(gx[k00], a1), __dmul_rn(gx[k10], a3));
+  double t1 = __dadd_rn(__dmul_rn(gy[k00], a2), __dmul_rn(gy[k10], a4));
+  double t2 = __dadd_rn(__dmul_rn(gx[k00 + 1], a1), __dmul_rn(gx[k10 + 1], a3));
+  double t3 = __dadd_rn(__dmul_rn(gy[k00 + 1], a2), __dmul_rn(gy[k10 + 1], a4));
+  return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(t0, b0), __dmul_rn(t1, b1)), __dmul_rn(t2, b2)), __dmul_rn(t3, b3));
+}
+
+// worldgen._gen_cave (:418-468)
+template <bool EXT>
+__device__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo, bool* fragile) {
+  using T = WT<EXT>;
+  const Stream s = Stream::raw(seed).split(2000 + (uint64_t)attempt);
+  for (int k = threadIdx.x; k < 106; k += WG_THREADS) {
+    const float a = angle_of(s.at((uint64_t)k));
+    double sn, cs;
+    dd_sincos((double)a, &sn, &cs);
+    sm.dgx[k] = cs;
+    sm.dgy[k] = sn;
+  }
+  __syncthreads();
+  const uint32_t k32 = (uint32_t)(hash2(hash2(seed, 11 + (uint64_t)attempt), 5) & 0xFFFFFFFFull);
+  int frag = 0;
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+    const int r = t / T::W, c = t % T::W;
+    const double o1 = octave_at_d<EXT>(sm, 0, sm.dgx, sm.dgy, 4, r, c);
+    const double o2 = octave_at_d<EXT>(sm, 1, sm.dgx + 25, sm.dgy + 25, 8, r, c);
+    const double field = __ddiv_rn(__dadd_rn(__dmul_rn(1.0, o1), __dmul_rn(0.5, o2)), 1.5);
+    frag |= fabs(field + 0.02) < 1e-12 || fabs(field + 0.62) < 1e-12;
+    sm.f64[t] = field;
+    const float u = u32f(k32, (uint32_t)t);
+    sm.u[t] = u;
+    const bool open = field > -0.02;
+    uint8_t b = open ? B_PATH : B_STONE;
+    if (open && u < 0.04f) b = B_STALAGMITE;
+    if (b == B_STONE) {
+      if (floor == 2) {
+        if (u < 0.06f) b = B_COAL;
+        if (u >= 0.90f && u < 0.93f) b = B_IRON;
+        if (u >= 0.975f) b = B_SAPPHIRE;
+      } else {
+        if (u < 0.05f) b = B_COAL;
+        if (u >= 0.90f && u < 0.93f) b = B_IRON;
+        if (u >= 0.96f && u < 0.975f) b = B_DIAMOND;
+        if (u >= 0.985f) b = B_RUBY;
+      }
+    }
+    if (floor != 2 && field < -0.62) b = B_LAVA;
+    sm.blk[t] = b;
+    sm.itm[t] = 0;
+  }
+  if (__syncthreads_or(frag)) *fragile = true;
+  const uint8_t must2[3] = {B_COAL, B_IRON, B_SAPPHIRE};
+  const uint8_t must5[4] = {B_COAL, B_IRON, B_DIAMOND, B_RUBY};
+  const int nm = floor == 2 ? 3 : 4;
+  for (int k = 0; k < nm; ++k) {
+    const uint8_t b = floor == 2 ? must2[k] : must5[k];
+    if ((census(sm) >> b) & 1ull) continue;
+    double bv = 0.0;
+    int bi = INT_MAX;
+    for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
+      if (sm.blk[t] == B_STONE && (bi == INT_MAX || -sm.f64[t] > bv)) { bv = -sm.f64[t]; bi = t; }
+    const int pos = block_argmax_d(sm, bv, bi);
+    if (pos < 0) return false;   // no stone and caves hold no grass / trees
+    if (threadIdx.x == 0) sm.blk[pos] = b;
+    __syncthreads();
+  }
+  int cnt = 0;
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) cnt += sm.blk[t] == B_PATH;
+  {
+    // block sum of cnt
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0) sm.ri[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int k = 0; k < WG_THREADS / 32; ++k) tot += sm.ri[k];
+      sm.res_i = tot;
+    }
+    __syncthreads();
+    cnt = sm.res_i;
+    __syncthreads();
+  }
+  if (cnt < 40) return false;
+  const int up = pick_u<EXT>(sm, sm.u, [&](int t) { return sm.blk[t] == B_PATH; });
+  if (up < 0) return false;
+  const int ur = up / T::W, uc = up % T::W;
+  // argmax of chebyshev(up)/max over open tiles == argmax of the distance
+  unsigned long long best = ~0ull;
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
+    if (sm.blk[t] == B_PATH) {
+      unsigned long long k = ((unsigned long long)(1000 - cheb(t / T::W, t % T::W, ur, uc)) << 32) | (unsigned)t;
+      best = k < best ? k : best;
+    }
+  best = block_min_u64(sm, best);
+  const int down = (int)(best & 0xFFFFFFFFull);
+  if (best == ~0ull || down == up) return false;
+  if (threadIdx.x == 0) {
+    carve<EXT>(sm, ur, uc, down / T::W, down % T::W);
+    sm.blk[up] = B_PATH;
+    sm.blk[down] = B_PATH;
+    sm.itm[up] = I_LADDER_UP;
+    sm.itm[down] = I_LADDER_DOWN;
+  }
+  __syncthreads();
+  fo->spawn = up; fo->lu = up; fo->ld = down;
+  return true;
+}
+
+// worldgen._gen_graveyard (:523-546)
+template <bool EXT>
+__device__ void gen_graveyard(WSmem<EXT>& sm, FloorOut* fo) {
+  using T = WT<EXT>;
+  const int cr = T::H / 2, cc = T::W / 2;
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+    const int r = t / T::W, c = t % T::W;
+    uint8_t b = B_DARKNESS;
+    if (r >= cr - 10 && r <= cr + 10 && c >= cc - 10 && c <= cc + 10) b = B_WALL;
+    if (r > cr - 10 && r < cr + 10 && c > cc - 10 && c < cc + 10) b = B_PATH;
+    sm.blk[t] = b;
+    sm.itm[t] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int go[12][2] = {{-3, -5}, {-3, 5}, {0, -7}, {0, 7}, {3, -4}, {3, 4},
+                           {5, 0}, {-5, -2}, {-5, 2}, {6, -6}, {6, 6}, {2, 0}};
+    for (int k = 0; k < 12; ++k) sm.blk[(cr + go[k][0]) * T::W + cc + go[k][1]] = B_GRAVE + k % 3;
+    for (int r = cr + 4; r < cr + 7; ++r)
+      for (int c = cc - 5; c < cc - 2; ++c) sm.blk[r * T::W + c] = B_WATER;
+    sm.blk[(cr - 6) * T::W + cc] = B_NECROMANCER;
+    const int up = (cr + 10 - 2) * T::W + cc;
+    sm.blk[up] = B_PATH;
+    sm.itm[up] = I_LADDER_UP;
+  }
+  __syncthreads();
+  const int up = (cr + 8) * T::W + cc;
+  fo->spawn = up; fo->lu = up; fo->ld = -1;
+}
+
+// worldgen._template_floor (:549-575)
+template <bool EXT>
+__device__ void gen_template(WSmem<EXT>& sm, int floor, FloorOut* fo) {
+  using T = WT<EXT>;
+  const int H = T::H, W = T::W, cr = H / 2, cc = W / 2;
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+    const int r = t / W, c = t % W;
+    uint8_t b = floor == 0 ? B_GRASS : B_PATH;
+    if (floor != 0 && (r == 0 || r == H - 1 || c == 0 || c == W - 1)) b = B_WALL;
+    if (floor == 0) {
+      if (r >= 2 && r < 5 && c >= 2 && c < 5) b = B_WATER;
+      if (r >= 6 && r < 8 && c >= 2 && c < 6) b = B_SAND;
+      if (r == cr - 4 && c == cc) b = B_TREE;
+      if (r >= H - 6 && r < H - 2 && c >= W - 6 && c < W - 2) b = B_STONE;
+      if (r == H - 5 && c == W - 5) b = B_COAL;
+      if (r == H - 4 && c == W - 4) b = B_IRON;
+      if (r == H - 3 && c == W - 3) b = B_DIAMOND;
+      if (r == H - 6 && c == W - 3) b = B_LAVA;
+    }
+    sm.blk[t] = b;
+    sm.itm[t] = 0;
+  }
+  __syncthreads();
+  fo->spawn = cr * W + cc;
+  fo->lu = floor != 0 ? cr * W + cc - 5 : -1;
+  fo->ld = floor != 8 ? cr * W + cc + 5 : -1;
+  if (threadIdx.x == 0) {
+    if (fo->lu >= 0) sm.itm[fo->lu] = I_LADDER_UP;
+    if (fo->ld >= 0) sm.itm[fo->ld] = I_LADDER_DOWN;
+  }
+  __syncthreads();
+}
+
+// worldgen._assign_chests for one floor (:598-623), thread 0
+template <bool EXT>
+__device__ void assign_chests(WSmem<EXT>& sm, uint64_t world_seed, int f, WMeta* meta) {
+  using T = WT<EXT>;
+  const int per_floor[9] = {0, 4, 2, 3, 3, 2, 2, 2, 0};
+  const int nc = per_floor[f];
+  if (nc == 0) {
+    if (threadIdx.x == 0) meta->nch[f] = 0;
+    return;
+  }
+  // PATH tiles per row (the list of np.nonzero, row-major)
+  for (int r = threadIdx.x; r < T::H; r += WG_THREADS) {
+    int c0 = 0;
+    for (int c = 0; c < T::W; ++c) c0 += sm.blk[r * T::W + c] == B_PATH;
+    sm.rowcnt[r] = c0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int len = 0;
+    for (int r = 0; r < T::H; ++r) len += sm.rowcnt[r];
+    int nl = 0;
+    if (len) {
+      Stream s = Stream::raw(world_seed).split(5000 + (uint64_t)f);
+      const int lim = min(min(nc, 6), len);
+      for (int k = 0; k < lim; ++k) {
+        int j = s.randint(0, len);
+        int r = 0;
+        while (j >= sm.rowcnt[r]) { j -= sm.rowcnt[r]; ++r; }
+        int t = r * T::W;
+        for (;; ++t) {
+          const uint8_t b = sm.blk[t];
+          if (b == B_PATH || b == B_CHEST) {   // chests placed here were PATH in the list
+            if (j == 0) break;
+            --j;
+          }
+        }
+        if (sm.blk[t] != B_PATH || sm.itm[t] != I_EMPTY) continue;
+        sm.blk[t] = B_CHEST;
+        int loot, qty;
+        if (f == 1 && nl == 0) { loot = LOOT_BOW; qty = 1; }
+        else if (f == 1 && nl == 1) { loot = LOOT_BOOK; qty = 1; }
+        else {
+          const double u = s.uniform01();
+          // _weighted_loot: cumulative weights accumulated in float64
+          double acc = 0.0;
+          const int kinds[4] = {LOOT_POTION, LOOT_ARROWS, LOOT_TORCHES, LOOT_BOOK};
+          const int qtys[4] = {1, 3, 4, 1};
+          const double wts[4] = {0.40, 0.25, 0.20, 0.15};
+          loot = kinds[3]; qty = qtys[3];
+          for (int q = 0; q < 4; ++q) {
+            acc = __dadd_rn(acc, wts[q]);
+            if (u < acc) { loot = kinds[q]; qty = qtys[q]; break; }
+          }
+        }
+        meta->chest[f][nl][0] = (int16_t)(t / T::W);
+        meta->chest[f][nl][1] = (int16_t)(t % T::W);
+        meta->chest[f][nl][2] = (int16_t)loot;
+        meta->chest[f][nl][3] = (int16_t)qty;
+        ++nl;
+      }
+    }
+    meta->nch[f] = (uint8_t)nl;
+  }
+  __syncthreads();
+}
+
+template <bool EXT>
+__global__ void __launch_bounds__(WG_THREADS) k_worldgen(WorldJob job) {
+  using T = WT<EXT>;
+  __shared__ WSmem<EXT> sm;
+  const int64_t nworlds = job.mode == 1 ? (int64_t)job.info->n_pool : job.count;
+  const int64_t items = nworlds * T::F;
+  build_profiles_f32<EXT>(sm);
+  if (EXT) build_profiles_f64<EXT>(sm);
+  __syncthreads();
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t w = it / T::F;
+    const int f = (int)(it % T::F);
+    uint64_t seed, key;
+    if (job.mode == 0) {
+      seed = hash2(job.env_key, hash2((uint64_t)(job.env_offset + w), 0));
+      key = hash2(seed, hash2(1, 0));
+    } else {
+      const int64_t slot = ((int64_t)job.info->offset + w) % job.M;
+      seed = hash2(job.info->step_key, (uint64_t)slot);
+      key = hash2(job.info->step_key, (1ull << 32) + (uint64_t)slot);
+    }
+    WMeta* meta = job.out.meta + w;
+    // make_level_params (worldgen.py:75-87)
+    const uint64_t base = mix64(seed);
+    const uint64_t fseed = hash2(base, hash2(100 + (uint64_t)f, 0));
+    bool fragile = false;
+    FloorOut fo{-1, -1, -1};
+    int attempt = 0;
+    bool ok = false;
+    if (f == 0) {
+      const uint64_t k1 = hash2(base, hash2(1, 0));
+      for (int k = threadIdx.x; k < 252; k += WG_THREADS) sm.ang[k] = angle_of(u64d(k1, (uint64_t)k));
+      __syncthreads();
+      overworld_gradients<EXT>(sm);
+      for (attempt = 0; attempt < 16 && !ok; ++attempt) {
+        int ld;
+        ok = gen_overworld<EXT>(sm, fseed, EXT, attempt, &ld);
+        if (ok) { fo.spawn = sm.spawn; fo.ld = ld; fo.lu = -1; }
+      }
+    } else if (f == 1 || f == 3 || f == 4) {
+      for (attempt = 0; attempt < 16 && !ok; ++attempt) ok = gen_dungeon<EXT>(sm, fseed, f, attempt, &fo);
+    } else if (f == 2 || f == 5) {
+      for (attempt = 0; attempt < 16 && !ok; ++attempt) ok = gen_cave<EXT>(sm, fseed, f, attempt, &fo, &fragile);
+    } else if (f == 6 || f == 7) {
+      for (attempt = 0; attempt < 16 && !ok; ++attempt) ok = gen_realm<EXT>(sm, fseed, f, attempt, &fo);
+    } else {
+      gen_graveyard<EXT>(sm, &fo);
+      ok = true;
+      attempt = 1;
+    }
+    uint32_t flags = 0;
+    if (attempt > 1) flags |= WG_FLAG_RETRY;
+    if (!ok) {
+      gen_template<EXT>(sm, f, &fo);
+      flags |= WG_FLAG_TEMPLATE;
+    }
+    if (fragile) flags |= WG_FLAG_FRAGILE;
+    if (EXT && f >= 1 && f <= 7) assign_chests<EXT>(sm, seed, f, meta);
+    // write the floor out (16-byte vectors)
+    uint8_t* ob = job.out.blocks + ((size_t)w * T::F + f) * T::HW;
+    uint8_t* oi = job.out.items + ((size_t)w * T::F + f) * T::HW;
+    for (int q = threadIdx.x; q < T::HW / 16; q += WG_THREADS) {
+      reinterpret_cast<uint4*>(ob)[q] = reinterpret_cast<const uint4*>(sm.blk)[q];
+      reinterpret_cast<uint4*>(oi)[q] = reinterpret_cast<const uint4*>(sm.itm)[q];
+    }
+    if (threadIdx.x == 0) {
+      meta->ld[f][0] = (int16_t)(fo.ld >= 0 ? fo.ld / T::W : -1);
+      meta->ld[f][1] = (int16_t)(fo.ld >= 0 ? fo.ld % T::W : -1);
+      meta->lu[f][0] = (int16_t)(fo.lu >= 0 ? fo.lu / T::W : -1);
+      meta->lu[f][1] = (int16_t)(fo.lu >= 0 ? fo.lu % T::W : -1);
+      if (f == 0) {
+        meta->spawn[0] = (int16_t)(fo.spawn / T::W);
+        meta->spawn[1] = (int16_t)(fo.spawn % T::W);
+        meta->seed = seed;
+        meta->key = key;
+        // potion permutation: argsort of six hashed float32 draws
+        const uint32_t pk = (uint32_t)(hash2(seed, 42) & 0xFFFFFFFFull);
+        float v[6];
+        int idx[6];
+        for (int q = 0; q < 6; ++q) { v[q] = u32f(pk, (uint32_t)q); idx[q] = q; }
+        for (int a = 1; a < 6; ++a)
+          for (int b = a; b > 0 && v[idx[b - 1]] > v[idx[b]]; --b) { int tq = idx[b]; idx[b] = idx[b - 1]; idx[b - 1] = tq; }
+        bool tie = false;
+        for (int a = 0; a < 6; ++a) {
+          meta->potion[a] = (uint8_t)idx[a];
+          for (int b = a + 1; b < 6; ++b) tie |= v[a] == v[b];
+        }
+        if (tie) flags |= WG_FLAG_POTION_TIE;
+        if (!EXT) meta->nch[0] = 0;
+      }
+      if (flags) {
+        atomicOr(&meta->flags, flags);
+        if (job.counters) {
+          if (flags & WG_FLAG_RETRY) atomicAdd(&job.counters[1], 1ull);
+          if (flags & WG_FLAG_TEMPLATE) atomicAdd(&job.counters[2], 1ull);
+          if (flags & WG_FLAG_POTION_TIE) atomicAdd(&job.counters[3], 1ull);
+          if (flags & WG_FLAG_FRAGILE) atomicAdd(&job.counters[4], 1ull);
+        }
+      }
+      if (f == 0 && job.counters) atomicAdd(&job.counters[0], 1ull);
+    }
+    __syncthreads();
+  }
+}
+
+void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st) {
+  // persistent grid: a few CTAs per SM walk the (world, floor) items
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t max_items = (j.mode == 0 ? j.count : j.out.cap) * (ext ? 9 : 1);
+  int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * 4);
+  if (grid <= 0) return;
+  if (ext) k_worldgen<true><<<grid, WG_THREADS, 0, st>>>(j);
+  else k_worldgen<false><<<grid, WG_THREADS, 0, st>>>(j);
+}
+
+}  // namespace gr

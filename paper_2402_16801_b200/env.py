@@ -1,0 +1,309 @@
+"""Host-side mirror of the reference's batched-env interface.
+
+``BatchEnv`` is a drop-in for ``gridrogue_gym.BatchEnv``
+(/root/reference/pkg/bindings/src/gridrogue_gym/__init__.py:24-95): same
+constructor, properties, ``reset() -> obs``, ``step(actions) -> (obs, reward,
+done, info)``, error messages and single-owner rule, backed by the CUDA
+library instead of numpy.  ``GridrogueBatch`` is the lower-level handle that
+keeps everything on the device (torch tensors as carriers) for training
+loops and the benchmark.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+TIERS = {
+    "classic": dict(n_actions=17, n_achievements=22, obs=1345, view=(7, 9), side=0),
+    "extended": dict(n_actions=43, n_achievements=67, obs=8268, view=(9, 11), side=2),
+}
+SUPPORTED_TILE_PX = (7, 10, 16)
+DEFAULT_TILE_PX = {"classic": 7, "extended": 10}
+
+
+def _tier_name(tier) -> str:
+    name = getattr(tier, "name", tier)
+    if name not in TIERS:
+        raise ValueError(f"unknown tier {name!r}")   # constants.tier_by_name
+    return name
+
+
+def pixel_shape(tier: str, tile_px: int) -> tuple:
+    t = TIERS[tier]
+    vr, vc = t["view"]
+    return ((vr + 2) * tile_px, (vc + t["side"]) * tile_px, 3)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class GridrogueBatch:
+    """One shard of the batch on one GPU: device state + device I/O tensors.
+
+    Output tensors are preallocated once and overwritten by every call
+    (the reference allocates fresh arrays per step; clone if you keep them).
+    """
+
+    def __init__(self, n_envs: int, tier: str = "extended", seed: int = 0,
+                 obs_mode: str = "symbolic", max_episode_length: int | None = None,
+                 tile_px: int | None = None, device: int = 0, reset_ratio: int = 16,
+                 env_offset: int = 0, n_envs_global: int | None = None,
+                 newly: bool = True, info: bool = True):
+        import torch
+        self.torch = torch
+        self.tier = _tier_name(tier)
+        if obs_mode not in _lib.OBS_IDS:
+            raise ValueError(f"unknown obs_mode {obs_mode!r}")
+        self.obs_mode = obs_mode
+        self.n = int(n_envs)
+        self.tile_px = int(tile_px or DEFAULT_TILE_PX[self.tier])
+        if obs_mode == "pixels" and self.tile_px not in SUPPORTED_TILE_PX:
+            raise ValueError(f"tile_px must be one of {SUPPORTED_TILE_PX}")
+        self.device = torch.device("cuda", device)
+        cfg = _lib.GrConfig()
+        cfg.tier = _lib.TIER_IDS[self.tier]
+        cfg.obs_mode = _lib.OBS_IDS[obs_mode]
+        cfg.tile_px = self.tile_px
+        cfg.reset_ratio = int(reset_ratio)
+        cfg.n_envs = self.n
+        cfg.env_offset = int(env_offset)
+        cfg.n_envs_global = int(n_envs_global or self.n)
+        cfg.max_episode_length = int(max_episode_length or 0)
+        cfg.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+        cfg.device = int(device)
+        self.cfg = cfg
+        self.h = ctypes.c_void_p()
+        check(lib().gr_create(ctypes.byref(cfg), ctypes.byref(self.h)))
+        t = TIERS[self.tier]
+        self.n_actions = t["n_actions"]
+        self.n_achievements = t["n_achievements"]
+        dev = self.device
+        n = self.n
+        if obs_mode == "symbolic":
+            self.obs = torch.empty((n, t["obs"]), dtype=torch.float32, device=dev)
+        elif obs_mode == "pixels":
+            self.obs = torch.empty((n,) + pixel_shape(self.tier, self.tile_px), dtype=torch.uint8, device=dev)
+        else:
+            self.obs = torch.empty((n, 0), dtype=torch.float32, device=dev)
+        self.actions = torch.zeros(n, dtype=torch.int64, device=dev)
+        self.reward = torch.empty(n, dtype=torch.float32, device=dev)
+        self.done = torch.empty(n, dtype=torch.uint8, device=dev)
+        self.newly = torch.empty((n, t["n_achievements"]), dtype=torch.uint8, device=dev) if newly else None
+        self.time = torch.empty(n, dtype=torch.int32, device=dev) if info else None
+        self.floor = torch.empty(n, dtype=torch.uint8, device=dev) if info else None
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            lib().gr_destroy(h)
+            self.h = None
+
+    # --- hot path -----------------------------------------------------
+    def _stream(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _obs_ptr(self):
+        return _ptr(self.obs) if self.obs_mode != "none" else None
+
+    def reset(self):
+        check(lib().gr_reset(self.h, self._obs_ptr(), self._stream()))
+        return self.obs
+
+    def random_actions(self, seed: int, t: int, out=None):
+        out = self.actions if out is None else out
+        check(lib().gr_random_actions(self.h, seed & 0xFFFFFFFF, t, _ptr(out), self._stream()))
+        return out
+
+    def set_validate(self, on: bool) -> None:
+        check(lib().gr_set_validate(self.h, 1 if on else 0))
+
+    def step(self, actions=None):
+        """Device step; returns (obs, reward, done, newly, time, floor) tensors."""
+        a = self.actions if actions is None else actions
+        if a.dtype != self.torch.int64 or a.device != self.device or not a.is_contiguous():
+            a = a.to(device=self.device, dtype=self.torch.int64).contiguous()
+        if tuple(a.shape) != (self.n,):
+            raise ValueError(f"actions must have shape ({self.n},), got {tuple(a.shape)}")
+        check(lib().gr_step(self.h, _ptr(a), self._obs_ptr(), _ptr(self.reward), _ptr(self.done),
+                            _ptr(self.newly), _ptr(self.time), _ptr(self.floor), self._stream()))
+        return self.obs, self.reward, self.done, self.newly, self.time, self.floor
+
+    # sharded step (see parallel.py)
+    def step_local(self, actions, exchange):
+        check(lib().gr_step_local(self.h, _ptr(actions), _ptr(self.reward), _ptr(self.done),
+                                  _ptr(self.newly), _ptr(self.time), _ptr(self.floor),
+                                  _ptr(exchange), self._stream()))
+
+    def step_finish(self, exchange_all, rank: int, world: int):
+        check(lib().gr_step_finish(self.h, _ptr(exchange_all), rank, world, self._obs_ptr(),
+                                   self._stream()))
+        return self.obs, self.reward, self.done, self.newly, self.time, self.floor
+
+    def observe(self):
+        check(lib().gr_observe(self.h, self._obs_ptr(), self._stream()))
+        return self.obs
+
+    # --- state channel --------------------------------------------------
+    def field_shape(self, name: str) -> tuple:
+        n_el = ctypes.c_int64()
+        esz = ctypes.c_int32()
+        check(lib().gr_field_info(self.cfg.tier, _lib.FIELD_ID[name], ctypes.byref(n_el), ctypes.byref(esz)))
+        return n_el.value, esz.value
+
+    def export_field(self, name: str) -> np.ndarray:
+        self.torch.cuda.synchronize(self.device)
+        n_el, esz = self.field_shape(name)
+        buf = np.empty(self.n * n_el * esz, np.uint8)
+        check(lib().gr_export_field(self.h, _lib.FIELD_ID[name], buf.ctypes.data_as(ctypes.c_void_p)))
+        return buf
+
+    def import_field(self, name: str, arr: np.ndarray) -> None:
+        self.torch.cuda.synchronize(self.device)
+        a = np.ascontiguousarray(arr)
+        n_el, esz = self.field_shape(name)
+        if a.nbytes != self.n * n_el * esz:
+            raise ValueError(f"field {name}: expected {self.n * n_el * esz} bytes, got {a.nbytes}")
+        check(lib().gr_import_field(self.h, _lib.FIELD_ID[name], a.ctypes.data_as(ctypes.c_void_p)))
+
+    def export_state(self, shapes: dict) -> dict:
+        """Every SimState field as numpy, given {name: (dtype, shape)}."""
+        out = {}
+        for name in _lib.FIELD_NAMES:
+            dt, shape = shapes[name]
+            out[name] = self.export_field(name).view(dt).reshape(shape)
+        return out
+
+    def import_state(self, fields: dict) -> None:
+        for name in _lib.FIELD_NAMES:
+            self.import_field(name, fields[name])
+
+    # --- metrics ------------------------------------------------------
+    def stats(self) -> dict:
+        s = _lib.GrStats()
+        check(lib().gr_stats_get(self.h, ctypes.byref(s)))
+        return {"episodes": s.episodes, "total_return": s.total_return, "total_steps": s.total_steps,
+                "ach_episodes": np.array(s.ach_episodes[:self.n_achievements], np.int64)}
+
+    def episodes_completed(self) -> int:
+        v = ctypes.c_int64()
+        check(lib().gr_episodes_completed(self.h, ctypes.byref(v)))
+        return v.value
+
+    def level_seeds(self) -> np.ndarray:
+        self.torch.cuda.synchronize(self.device)
+        out = np.empty(self.n, np.uint64)
+        check(lib().gr_level_seeds(self.h, out.ctypes.data_as(ctypes.c_void_p)))
+        return out
+
+    def kernel_launches(self) -> int:
+        return int(lib().gr_kernel_launches(self.h))
+
+    def worldgen_counters(self) -> dict:
+        c = (ctypes.c_int64 * 5)()
+        check(lib().gr_worldgen_counters(self.h, c))
+        return dict(zip(("worlds", "retried_floors", "template_floors", "potion_ties", "fragile_caves"), c))
+
+
+class BatchEnv:
+    """N parallel episodes behind a (obs, reward, done, info) step contract.
+
+    Drop-in for gridrogue_gym.BatchEnv (__init__.py:24-95) with numpy
+    inputs/outputs; the work runs on the GPU through the C ABI with
+    host<->device copies inside ``step``.  obs_mode "pixels" adds the RGB
+    frame of tiles.render_tiles per env (the reference renders one env).
+    """
+
+    metadata = {"obs_modes": ("symbolic", "none", "pixels")}
+
+    def __init__(self, n_envs: int, tier: str = "extended", seed: int = 0,
+                 obs_mode: str = "symbolic", max_episode_length: int | None = None,
+                 tile_px: int | None = None, device: int = 0):
+        if obs_mode not in self.metadata["obs_modes"]:
+            raise ValueError(f"unknown obs_mode {obs_mode!r}")
+        self.tier_name = _tier_name(tier)
+        self.n_envs = int(n_envs)
+        self.obs_mode = obs_mode
+        self.seed = int(seed)
+        self._batch = GridrogueBatch(self.n_envs, self.tier_name, self.seed, obs_mode,
+                                     max_episode_length, tile_px, device)
+        self._stepping = threading.Lock()
+        self._ready = False
+        import torch
+        n = self.n_envs
+        t = TIERS[self.tier_name]
+        pin = dict(pin_memory=True)
+        if obs_mode == "symbolic":
+            self._h_obs = torch.empty((n, t["obs"]), dtype=torch.float32, **pin).numpy()
+        elif obs_mode == "pixels":
+            self._h_obs = torch.empty((n,) + pixel_shape(self.tier_name, self._batch.tile_px),
+                                      dtype=torch.uint8, **pin).numpy()
+        else:
+            self._h_obs = np.zeros((n, 0), np.float32)
+        self._h_act = torch.empty(n, dtype=torch.int64, **pin).numpy()
+        self._h_rew = torch.empty(n, dtype=torch.float32, **pin).numpy()
+        self._h_done = torch.empty(n, dtype=torch.bool, **pin).numpy()
+        self._h_newly = torch.empty((n, t["n_achievements"]), dtype=torch.bool, **pin).numpy()
+        self._h_time = torch.empty(n, dtype=torch.int32, **pin).numpy()
+        self._h_floor = torch.empty(n, dtype=torch.uint8, **pin).numpy()
+
+    @property
+    def n_actions(self) -> int:
+        return TIERS[self.tier_name]["n_actions"]
+
+    @property
+    def obs_width(self) -> int:
+        if self.obs_mode == "symbolic":
+            return TIERS[self.tier_name]["obs"]
+        if self.obs_mode == "pixels":
+            return int(np.prod(pixel_shape(self.tier_name, self._batch.tile_px)))
+        return 0
+
+    @property
+    def batch(self) -> GridrogueBatch:
+        return self._batch
+
+    def _vp(self, a):
+        return a.ctypes.data_as(ctypes.c_void_p)
+
+    def reset(self) -> np.ndarray:
+        obs_p = self._vp(self._h_obs) if self.obs_mode != "none" else None
+        check(lib().gr_reset_host(self._batch.h, obs_p))
+        self._ready = True
+        return self._h_obs.copy()
+
+    def step(self, actions):
+        if not self._ready:
+            raise RuntimeError("call reset() before step()")
+        if not self._stepping.acquire(blocking=False):
+            raise RuntimeError("BatchEnv is single-owner: concurrent step() calls are not allowed")
+        try:
+            actions = np.ascontiguousarray(actions, dtype=np.int64)
+            if actions.shape != (self.n_envs,):
+                raise ValueError(f"actions must have shape ({self.n_envs},), got {actions.shape}")
+            bad = (actions < 0) | (actions >= self.n_actions)
+            if bad.any():
+                i = int(np.argmax(bad))
+                raise ValueError(f"invalid action {int(actions[i])} for env {i}")
+            np.copyto(self._h_act, actions)
+            obs_p = self._vp(self._h_obs) if self.obs_mode != "none" else None
+            check(lib().gr_step_host(self._batch.h, self._vp(self._h_act), obs_p, self._vp(self._h_rew),
+                                     self._vp(self._h_done), self._vp(self._h_newly),
+                                     self._vp(self._h_time), self._vp(self._h_floor)))
+            info = {"time": self._h_time.view(np.uint32).copy(), "floor": self._h_floor.copy(),
+                    "newly_unlocked": self._h_newly.copy(),
+                    "episodes_completed": self._batch.episodes_completed()}
+            return self._h_obs.copy(), self._h_rew.copy(), self._h_done.copy(), info
+        finally:
+            self._stepping.release()
+
+    def level_seeds(self) -> np.ndarray:
+        return self._batch.level_seeds()
