@@ -170,6 +170,10 @@ int gr_level_seeds(gr_env *env, uint64_t *host_dst);          /* BatchState.leve
 int gr_episodes_completed(gr_env *env, int64_t *out);         /* info["episodes_completed"] */
 /* count of kernels this library launched since creation (bench evidence) */
 int64_t gr_kernel_launches(const gr_env *env);
+/* per-kernel device timing with CUDA events on the launching stream:
+ * classes 0..7 = step, scan, info, worldgen, install, obs, policy, other */
+int gr_set_profiling(gr_env *env, int32_t on);
+int gr_kernel_times(gr_env *env, double *ms, int64_t *counts, int32_t n_classes);
 /* worldgen diagnostics: [worlds generated, floors retried, template floors,
  * potion argsort ties, numerically fragile cave floors] */
 int gr_worldgen_counters(gr_env *env, int64_t out[5]);

@@ -99,6 +99,8 @@ def lib() -> ctypes.CDLL:
         "gr_episodes_completed": (I32, [P, ctypes.POINTER(I64)]),
         "gr_kernel_launches": (I64, [P]),
         "gr_worldgen_counters": (I32, [P, ctypes.POINTER(I64)]),
+        "gr_set_profiling": (I32, [P, I32]),
+        "gr_kernel_times": (I32, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64), I32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

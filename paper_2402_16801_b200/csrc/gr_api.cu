@@ -97,7 +97,27 @@ static int fail(int code, const char* fmt, ...) {
     if (e_ != cudaSuccess) return fail(GR_E_CUDA, "%s: %s", #x, cudaGetErrorString(e_));   \
   } while (0)
 
+// per-kernel CUDA-event timing (gr_set_profiling / gr_kernel_times)
+enum { PK_STEP, PK_SCAN, PK_INFO, PK_WORLDGEN, PK_INSTALL, PK_OBS, PK_POLICY, PK_OTHER, PK_N };
+
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[PK_N];
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t x;
+      cudaEventCreate(&x);
+      return x;
+    }
+    cudaEvent_t x = pool.back();
+    pool.pop_back();
+    return x;
+  }
+};
+
 struct gr_env {
+  Prof prof;
   gr_config cfg;
   bool ext;
   TierDims d;
@@ -126,6 +146,28 @@ struct gr_env {
   uint32_t* h_time_dev = nullptr;
   cudaStream_t h_stream = nullptr;
   std::vector<void*> allocs;
+};
+
+// records a (start, stop) event pair around one launch when profiling
+struct PTimer {
+  gr_env* e;
+  int cls;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  PTimer(gr_env* e_, int cls_, cudaStream_t st_) : e(e_), cls(cls_), st(st_) {
+    if (e->prof.on) {
+      a = e->prof.get();
+      b = e->prof.get();
+      cudaEventRecord(a, st);
+    }
+    e->launches++;
+  }
+  ~PTimer() {
+    if (a) {
+      cudaEventRecord(b, st);
+      e->prof.ev[cls].push_back({a, b});
+    }
+  }
 };
 
 static int64_t obs_elems_of(const gr_env* e) {
@@ -256,13 +298,15 @@ static int observe(gr_env* e, void* obs_dev, cudaStream_t st, bool recompute_fla
   if (!obs_dev || e->cfg.obs_mode == GR_OBS_NONE) return GR_OK;
   if (recompute_flags) {
     CK(cudaMemsetAsync(e->cur_flags, 0, sizeof(uint32_t), st));
+    PTimer t(e, PK_OTHER, st);
     k_dark<<<(unsigned)e->nb, 128, 0, st>>>(e->S, e->n, e->cur_flags);
-    e->launches++;
   }
   ObsArgs oa{obs_dev, e->n, recompute_flags ? e->cur_flags : e->prev_flags, e->cfg.tile_px};
-  if (e->cfg.obs_mode == GR_OBS_SYMBOLIC) launch_symbolic(e->ext, e->S, oa, st);
-  else launch_pixels(e->ext, e->S, oa, st);
-  e->launches++;
+  {
+    PTimer t(e, PK_OBS, st);
+    if (e->cfg.obs_mode == GR_OBS_SYMBOLIC) launch_symbolic(e->ext, e->S, oa, st);
+    else launch_pixels(e->ext, e->S, oa, st);
+  }
   CK(cudaGetLastError());
   return GR_OK;
 }
@@ -285,9 +329,14 @@ int gr_reset(gr_env* e, void* obs_dev, void* stream) {
   j.M = e->M;
   j.out = WBuf{(uint8_t*)e->S.f[GR_F_BLOCKS], (uint8_t*)e->S.f[GR_F_ITEMS], e->init_meta, e->n};
   j.counters = e->counters;
-  launch_worldgen(e->ext, j, st);
-  launch_install_initial(e->ext, e->S, j.out, e->n, st);
-  e->launches += 2;
+  {
+    PTimer t(e, PK_WORLDGEN, st);
+    launch_worldgen(e->ext, j, st);
+  }
+  {
+    PTimer t(e, PK_INSTALL, st);
+    launch_install_initial(e->ext, e->S, j.out, e->n, st);
+  }
   CK(cudaMemsetAsync(e->prev_flags, 0, sizeof(uint32_t), st));
   CK(cudaMemsetAsync(e->st_episodes, 0, sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(e->st_steps, 0, sizeof(unsigned long long), st));
@@ -302,9 +351,9 @@ int gr_reset(gr_env* e, void* obs_dev, void* stream) {
 int gr_random_actions(gr_env* e, uint32_t seed, uint64_t t, int64_t* actions_dev, void* stream) {
   if (!e || !actions_dev) return fail(GR_E_INVALID, "null argument");
   const uint32_t key = (uint32_t)((uint64_t)seed + t * 2654435761ull);
+  PTimer tm(e, PK_POLICY, (cudaStream_t)stream);
   k_random_actions<<<(unsigned)((e->n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       actions_dev, e->n, e->cfg.env_offset, key, e->d.NA);
-  e->launches++;
   CK(cudaGetLastError());
   return GR_OK;
 }
@@ -317,8 +366,10 @@ int gr_step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, uint
   cudaStream_t st = (cudaStream_t)stream;
   if (e->validate) {
     CK(cudaMemsetAsync(e->bad, 0xFF, sizeof(unsigned long long), st));
-    k_validate<<<(unsigned)((e->n + 255) / 256), 256, 0, st>>>(actions_dev, e->n, e->d.NA, e->bad);
-    e->launches++;
+    {
+      PTimer t(e, PK_OTHER, st);
+      k_validate<<<(unsigned)((e->n + 255) / 256), 256, 0, st>>>(actions_dev, e->n, e->d.NA, e->bad);
+    }
     unsigned long long bad = 0;
     CK(cudaMemcpyAsync(&bad, e->bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -344,9 +395,14 @@ int gr_step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, uint
   a.cur_flags = e->cur_flags;
   a.block_done = e->block_done;
   a.bad = nullptr;
-  launch_step(e->ext, e->S, a, st);
-  launch_scan(e->block_done, e->block_off, (int)e->nb, e->cur_flags, exchange_dev ? exchange_dev : e->exchange, st);
-  e->launches += 2;
+  {
+    PTimer t(e, PK_STEP, st);
+    launch_step(e->ext, e->S, a, st);
+  }
+  {
+    PTimer t(e, PK_SCAN, st);
+    launch_scan(e->block_done, e->block_off, (int)e->nb, e->cur_flags, exchange_dev ? exchange_dev : e->exchange, st);
+  }
   CK(cudaGetLastError());
   return GR_OK;
 }
@@ -358,15 +414,21 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
   cudaStream_t st = (cudaStream_t)stream;
   // WorldPool(pool_key, step_index + 1, M) (batch.py:217)
   const uint64_t step_key = hash2(e->pool_key, (uint64_t)(e->step_index + 1));
-  launch_finish_info(exchange_all_dev ? exchange_all_dev : e->exchange, rank, world, e->M, step_key, e->info,
-                     e->prev_flags, st);
+  {
+    PTimer t(e, PK_INFO, st);
+    launch_finish_info(exchange_all_dev ? exchange_all_dev : e->exchange, rank, world, e->M, step_key, e->info,
+                       e->prev_flags, st);
+  }
   WorldJob j{};
   j.mode = 1;
   j.info = e->info;
   j.M = e->M;
   j.out = e->pool;
   j.counters = e->counters;
-  launch_worldgen(e->ext, j, st);
+  {
+    PTimer t(e, PK_WORLDGEN, st);
+    launch_worldgen(e->ext, j, st);
+  }
   InstallArgs ia{};
   ia.mode = 1;
   ia.n = e->n;
@@ -377,8 +439,10 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
   ia.st_steps = e->st_steps;
   ia.st_return = e->st_return;
   ia.st_ach = e->st_ach;
-  launch_install_pool(e->ext, e->S, ia, e->block_off, st);
-  e->launches += 3;
+  {
+    PTimer t(e, PK_INSTALL, st);
+    launch_install_pool(e->ext, e->S, ia, e->block_off, st);
+  }
   CK(cudaGetLastError());
   e->step_index += 1;
   return observe(e, obs_dev, st, false);
@@ -458,8 +522,10 @@ int gr_step_host(gr_env* e, const int64_t* actions_host, void* obs_host, float* 
 }
 
 static int materialize(gr_env* e) {
-  k_materialize<<<(unsigned)e->nb, 128>>>(e->S, e->n, e->d.F, e->prev_flags);
-  e->launches++;
+  {
+    PTimer t(e, PK_OTHER, 0);
+    k_materialize<<<(unsigned)e->nb, 128>>>(e->S, e->n, e->d.F, e->prev_flags);
+  }
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   return GR_OK;
@@ -559,6 +625,36 @@ int gr_episodes_completed(gr_env* e, int64_t* out) {
 }
 
 int gr_level_seeds(gr_env* e, uint64_t* host_dst) { return gr_export_field(e, GR_F_PARAMS_SEED, host_dst); }
+
+int gr_set_profiling(gr_env* e, int32_t on) {
+  if (!e) return fail(GR_E_INVALID, "null env");
+  e->prof.on = on != 0;
+  return GR_OK;
+}
+
+// per kernel class: summed device milliseconds and launch counts since the
+// last call (classes: step, scan, info, worldgen, install, obs, policy, other)
+int gr_kernel_times(gr_env* e, double* ms, int64_t* counts, int32_t n) {
+  if (!e) return fail(GR_E_INVALID, "null env");
+  CK(cudaSetDevice(e->cfg.device));
+  CK(cudaDeviceSynchronize());
+  for (int c = 0; c < PK_N; ++c) {
+    double tot = 0;
+    for (auto& p : e->prof.ev[c]) {
+      float x = 0;
+      cudaEventElapsedTime(&x, p.first, p.second);
+      tot += x;
+      e->prof.pool.push_back(p.first);
+      e->prof.pool.push_back(p.second);
+    }
+    if (c < n) {
+      if (ms) ms[c] = tot;
+      if (counts) counts[c] = (int64_t)e->prof.ev[c].size();
+    }
+    e->prof.ev[c].clear();
+  }
+  return GR_OK;
+}
 
 int gr_worldgen_counters(gr_env* e, int64_t out[5]) {
   if (!e || !out) return fail(GR_E_INVALID, "null argument");

@@ -207,6 +207,19 @@ class GridrogueBatch:
     def kernel_launches(self) -> int:
         return int(lib().gr_kernel_launches(self.h))
 
+    KERNEL_CLASSES = ("step", "scan", "info", "worldgen", "install", "obs", "policy", "other")
+
+    def set_profiling(self, on: bool) -> None:
+        check(lib().gr_set_profiling(self.h, 1 if on else 0))
+
+    def kernel_times(self) -> dict:
+        """{class: (device ms, launches)} since the last call (CUDA events)."""
+        k = len(self.KERNEL_CLASSES)
+        ms = (ctypes.c_double * k)()
+        cnt = (ctypes.c_int64 * k)()
+        check(lib().gr_kernel_times(self.h, ms, cnt, k))
+        return {c: (ms[i], cnt[i]) for i, c in enumerate(self.KERNEL_CLASSES)}
+
     def worldgen_counters(self) -> dict:
         c = (ctypes.c_int64 * 5)()
         check(lib().gr_worldgen_counters(self.h, c))
