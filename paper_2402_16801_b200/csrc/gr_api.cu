@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdarg>
+#include <cstdlib>
 #include <string>
 #include <vector>
 #include <algorithm>
@@ -145,6 +146,12 @@ struct gr_env {
   uint8_t *h_done_dev = nullptr, *h_newly_dev = nullptr, *h_floor_dev = nullptr;
   uint32_t* h_time_dev = nullptr;
   cudaStream_t h_stream = nullptr;
+  // reset work (worldgen + install + obs of reset envs) overlaps the obs of
+  // the other envs on a second stream
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  const uint8_t* last_done = nullptr;
+  bool overlap = true;
   std::vector<void*> allocs;
 };
 
@@ -206,8 +213,13 @@ int gr_field_info(int32_t tier, int32_t field, int64_t* elems_per_env, int32_t* 
 void gr_destroy(gr_env* e) {
   if (!e) return;
   cudaSetDevice(e->cfg.device);
+  cudaDeviceSynchronize();
   for (void* p : e->allocs) cudaFree(p);
   if (e->h_stream) cudaStreamDestroy(e->h_stream);
+  if (e->side) cudaStreamDestroy(e->side);
+  if (e->ev_fork) cudaEventDestroy(e->ev_fork);
+  if (e->ev_join) cudaEventDestroy(e->ev_join);
+  for (auto x : e->prof.pool) cudaEventDestroy(x);
   delete e;
 }
 
@@ -232,6 +244,7 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   e->cfg = *cfg;
   e->cfg.n_envs_global = ng;
   if (e->cfg.max_episode_length <= 0) e->cfg.max_episode_length = 100000;
+  if (const char* ov = getenv("GR_OVERLAP")) e->overlap = atoi(ov) != 0;
   e->ext = cfg->tier == GR_TIER_EXTENDED;
   e->d = e->ext ? EXT_DIMS : CLASSIC_DIMS;
   e->n = cfg->n_envs;
@@ -264,6 +277,12 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->st_steps, sizeof(unsigned long long));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->st_ach, 67 * sizeof(unsigned long long));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->st_return, sizeof(double));
+  if (rc == GR_OK) {
+    if (cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess)
+      rc = fail(GR_E_CUDA, "stream/event creation failed");
+  }
   if (rc != GR_OK) {
     gr_destroy(e);
     return rc;
@@ -294,14 +313,15 @@ int gr_bad_action(const gr_env* e, int64_t* env_index, int64_t* action) {
   return GR_OK;
 }
 
-static int observe(gr_env* e, void* obs_dev, cudaStream_t st, bool recompute_flags) {
+// sel: 0 every env, 1 envs not reset this step, 2 envs reset this step
+static int observe(gr_env* e, void* obs_dev, cudaStream_t st, bool recompute_flags, int sel = 0) {
   if (!obs_dev || e->cfg.obs_mode == GR_OBS_NONE) return GR_OK;
   if (recompute_flags) {
     CK(cudaMemsetAsync(e->cur_flags, 0, sizeof(uint32_t), st));
     PTimer t(e, PK_OTHER, st);
     k_dark<<<(unsigned)e->nb, 128, 0, st>>>(e->S, e->n, e->cur_flags);
   }
-  ObsArgs oa{obs_dev, e->n, recompute_flags ? e->cur_flags : e->prev_flags, e->cfg.tile_px};
+  ObsArgs oa{obs_dev, e->n, recompute_flags ? e->cur_flags : e->prev_flags, e->cfg.tile_px, e->last_done, sel};
   {
     PTimer t(e, PK_OBS, st);
     if (e->cfg.obs_mode == GR_OBS_SYMBOLIC) launch_symbolic(e->ext, e->S, oa, st);
@@ -395,6 +415,7 @@ int gr_step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, uint
   a.cur_flags = e->cur_flags;
   a.block_done = e->block_done;
   a.bad = nullptr;
+  e->last_done = done_dev;
   {
     PTimer t(e, PK_STEP, st);
     launch_step(e->ext, e->S, a, st);
@@ -419,6 +440,13 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
     launch_finish_info(exchange_all_dev ? exchange_all_dev : e->exchange, rank, world, e->M, step_key, e->info,
                        e->prev_flags, st);
   }
+  // reset work on the side stream, overlapping the obs of the other envs
+  const bool split = e->overlap && obs_dev && e->cfg.obs_mode != GR_OBS_NONE && e->last_done;
+  cudaStream_t rs = split ? e->side : st;
+  if (split) {
+    CK(cudaEventRecord(e->ev_fork, st));
+    CK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+  }
   WorldJob j{};
   j.mode = 1;
   j.info = e->info;
@@ -426,8 +454,8 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
   j.out = e->pool;
   j.counters = e->counters;
   {
-    PTimer t(e, PK_WORLDGEN, st);
-    launch_worldgen(e->ext, j, st);
+    PTimer t(e, PK_WORLDGEN, rs);
+    launch_worldgen(e->ext, j, rs);
   }
   InstallArgs ia{};
   ia.mode = 1;
@@ -440,12 +468,19 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
   ia.st_return = e->st_return;
   ia.st_ach = e->st_ach;
   {
-    PTimer t(e, PK_INSTALL, st);
-    launch_install_pool(e->ext, e->S, ia, e->block_off, st);
+    PTimer t(e, PK_INSTALL, rs);
+    launch_install_pool(e->ext, e->S, ia, e->block_off, rs);
   }
   CK(cudaGetLastError());
   e->step_index += 1;
-  return observe(e, obs_dev, st, false);
+  if (!split) return observe(e, obs_dev, st, false);
+  int rc = observe(e, obs_dev, rs, false, 2);   // reset envs, after their install
+  if (rc) return rc;
+  rc = observe(e, obs_dev, st, false, 1);       // everyone else, concurrently
+  if (rc) return rc;
+  CK(cudaEventRecord(e->ev_join, e->side));
+  CK(cudaStreamWaitEvent(st, e->ev_join, 0));
+  return GR_OK;
 }
 
 int gr_step(gr_env* e, const int64_t* actions_dev, void* obs_dev, float* reward_dev, uint8_t* done_dev,

@@ -63,6 +63,8 @@ struct ObsArgs {
   int64_t n;
   const uint32_t* flags;    // bit2: some env stands on a dark floor (glow on)
   int tile_px;
+  const uint8_t* done;      // this step's done flags (for sel 1/2)
+  int sel;                  // 0: every env, 1: envs not reset this step, 2: envs reset this step
 };
 
 void launch_step(bool ext, const DS& S, const StepArgs& a, cudaStream_t st);

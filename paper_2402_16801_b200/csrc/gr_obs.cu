@@ -91,34 +91,45 @@ __device__ void build_view(const DS& S, int64_t i, bool glow, ViewSmem<EXT>& v) 
   }
   if (sleeping)
     for (int t = lane; t < O::T; t += 32) v.light[t] = 0.0f;
-  // creature channels: later lanes overwrite earlier ones (obs.py:263-296)
-  if (lane == 0) {
-    auto paint = [&](int r, int c, bool alive, int ch) {
-      const int wr = r - r0, wc = c - c0;
-      if (alive && wr >= 0 && wr < O::VR && wc >= 0 && wc < O::VC) v.cre[wr * O::VC + wc] = (uint8_t)ch;
-    };
-    const int cls_fid[3] = {GR_F_MEL_POS, GR_F_RAN_POS, GR_F_PAS_POS};
-    const int caps[3] = {3, 2, 3};
-    for (int cls = 0; cls < 3; ++cls) {
-      const int fp = cls_fid[cls], cap = caps[cls];
-      const int fa = cls < 2 ? fp + 3 : fp + 2, ft = cls < 2 ? fp + 4 : fp + 3;
-      for (int l = 0; l < cap; ++l) {
-        const int lanei = pf * cap + l;
-        const int ty = GR_AT(S, ft, uint8_t, lanei, i);
-        int ch;
-        if (EXT) ch = ty + 1;
-        else ch = ty == 0 ? 1 : ty == 2 ? 2 : ty == 1 ? 3 : 0;
-        paint(GR_AT(S, fp, int16_t, 2 * lanei, i), GR_AT(S, fp, int16_t, 2 * lanei + 1, i),
-              GR_AT(S, fa, uint8_t, lanei, i), ch);
+  // creature channels (obs.py:263-296): lane s loads slot s in parallel
+  // (melee 0-2, ranged 3-4, passive 5-7, enemy proj 8-10, player proj 11-13);
+  // the paint order -- later slots overwrite earlier ones -- is kept by
+  // letting the highest slot index win each cell
+  {
+    constexpr int NSLOT = EXT ? 14 : 11;
+    int cell = -1, ch = 0;
+    if (lane < NSLOT) {
+      int r = 0, c = 0, alive = 0;
+      if (lane < 8) {
+        const int cls = lane < 3 ? 0 : lane < 5 ? 1 : 2;
+        const int l = lane - (cls == 0 ? 0 : cls == 1 ? 3 : 5), cap = cls == 1 ? 2 : 3;
+        const int fp = cls == 0 ? GR_F_MEL_POS : cls == 1 ? GR_F_RAN_POS : GR_F_PAS_POS;
+        const int fa = cls < 2 ? fp + 3 : fp + 2, ft = cls < 2 ? fp + 4 : fp + 3;
+        const int li = pf * cap + l;
+        r = GR_AT(S, fp, int16_t, 2 * li, i);
+        c = GR_AT(S, fp, int16_t, 2 * li + 1, i);
+        alive = GR_AT(S, fa, uint8_t, li, i);
+        const int ty = GR_AT(S, ft, uint8_t, li, i);
+        ch = EXT ? ty + 1 : (ty == 0 ? 1 : ty == 2 ? 2 : ty == 1 ? 3 : 0);
+      } else {
+        const bool ep = lane < 11;
+        const int l = ep ? lane - 8 : lane - 11;
+        const int fp = ep ? GR_F_EPROJ_POS : GR_F_PPROJ_POS;
+        r = GR_AT(S, fp, int16_t, 2 * l, i);
+        c = GR_AT(S, fp, int16_t, 2 * l + 1, i);
+        alive = GR_AT(S, ep ? GR_F_EPROJ_ALIVE : GR_F_PPROJ_ALIVE, uint8_t, l, i);
+        ch = EXT ? GR_AT(S, ep ? GR_F_EPROJ_TYPE : GR_F_PPROJ_TYPE, uint8_t, l, i) + 20 : 4;
       }
+      const int wr = r - r0, wc = c - c0;
+      if (alive && wr >= 0 && wr < O::VR && wc >= 0 && wc < O::VC) cell = wr * O::VC + wc;
     }
-    for (int l = 0; l < 3; ++l)
-      paint(GR_AT(S, GR_F_EPROJ_POS, int16_t, 2 * l, i), GR_AT(S, GR_F_EPROJ_POS, int16_t, 2 * l + 1, i),
-            GR_AT(S, GR_F_EPROJ_ALIVE, uint8_t, l, i), EXT ? GR_AT(S, GR_F_EPROJ_TYPE, uint8_t, l, i) + 20 : 4);
-    if (EXT)
-      for (int l = 0; l < 3; ++l)
-        paint(GR_AT(S, GR_F_PPROJ_POS, int16_t, 2 * l, i), GR_AT(S, GR_F_PPROJ_POS, int16_t, 2 * l + 1, i),
-              GR_AT(S, GR_F_PPROJ_ALIVE, uint8_t, l, i), GR_AT(S, GR_F_PPROJ_TYPE, uint8_t, l, i) + 20);
+    // later slots win: a slot paints unless a higher slot targets the same cell
+    bool win = cell >= 0;
+    for (int s = 1; s < NSLOT; ++s) {
+      const int oc = __shfl_down_sync(0xffffffffu, cell, s);
+      if (lane + s < NSLOT && oc == cell) win = false;
+    }
+    if (win) v.cre[cell] = (uint8_t)ch;
   }
   // inventory section (obs._scaled_inventory, obs.py:300-340)
   for (int k = lane; k < O::NINV; k += 32) {
@@ -214,6 +225,37 @@ __device__ __forceinline__ float sym_value(const ViewSmem<EXT>& v, int p) {
   return k < O::NINV ? v.inv[k] : 0.0f;
 }
 
+// zero one obs row with 16-byte stores (head/tail peeled: classic rows are
+// only 4-byte aligned)
+__device__ __forceinline__ void zero_row(float* row, int L, int lane) {
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(row);
+  const int head = (int)(((16u - (unsigned)(addr & 15u)) & 15u) >> 2);
+  if (lane < head && lane < L) row[lane] = 0.0f;
+  const int nv = (L - head) >> 2;
+  float4* r4 = reinterpret_cast<float4*>(row + head);
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int q = lane; q < nv; q += 32) r4[q] = z;
+  const int t0 = head + nv * 4;
+  if (t0 + lane < L) row[t0 + lane] = 0.0f;
+}
+
+// the non-zero entries of encode_symbolic_batch (obs.py:364-385)
+template <bool EXT>
+__device__ __forceinline__ void scatter_row(const ViewSmem<EXT>& v, float* row, int lane) {
+  using O = OT<EXT>;
+  for (int t = lane; t < O::T; t += 32) {
+    float* tv = row + t * O::STRIDE;
+    const float l = v.light[t];
+    if (l >= 0.05f) {
+      tv[EXT ? v.blk[t] : C_CLASSIC_LOCAL[v.blk[t]]] = 1.0f;
+      if (EXT) tv[O::BCH + v.itm[t]] = 1.0f;
+      tv[O::BCH + O::ICH + v.cre[t]] = 1.0f;
+    }
+    tv[O::STRIDE - 1] = l;
+  }
+  for (int k = lane; k < O::NINV; k += 32) row[O::T * O::STRIDE + k] = v.inv[k];
+}
+
 template <bool EXT>
 __global__ void __launch_bounds__(OBS_WARPS * 32) k_symbolic(DS S, ObsArgs a) {
   using O = OT<EXT>;
@@ -222,20 +264,16 @@ __global__ void __launch_bounds__(OBS_WARPS * 32) k_symbolic(DS S, ObsArgs a) {
   ViewSmem<EXT>& v = views[warp];
   const bool glow = EXT && a.flags && (a.flags[0] & 4u);
   for (int64_t i = (int64_t)blockIdx.x * OBS_WARPS + warp; i < a.n; i += (int64_t)gridDim.x * OBS_WARPS) {
-    build_view<EXT>(S, i, glow, v);
+    if (a.sel && (a.done[i] != 0) != (a.sel == 2)) continue;   // warp-uniform env filter
     float* row = (float*)a.out + (size_t)i * O::L;
-    if (EXT) {
-      // 8268 floats = 2067 float4, rows 16-byte aligned
-      float4* r4 = reinterpret_cast<float4*>(row);
-      for (int q = lane; q < O::L / 4; q += 32) {
-        const int p = 4 * q;
-        float4 val = make_float4(sym_value<EXT>(v, p), sym_value<EXT>(v, p + 1), sym_value<EXT>(v, p + 2),
-                                 sym_value<EXT>(v, p + 3));
-        __stcs(r4 + q, val);
-      }
-    } else {
-      for (int p = lane; p < O::L; p += 32) __stcs(row + p, sym_value<EXT>(v, p));
-    }
+    // 1) the row is ~95% zeros: stream zeros with 16-byte stores first
+    //    (fire-and-forget; they overlap the view loads below)
+    zero_row(row, O::L, lane);
+    // 2) egocentric view + inventory into shared memory
+    build_view<EXT>(S, i, glow, v);
+    __syncwarp();   // orders the zero stores before the scatter (same lines)
+    // 3) scatter the <= 4 non-zeros per tile and the inventory section
+    scatter_row<EXT>(v, row, lane);
     __syncwarp();
   }
 }
@@ -288,6 +326,7 @@ __global__ void __launch_bounds__(128) k_pixels(DS S, ObsArgs a) {
   const int inset = max(1, px / 4);
   const int64_t frame = (int64_t)FH * FW * 3;
   for (int64_t i = blockIdx.x; i < a.n; i += gridDim.x) {
+    if (a.sel && (a.done[i] != 0) != (a.sel == 2)) continue;   // CTA-uniform env filter
     if (threadIdx.x < 32) {
       // render_tiles sees a one-env batch: glow iff this env's floor is dark
       const int pf = EXT ? GR_AT(S, GR_F_PFLOOR, uint8_t, 0, i) : 0;
