@@ -259,6 +259,7 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.cd_pending, e->n);
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.ep_return, e->n * sizeof(double));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.ep_length, e->n * sizeof(int32_t));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.desc, e->n * 256);
   const int64_t cap = std::min(e->n, e->M);
   const size_t wbytes = (size_t)cap * e->d.F * e->d.H * e->d.W;
   e->pool.cap = cap;
@@ -630,6 +631,10 @@ int gr_import_field(gr_env* e, int32_t field, const void* host_src) {
 int gr_observe(gr_env* e, void* obs_dev, void* stream) {
   if (!e) return fail(GR_E_INVALID, "null env");
   CK(cudaSetDevice(e->cfg.device));
+  {
+    PTimer t(e, PK_OTHER, (cudaStream_t)stream);
+    launch_make_desc(e->ext, e->S, e->n, (cudaStream_t)stream);
+  }
   return observe(e, obs_dev, (cudaStream_t)stream, true);
 }
 

@@ -13,6 +13,7 @@
 #include "gr_device.cuh"
 #include "gr_state.cuh"
 #include "gr_kernels.cuh"
+#include "gr_desc.cuh"
 
 namespace gr {
 
@@ -37,14 +38,6 @@ struct ViewSmem {
   float inv[OT<EXT>::NINV];
 };
 
-// obs.daylight (obs.py:191-195): float32 with numpy's SIMD sin
-__device__ __forceinline__ float daylight(uint32_t time) {
-  float phase = __fdiv_rn((float)(time % 300u), 300.0f);
-  float m = phase < 0.5f ? phase : 0.5f;
-  float arg = __fmul_rn(__fmul_rn(3.14159274101257324f, m), 2.0f);
-  float lift = np_sincosf(arg, false);
-  return __fadd_rn(0.150000006f, __fmul_rn(0.850000024f, lift > 0.0f ? lift : 0.0f));
-}
 
 __constant__ int8_t C_CLASSIC_LOCAL[37] = {0, 0, 1, 2, 3, 4, 0, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 0, 0,
                                            0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -413,6 +406,128 @@ __global__ void __launch_bounds__(128) k_pixels(DS S, ObsArgs a) {
   }
 }
 
+// ---------------------------------------------------- descriptor writer
+// One warp per env: the 256-byte descriptor + the view window of the maps
+// become, per tile, three one-hot channel targets (pre-masked by the light
+// threshold) and the light scalar in shared memory; the row is then
+// produced as 16-byte vectors, each value computed in registers and every
+// byte of the row written exactly once with full-line stores.
+template <bool EXT>
+struct TileSmem {
+  uint32_t tgt[OT<EXT>::T];   // on-channels: 3 x 8 bits (0xFF = none)
+  float light[OT<EXT>::T];
+  float inv[OT<EXT>::NINV];
+  uint32_t desc[DESC_WORDS];
+};
+
+template <bool EXT>
+__device__ __forceinline__ float desc_value(const TileSmem<EXT>& v, int p) {
+  using O = OT<EXT>;
+  if (p < O::T * O::STRIDE) {
+    const int t = p / O::STRIDE, o = p - t * O::STRIDE;
+    const uint32_t g = v.tgt[t];
+    if (o == O::STRIDE - 1) return v.light[t];
+    return (o == (int)(g & 0xFF) || o == (int)((g >> 8) & 0xFF) || o == (int)(g >> 16)) ? 1.0f : 0.0f;
+  }
+  const int k = p - O::T * O::STRIDE;
+  return k < O::NINV ? v.inv[k] : 0.0f;
+}
+
+template <bool EXT>
+__global__ void __launch_bounds__(OBS_WARPS * 32) k_symbolic_desc(DS S, ObsArgs a) {
+  using O = OT<EXT>;
+  __shared__ TileSmem<EXT> views[OBS_WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  TileSmem<EXT>& v = views[warp];
+  const bool glow = EXT && a.flags && (a.flags[0] & 4u);
+  for (int64_t i = (int64_t)blockIdx.x * OBS_WARPS + warp; i < a.n; i += (int64_t)gridDim.x * OBS_WARPS) {
+    if (a.sel && (a.done[i] != 0) != (a.sel == 2)) continue;   // warp-uniform env filter
+    // descriptor: 256 contiguous bytes, 8 per lane
+    const uint2 dw = reinterpret_cast<const uint2*>(S.desc + (size_t)i * DESC_WORDS)[lane];
+    v.desc[2 * lane] = dw.x;
+    v.desc[2 * lane + 1] = dw.y;
+    __syncwarp();
+    const uint32_t pos = v.desc[D_POS], fl = v.desc[D_FLAGS];
+    const int pr = (int16_t)(pos & 0xFFFF), pc = (int16_t)(pos >> 16), pf = fl & 0xFF;
+    const bool sleeping = (fl >> 8) & 1;
+    const float base = __uint_as_float(v.desc[D_BASE]);
+    const uint8_t* blk = (const uint8_t*)S.f[GR_F_BLOCKS] + ((size_t)i * O::F + pf) * O::HW;
+    const uint8_t* itm = (const uint8_t*)S.f[GR_F_ITEMS] + ((size_t)i * O::F + pf) * O::HW;
+    const int r0 = pr - O::VR / 2, c0 = pc - O::VC / 2;
+    uint8_t bq[(O::T + 31) / 32], iq[(O::T + 31) / 32];
+#pragma unroll
+    for (int q = 0; q < (O::T + 31) / 32; ++q) {
+      const int t = lane + 32 * q;
+      const int r = r0 + t / O::VC, c = c0 + t % O::VC;
+      const bool inb = t < O::T && r >= 0 && r < O::H && c >= 0 && c < O::W;
+      bq[q] = inb ? blk[r * O::W + c] : B_OOB;
+      iq[q] = inb && EXT ? itm[r * O::W + c] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < (O::T + 31) / 32; ++q) {
+      const int t = lane + 32 * q;
+      if (t < O::T) v.light[t] = base;
+    }
+    for (int k = lane; k < O::NINV; k += 32) v.inv[k] = __uint_as_float(v.desc[D_INV + k]);
+    __syncwarp();
+    if (glow) {
+      constexpr int WR = O::VR + 6, WC = O::VC + 6;
+      for (int t = lane; t < WR * WC; t += 32) {
+        const int wr = t / WC - 3, wc = t % WC - 3;
+        const int r = r0 + wr, c = c0 + wc;
+        if (r < 0 || r >= O::H || c < 0 || c >= O::W || itm[r * O::W + c] != I_TORCH) continue;
+        for (int aa = max(wr - 3, 0); aa <= min(wr + 3, O::VR - 1); ++aa)
+          for (int bb = max(wc - 3, 0); bb <= min(wc + 3, O::VC - 1); ++bb) {
+            const int d = max(abs(aa - wr), abs(bb - wc));
+            atomicMax(reinterpret_cast<int*>(&v.light[aa * O::VC + bb]), __float_as_int(1.0f - 0.25f * (float)d));
+          }
+      }
+      __syncwarp();
+    }
+    // creature cells: slot lane < 14; the highest slot wins a cell
+    constexpr int NSLOT = EXT ? 14 : 11;
+    uint32_t sl = 0xFFFFu;
+    if (lane < NSLOT) sl = (v.desc[D_CRE + (lane >> 1)] >> (16 * (lane & 1))) & 0xFFFFu;
+    int cell = sl == 0xFFFFu ? -1 : (int)(sl >> 8);
+    bool win = cell >= 0;
+    for (int s = 1; s < NSLOT; ++s) {
+      const int oc = __shfl_down_sync(0xffffffffu, cell, s);
+      if (lane + s < NSLOT && oc == cell) win = false;
+    }
+    // per-tile channel targets, masked by the light threshold
+#pragma unroll
+    for (int q = 0; q < (O::T + 31) / 32; ++q) {
+      const int t = lane + 32 * q;
+      if (t < O::T) {
+        if (sleeping) v.light[t] = 0.0f;
+        const bool lit = v.light[t] >= 0.05f;
+        const uint32_t bc = EXT ? bq[q] : (uint32_t)C_CLASSIC_LOCAL[bq[q]];
+        const uint32_t ic = EXT ? (uint32_t)(O::BCH + iq[q]) : 0xFFu;
+        v.tgt[t] = lit ? (bc | ic << 8 | (uint32_t)(O::BCH + O::ICH) << 16) : 0xFFFFFFu;
+      }
+    }
+    __syncwarp();
+    if (win && (v.tgt[cell] >> 16) != 0xFFu)
+      v.tgt[cell] = (v.tgt[cell] & 0xFFFFu) | ((uint32_t)(O::BCH + O::ICH + (sl & 0xFF)) << 16);
+    __syncwarp();
+    // stream the row out
+    float* row = (float*)a.out + (size_t)i * O::L;
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(row);
+    const int head = (int)(((16u - (unsigned)(addr & 15u)) & 15u) >> 2);
+    if (lane < head) row[lane] = desc_value<EXT>(v, lane);
+    const int nv = (O::L - head) >> 2;
+    float4* r4 = reinterpret_cast<float4*>(row + head);
+    for (int q = lane; q < nv; q += 32) {
+      const int p = head + 4 * q;
+      r4[q] = make_float4(desc_value<EXT>(v, p), desc_value<EXT>(v, p + 1), desc_value<EXT>(v, p + 2),
+                          desc_value<EXT>(v, p + 3));
+    }
+    const int t0 = head + nv * 4;
+    if (t0 + lane < O::L) row[t0 + lane] = desc_value<EXT>(v, t0 + lane);
+    __syncwarp();
+  }
+}
+
 void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
   if (a.n <= 0) return;
   int dev = 0, sms = 148;
@@ -420,8 +535,8 @@ void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t need = (a.n + OBS_WARPS - 1) / OBS_WARPS;
   const int grid = (int)std::min<int64_t>(need, (int64_t)sms * 16);
-  if (ext) k_symbolic<true><<<grid, OBS_WARPS * 32, 0, st>>>(S, a);
-  else k_symbolic<false><<<grid, OBS_WARPS * 32, 0, st>>>(S, a);
+  if (ext) k_symbolic_desc<true><<<grid, OBS_WARPS * 32, 0, st>>>(S, a);
+  else k_symbolic_desc<false><<<grid, OBS_WARPS * 32, 0, st>>>(S, a);
 }
 
 void launch_pixels(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {

@@ -12,6 +12,7 @@
 #include "gr_device.cuh"
 #include "gr_state.cuh"
 #include "gr_kernels.cuh"
+#include "gr_desc.cuh"
 
 namespace gr {
 
@@ -170,6 +171,29 @@ __device__ void install_one(const DS& S, int64_t i, const WMeta& m, const uint8_
     S.cd_pending[i] = 0;
     S.ep_return[i] = 0.0;
     S.ep_length[i] = 0;
+  }
+  // observation descriptor of the fresh episode (gr_desc.cuh)
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    constexpr int NINV = EXT ? 50 : 18;
+    uint32_t* d = S.desc + (size_t)i * DESC_WORDS;
+    __shared__ float inv_s[50];
+    if (lane == 0) {
+      InvSrc s{};
+      s.dex = s.str_ = s.intel = 1;
+      s.facing = 3;
+      s.health = 10.0f; s.food = 13.0f; s.drink = 13.0f; s.energy = 13.0f; s.mana = 17.0f;
+      inv_section<EXT>(s, inv_s);
+    }
+    __syncwarp();
+    for (int k = lane; k < DESC_WORDS; k += 32) {
+      uint32_t w = 0;
+      if (k < NINV) w = __float_as_uint(inv_s[k]);
+      else if (k == D_BASE) w = __float_as_uint(daylight(0));
+      else if (k == D_POS) w = (uint32_t)(uint16_t)m.spawn[0] | ((uint32_t)(uint16_t)m.spawn[1] << 16);
+      else if (k >= D_CRE && k < D_CRE + 7) w = 0xFFFFFFFFu;
+      d[k] = w;
+    }
   }
 #undef Z
 }

@@ -72,6 +72,7 @@ struct DS {
   uint8_t* cd_pending;        // deferred dead-lane cooldown decrements (bits)
   double* ep_return;          // batch.BatchState.ep_return
   int32_t* ep_length;         // batch.BatchState.ep_length
+  uint32_t* desc;             // [ns][64] observation descriptors (gr_desc.cuh)
 };
 
 // one generated world (worldgen.World) in a world buffer

@@ -30,6 +30,7 @@
 #include "gr_device.cuh"
 #include "gr_state.cuh"
 #include "gr_kernels.cuh"
+#include "gr_desc.cuh"
 
 namespace gr {
 
@@ -1123,6 +1124,74 @@ __device__ void grow_plants(Ctx& e) {
   }
 }
 
+// the observation descriptor of this env (gr_desc.cuh) from registers
+template <bool EXT>
+__device__ void write_desc(const Ctx& e, uint32_t* d) {
+  InvSrc s;
+  s.wood = e.inv_wood; s.stone = e.inv_stone; s.coal = e.inv_coal; s.iron = e.inv_iron;
+  s.diamond = e.inv_diamond; s.sapphire = e.inv_sapphire; s.ruby = e.inv_ruby; s.sapling = e.inv_sapling;
+  s.torch = e.inv_torch; s.arrow = e.inv_arrow; s.book = e.inv_book;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) s.potion[k] = e.inv_potion[k];
+  s.pick = e.pick_tier; s.sword = e.sword_tier; s.sword_ench = e.sword_ench; s.has_bow = e.has_bow;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) { s.armour[k] = e.armour[k]; s.armour_ench[k] = e.armour_ench[k]; }
+  s.xp = e.xp; s.dex = e.dex; s.str_ = e.str_; s.intel = e.intel; s.facing = e.facing;
+  s.sleeping = e.sleeping; s.resting = e.resting; s.learned_fire = e.learned_fire; s.learned_ice = e.learned_ice;
+  s.pf = e.pfloor; s.cleared = EXT ? (e.cleared >> e.pfloor) & 1 : 0; s.boss_vuln = EXT ? e.boss_vuln : 0;
+  s.health = e.health; s.food = e.food; s.drink = e.drink; s.energy = e.energy; s.mana = e.mana;
+  s.time = e.time;
+  float inv[50];
+  inv_section<EXT>(s, inv);
+  uint32_t w[DESC_WORDS];
+  constexpr int NINV = EXT ? 50 : 18;
+#pragma unroll
+  for (int k = 0; k < 50; ++k) w[k] = k < NINV ? __float_as_uint(inv[k]) : 0u;
+  w[D_BASE] = __float_as_uint(e.pfloor == 0 ? daylight(e.time) : C_FLOOR_AMB[e.pfloor]);
+  w[D_POS] = (uint32_t)(uint16_t)e.prow | ((uint32_t)(uint16_t)e.pcol << 16);
+  w[D_FLAGS] = (uint32_t)e.pfloor | ((uint32_t)e.sleeping << 8);
+  uint32_t slot[14];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int ch = EXT ? e.lty[q] + 1 : classic_channel(e.lty[q]);
+    slot[q] = cre_slot<EXT>(e.lr[q], e.lc[q], e.lal[q], ch, e.prow, e.pcol);
+  }
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    slot[8 + l] = cre_slot<EXT>(e.epr[l], e.epc[l], e.epal[l], EXT ? e.eptype[l] + 20 : 4, e.prow, e.pcol);
+    slot[11 + l] = EXT ? cre_slot<EXT>(e.ppr[l], e.ppc[l], e.ppal[l], e.pptype[l] + 20, e.prow, e.pcol) : 0xFFFFu;
+  }
+#pragma unroll
+  for (int q = 0; q < 7; ++q) w[D_CRE + q] = slot[2 * q] | (slot[2 * q + 1] << 16);
+  w[60] = w[61] = w[62] = w[63] = 0;
+  uint4* dst = reinterpret_cast<uint4*>(d);
+#pragma unroll
+  for (int q = 0; q < DESC_WORDS / 4; ++q) dst[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+}
+
+// observation descriptors straight from the stored state (after an import,
+// or for gr_observe); the step kernel writes them as a by-product
+template <bool EXT>
+__global__ void __launch_bounds__(128) k_make_desc(DS S, int64_t n) {
+  using T = TD<EXT>;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Ctx e;
+  e.i = i;
+  e.blk = (uint8_t*)S.f[GR_F_BLOCKS] + (size_t)i * T::F * T::HW;
+  e.itm = (uint8_t*)S.f[GR_F_ITEMS] + (size_t)i * T::F * T::HW;
+  load_env<EXT>(e, S);
+  load_lanes<EXT>(e, S, e.pfloor);
+  write_desc<EXT>(e, S.desc + (size_t)i * DESC_WORDS);
+}
+
+void launch_make_desc(bool ext, const DS& S, int64_t n, cudaStream_t st) {
+  const int grid = (int)((n + 127) / 128);
+  if (grid <= 0) return;
+  if (ext) k_make_desc<true><<<grid, 128, 0, st>>>(S, n);
+  else k_make_desc<false><<<grid, 128, 0, st>>>(S, n);
+}
+
 // apply the previous step's deferred dead-lane cooldown decrements to the
 // lanes currently loaded (the pending floor is the env's current floor)
 __device__ __forceinline__ void apply_pending(Ctx& e, uint8_t pend, uint32_t prev_flags) {
@@ -1213,6 +1282,7 @@ __global__ void __launch_bounds__(128) k_step(DS S, StepArgs a) {
       for (int k = 0; k < T::A; ++k) nw[k] = (newly[k >> 5] >> (k & 31)) & 1u;
     }
     if (a.reward64) a.reward64[i] = reward;
+    if (!done) write_desc<EXT>(e, S.desc + (size_t)i * DESC_WORDS);   // reset envs: install writes it
     my_done = done;
     if (EXT && !done && C_FLOOR_AMB[e.pfloor] < 1.0f) my_flags |= 4u;
   }

@@ -58,6 +58,21 @@ def run(tier, n, steps, seed, obs_mode="symbolic", maxlen=None, every=10):
     print("OK", tier, obs_mode, n, steps, "episodes", gb.stats()["episodes"], ob.stats()["episodes"], "%.1fs" % (time.time() - t0), gb.worldgen_counters())
     return True
 
+def observe_check(tier, n, seed):
+    """gr_observe after importing a foreign (oracle) state."""
+    import torch
+    gb = GridrogueBatch(n, tier, seed, "symbolic")
+    gb.reset()
+    ob = O.OracleBatch(tier, n, seed + 1)
+    for k in range(30):
+        ob.step(O.random_actions(seed, k, n, O.TIERS[tier]["NA"]))
+    gb.import_state(ob.state.export_fields())
+    o1 = gb.observe().cpu().numpy()
+    o2 = ob.state.encode_symbolic()
+    ok = np.array_equal(o1, o2)
+    print("observe-after-import", tier, "OK" if ok else "MISMATCH")
+    return ok
+
 if __name__ == "__main__":
     r = True
     r &= run("classic", 256, 200, 0)
@@ -65,4 +80,9 @@ if __name__ == "__main__":
     r &= run("extended", 128, 100, 3, maxlen=16)
     r &= run("classic", 64, 60, 1, obs_mode="pixels")
     r &= run("extended", 64, 60, 2, obs_mode="pixels")
+    r &= observe_check("extended", 64, 5)
+    r &= observe_check("classic", 64, 6)
+    r &= observe_check("extended", 64, 5)
+    r &= observe_check("classic", 64, 6)
     print("ALL OK" if r else "FAILURES")
+
