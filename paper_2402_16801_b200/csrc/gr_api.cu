@@ -151,7 +151,7 @@ struct gr_env {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   const uint8_t* last_done = nullptr;
-  bool overlap = true;
+  bool overlap = false;   // GR_OVERLAP=1: reset work on a side stream (measured slower so far)
   std::vector<void*> allocs;
 };
 

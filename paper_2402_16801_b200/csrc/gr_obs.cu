@@ -528,15 +528,160 @@ __global__ void __launch_bounds__(OBS_WARPS * 32) k_symbolic_desc(DS S, ObsArgs 
   }
 }
 
+// ---------------------------------------------- shared-memory row staging
+// The row is ~95% zeros.  Each warp keeps one zero-initialised copy of a row
+// in shared memory, scatters the <= 4 non-zeros per tile and the inventory
+// into it, copies it out with full-line 16-byte stores, and scatters the
+// zeros back -- O(non-zeros) work per env instead of O(row), and every
+// global byte written exactly once.
+template <bool EXT>
+__host__ __device__ constexpr int stage_warps() { return EXT ? 2 : 8; }
+
+template <bool EXT>
+__global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S, ObsArgs a) {
+  using O = OT<EXT>;
+  constexpr int NW = stage_warps<EXT>();
+  constexpr int ROWF = (O::L + 4 + 3) & ~3;   // floats per staged row (+ alignment shift)
+  extern __shared__ float4 dyn_smem[];
+  __shared__ TileSmem<EXT> views[NW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  TileSmem<EXT>& v = views[warp];
+  float* stage = reinterpret_cast<float*>(dyn_smem) + (size_t)warp * ROWF;
+  for (int q = lane; q < ROWF / 4; q += 32) reinterpret_cast<float4*>(stage)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncwarp();
+  const bool glow = EXT && a.flags && (a.flags[0] & 4u);
+  for (int64_t i = (int64_t)blockIdx.x * NW + warp; i < a.n; i += (int64_t)gridDim.x * NW) {
+    if (a.sel && (a.done[i] != 0) != (a.sel == 2)) continue;   // warp-uniform env filter
+    const uint2 dw = reinterpret_cast<const uint2*>(S.desc + (size_t)i * DESC_WORDS)[lane];
+    v.desc[2 * lane] = dw.x;
+    v.desc[2 * lane + 1] = dw.y;
+    __syncwarp();
+    const uint32_t pos = v.desc[D_POS], fl = v.desc[D_FLAGS];
+    const int pr = (int16_t)(pos & 0xFFFF), pc = (int16_t)(pos >> 16), pf = fl & 0xFF;
+    const bool sleeping = (fl >> 8) & 1;
+    const float base = __uint_as_float(v.desc[D_BASE]);
+    const uint8_t* blk = (const uint8_t*)S.f[GR_F_BLOCKS] + ((size_t)i * O::F + pf) * O::HW;
+    const uint8_t* itm = (const uint8_t*)S.f[GR_F_ITEMS] + ((size_t)i * O::F + pf) * O::HW;
+    const int r0 = pr - O::VR / 2, c0 = pc - O::VC / 2;
+    constexpr int TQ = (O::T + 31) / 32;
+    uint8_t bq[TQ], iq[TQ];
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) {
+      const int t = lane + 32 * q;
+      const int r = r0 + t / O::VC, c = c0 + t % O::VC;
+      const bool inb = t < O::T && r >= 0 && r < O::H && c >= 0 && c < O::W;
+      bq[q] = inb ? blk[r * O::W + c] : B_OOB;
+      iq[q] = inb && EXT ? itm[r * O::W + c] : 0;
+      if (t < O::T) v.light[t] = base;
+    }
+    __syncwarp();
+    if (glow) {
+      constexpr int WR = O::VR + 6, WC = O::VC + 6;
+      for (int t = lane; t < WR * WC; t += 32) {
+        const int wr = t / WC - 3, wc = t % WC - 3;
+        const int r = r0 + wr, c = c0 + wc;
+        if (r < 0 || r >= O::H || c < 0 || c >= O::W || itm[r * O::W + c] != I_TORCH) continue;
+        for (int aa = max(wr - 3, 0); aa <= min(wr + 3, O::VR - 1); ++aa)
+          for (int bb = max(wc - 3, 0); bb <= min(wc + 3, O::VC - 1); ++bb) {
+            const int d = max(abs(aa - wr), abs(bb - wc));
+            atomicMax(reinterpret_cast<int*>(&v.light[aa * O::VC + bb]), __float_as_int(1.0f - 0.25f * (float)d));
+          }
+      }
+      __syncwarp();
+    }
+    constexpr int NSLOT = EXT ? 14 : 11;
+    uint32_t sl = 0xFFFFu;
+    if (lane < NSLOT) sl = (v.desc[D_CRE + (lane >> 1)] >> (16 * (lane & 1))) & 0xFFFFu;
+    const int cell = sl == 0xFFFFu ? -1 : (int)(sl >> 8);
+    bool win = cell >= 0;
+    for (int s = 1; s < NSLOT; ++s) {
+      const int oc = __shfl_down_sync(0xffffffffu, cell, s);
+      if (lane + s < NSLOT && oc == cell) win = false;
+    }
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) {
+      const int t = lane + 32 * q;
+      if (t < O::T) {
+        if (sleeping) v.light[t] = 0.0f;
+        const bool lit = v.light[t] >= 0.05f;
+        const uint32_t bc = EXT ? bq[q] : (uint32_t)C_CLASSIC_LOCAL[bq[q]];
+        const uint32_t ic = EXT ? (uint32_t)(O::BCH + iq[q]) : 0xFFu;
+        v.tgt[t] = lit ? (bc | ic << 8 | (uint32_t)(O::BCH + O::ICH) << 16) : 0xFFFFFFu;
+      }
+    }
+    __syncwarp();
+    if (win && (v.tgt[cell] >> 16) != 0xFFu)
+      v.tgt[cell] = (v.tgt[cell] & 0xFFFFu) | ((uint32_t)(O::BCH + O::ICH + (sl & 0xFF)) << 16);
+    __syncwarp();
+    // scatter into the staged row; element p lives at stage[p + shift] so
+    // that 16-byte chunks line up with the destination row
+    float* row = (float*)a.out + (size_t)i * O::L;
+    const int shift = (int)((reinterpret_cast<uintptr_t>(row) & 15u) >> 2);
+    float* sr = stage + shift;
+    for (int t = lane; t < O::T; t += 32) {
+      const uint32_t g = v.tgt[t];
+      float* tv = sr + t * O::STRIDE;
+      if ((g & 0xFF) != 0xFF) {
+        tv[g & 0xFF] = 1.0f;
+        if (EXT) tv[(g >> 8) & 0xFF] = 1.0f;
+        tv[g >> 16] = 1.0f;
+      }
+      tv[O::STRIDE - 1] = v.light[t];
+    }
+    for (int k = lane; k < O::NINV; k += 32) sr[O::T * O::STRIDE + k] = __uint_as_float(v.desc[D_INV + k]);
+    __syncwarp();
+    // copy out: head floats, 16-byte body, tail
+    const int head = (4 - shift) & 3;
+    if (lane < head) row[lane] = sr[lane];
+    const int nv = (O::L - head) >> 2;
+    const float4* s4 = reinterpret_cast<const float4*>(sr + head);
+    float4* g4 = reinterpret_cast<float4*>(row + head);
+    for (int q = lane; q < nv; q += 32) g4[q] = s4[q];
+    const int t0 = head + nv * 4;
+    if (t0 + lane < O::L) row[t0 + lane] = sr[t0 + lane];
+    __syncwarp();
+    // scatter the zeros back
+    for (int t = lane; t < O::T; t += 32) {
+      const uint32_t g = v.tgt[t];
+      float* tv = sr + t * O::STRIDE;
+      if ((g & 0xFF) != 0xFF) {
+        tv[g & 0xFF] = 0.0f;
+        if (EXT) tv[(g >> 8) & 0xFF] = 0.0f;
+        tv[g >> 16] = 0.0f;
+      }
+      tv[O::STRIDE - 1] = 0.0f;
+    }
+    for (int k = lane; k < O::NINV; k += 32) sr[O::T * O::STRIDE + k] = 0.0f;
+    __syncwarp();
+  }
+}
+
 void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
   if (a.n <= 0) return;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t need = (a.n + OBS_WARPS - 1) / OBS_WARPS;
-  const int grid = (int)std::min<int64_t>(need, (int64_t)sms * 16);
-  if (ext) k_symbolic_desc<true><<<grid, OBS_WARPS * 32, 0, st>>>(S, a);
-  else k_symbolic_desc<false><<<grid, OBS_WARPS * 32, 0, st>>>(S, a);
+  if (ext) {
+    constexpr int NW = stage_warps<true>();
+    const size_t smem = (size_t)NW * ((OT<true>::L + 4 + 3) & ~3) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_symbolic_stage<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    const int grid = (int)std::min<int64_t>((a.n + NW - 1) / NW, (int64_t)sms * 3);
+    k_symbolic_stage<true><<<grid, NW * 32, smem, st>>>(S, a);
+  } else {
+    constexpr int NW = stage_warps<false>();
+    const size_t smem = (size_t)NW * ((OT<false>::L + 4 + 3) & ~3) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_symbolic_stage<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    const int grid = (int)std::min<int64_t>((a.n + NW - 1) / NW, (int64_t)sms * 4);
+    k_symbolic_stage<false><<<grid, NW * 32, smem, st>>>(S, a);
+  }
 }
 
 void launch_pixels(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
