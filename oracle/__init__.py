@@ -140,6 +140,17 @@ def lib():
         L.go_batch_stats.argtypes = [P, P, P, P, P]
         L.go_batch_ep.argtypes = [P, P, P]
         L.go_random_actions.argtypes = [c.c_uint32, c.c_uint64, c.c_int64, c.c_int64, c.c_int, P]
+        L.go_batch_create_shard.restype = P
+        L.go_batch_create_shard.argtypes = [c.c_int, c.c_int64, c.c_int64, c.c_int64, c.c_uint64, c.c_int,
+                                            c.c_int64, c.c_int]
+        L.go_batch_step_a.restype = c.c_int64
+        L.go_batch_step_a.argtypes = [P, P, P]
+        L.go_batch_step_b.restype = c.c_int64
+        L.go_batch_step_b.argtypes = [P, P, P, P, P, P, P]
+        L.go_batch_step_c.argtypes = [P, c.c_int64]
+        L.go_state_any_dark.restype = c.c_int
+        L.go_state_any_dark.argtypes = [P]
+        L.go_state_encode_flag.argtypes = [P, c.c_int, P]
         _lib = L
     return _lib
 
@@ -244,13 +255,47 @@ class OracleBatch:
     """batch.batch_reset / batch_step (batch.py:127-234) on the oracle."""
 
     def __init__(self, tier: str, n: int, seed: int, reset_ratio: int = 16,
-                 max_episode_length: int | None = None, threads: int = 1):
+                 max_episode_length: int | None = None, threads: int = 1,
+                 env_offset: int = 0, n_global: int | None = None):
         self.tier = tier
         self.n = n
         self.t = TIERS[tier]
-        self.h = lib().go_batch_create(self.t["classic"], n, ctypes.c_uint64(seed), reset_ratio,
-                                       max_episode_length or 0, threads)
+        self.h = lib().go_batch_create_shard(self.t["classic"], n, env_offset, n_global or n,
+                                             ctypes.c_uint64(seed), reset_ratio,
+                                             max_episode_length or 0, threads)
         self.state = OracleState(tier, n, _handle=lib().go_batch_state(self.h), _owner=self)
+
+    # --- sharded step: the three phases of go_batch_step ----------------
+    def step_a(self, actions) -> np.ndarray:
+        self._a = np.ascontiguousarray(actions, dtype=np.int64)
+        flags = np.zeros(2, np.int32)
+        rc = lib().go_batch_step_a(self.h, _ptr(self._a), _ptr(flags))
+        if rc < 0:
+            bad = -1 - rc
+            raise ValueError(f"invalid action {int(self._a[bad])} for env {bad}")
+        return flags
+
+    def step_b(self, flags):
+        fl = np.ascontiguousarray(flags, dtype=np.int32)
+        reward = np.zeros(self.n, np.float64)
+        done = np.zeros(self.n, np.bool_)
+        newly = np.zeros((self.n, self.t["A"]), np.bool_)
+        itime = np.zeros(self.n, np.uint32)
+        ifloor = np.zeros(self.n, np.uint8)
+        k = lib().go_batch_step_b(self.h, _ptr(fl), _ptr(reward), _ptr(done), _ptr(newly), _ptr(itime),
+                                  _ptr(ifloor))
+        return reward, done, newly, {"time": itime, "floor": ifloor}, int(k)
+
+    def step_c(self, offset: int) -> None:
+        lib().go_batch_step_c(self.h, int(offset))
+
+    def any_dark(self) -> bool:
+        return bool(lib().go_state_any_dark(self.state.h))
+
+    def encode_symbolic(self, dark: bool) -> np.ndarray:
+        out = np.empty((self.n, self.t["L"]), np.float32)
+        lib().go_state_encode_flag(self.state.h, 1 if dark else 0, _ptr(out))
+        return out
 
     def __del__(self):
         if getattr(self, "h", None):

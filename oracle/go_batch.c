@@ -127,11 +127,13 @@ int64_t go_state_step(go_state_t *s, const int64_t *actions, double *reward, uin
 void go_state_encode(const go_state_t *s, float *out) {
   int L = s->classic ? 1345 : 8268;
   int dark = gs_any_dark(s);
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < s->n; ++i) gs_encode_symbolic(s, i, dark, out + (size_t)i * L);
 }
 
 void go_state_pixels(const go_state_t *s, int px, uint8_t *out) {
   size_t fr = (size_t)(s->VR + 2) * px * (s->VC + (s->classic ? 0 : 2)) * px * 3;
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < s->n; ++i) gs_render_pixels(s, i, px, out + i * fr);
 }
 
@@ -149,16 +151,27 @@ struct go_batch {
   double total_return;
   int64_t ach_counts[67];
   int64_t *done_idx;
+  int64_t k_local;
   go_world *worlds;
   int n_worlds_cap;
+  int64_t env_offset, n_global;   /* shard of a larger batch (multi-rank) */
 };
 
 go_batch *go_batch_create(int classic, int64_t n, uint64_t seed, int reset_ratio, int64_t max_len,
                           int threads) {
+  return go_batch_create_shard(classic, n, 0, n, seed, reset_ratio, max_len, threads);
+}
+
+/* one contiguous shard [env_offset, env_offset + n) of an n_global batch:
+ * every key uses the global env index, the pool size is global */
+go_batch *go_batch_create_shard(int classic, int64_t n, int64_t env_offset, int64_t n_global,
+                                uint64_t seed, int reset_ratio, int64_t max_len, int threads) {
   go_batch *b = (go_batch *)calloc(1, sizeof(go_batch));
   gs_init(&b->st, classic, n, max_len);
   b->threads = threads > 0 ? threads : 1;
-  b->M = (int)((n + reset_ratio - 1) / reset_ratio);
+  b->env_offset = env_offset;
+  b->n_global = n_global;
+  b->M = (int)((n_global + reset_ratio - 1) / reset_ratio);
   if (b->M < 1) b->M = 1;
   /* batch.py:139-160 */
   uint64_t base = go_mix(seed);
@@ -173,7 +186,7 @@ go_batch *go_batch_create(int classic, int64_t n, uint64_t seed, int reset_ratio
     go_world *w = (go_world *)malloc(sizeof(go_world));
 #pragma omp for schedule(dynamic, 4)
     for (int64_t i = 0; i < n; ++i) {
-      uint64_t ps = go_hash2(env_key, go_hash2((uint64_t)i, 0));
+      uint64_t ps = go_hash2(env_key, go_hash2((uint64_t)(env_offset + i), 0));
       uint64_t key = go_hash2(ps, go_hash2(1, 0));
       go_generate_world(ps, classic, w);
       gs_install(&b->st, i, w, key);
@@ -191,9 +204,12 @@ void go_batch_destroy(go_batch *b) {
 
 go_state_t *go_batch_state(go_batch *b) { return &b->st; }
 
-/* batch.py:193-234 */
-int64_t go_batch_step(go_batch *b, const int64_t *actions, double *reward, uint8_t *done,
-                      uint8_t *newly, uint32_t *info_time, uint8_t *info_floor) {
+/* batch.py:193-234 in three phases so that a sharded batch can exchange
+ * the batch-wide quantities between them (the reference batch is global):
+ *   a: validation + player actions/projectiles -> local `alive.any()` flags
+ *   b: (global flags) creatures .. reward/done  -> local done count
+ *   c: (global rank offset of this shard's first done env) pool + install */
+int64_t go_batch_step_a(go_batch *b, const int64_t *actions, int *flags) {
   go_state *s = &b->st;
   int64_t n = s->n;
   for (int64_t i = 0; i < n; ++i)
@@ -208,7 +224,18 @@ int64_t go_batch_step(go_batch *b, const int64_t *actions, double *reward, uint8
     if (lo < hi) gs_step_pass1(s, actions, b->ws, lo, hi, fl);
     mel |= fl[0]; ran |= fl[1];
   }
-  int fl[2] = {mel, ran};
+  flags[0] = mel;
+  flags[1] = ran;
+  return 0;
+}
+
+int64_t go_batch_step_b(go_batch *b, const int *flags, double *reward, uint8_t *done, uint8_t *newly,
+                        uint32_t *info_time, uint8_t *info_floor) {
+  go_state *s = &b->st;
+  int64_t n = s->n;
+  int T = b->threads;
+  int64_t chunk = (n + T - 1) / T;
+  int fl[2] = {flags[0], flags[1]};
 #pragma omp parallel for num_threads(T)
   for (int t = 0; t < T; ++t) {
     int64_t lo = t * chunk, hi = lo + chunk < n ? lo + chunk : n;
@@ -222,8 +249,17 @@ int64_t go_batch_step(go_batch *b, const int64_t *actions, double *reward, uint8
     if (info_floor) info_floor[i] = s->env[i].pfloor;
     if (done[i]) b->done_idx[k++] = i;
   }
+  b->k_local = k;
+  return k;
+}
+
+void go_batch_step_c(go_batch *b, int64_t offset) {
+  go_state *s = &b->st;
+  int T = b->threads;
+  int64_t k = b->k_local;
   uint64_t step_key = go_hash2(b->pool_key, (uint64_t)(b->step_index + 1));
   if (k) {
+    /* pool entry p holds slot (offset + p) % M; local done rank r uses entry r % M */
     int m = (int)(k < b->M ? k : b->M);
     if (m > b->n_worlds_cap) {
       free(b->worlds);
@@ -231,7 +267,8 @@ int64_t go_batch_step(go_batch *b, const int64_t *actions, double *reward, uint8
       b->n_worlds_cap = m;
     }
 #pragma omp parallel for num_threads(T) schedule(dynamic, 1)
-    for (int j = 0; j < m; ++j) go_generate_world(go_hash2(step_key, (uint64_t)j), s->classic, &b->worlds[j]);
+    for (int j = 0; j < m; ++j)
+      go_generate_world(go_hash2(step_key, (uint64_t)((offset + j) % b->M)), s->classic, &b->worlds[j]);
     for (int64_t r = 0; r < k; ++r) {
       int64_t i = b->done_idx[r];
       b->episodes += 1;
@@ -242,14 +279,33 @@ int64_t go_batch_step(go_batch *b, const int64_t *actions, double *reward, uint8
 #pragma omp parallel for num_threads(T)
     for (int64_t r = 0; r < k; ++r) {
       int64_t i = b->done_idx[r];
-      int slot = (int)(r % b->M);
-      gs_install(s, i, &b->worlds[slot], go_hash2(step_key, (1ULL << 32) + (uint64_t)slot));
+      int p = (int)(r % b->M);
+      uint64_t slot = (uint64_t)((offset + r) % b->M);
+      gs_install(s, i, &b->worlds[p], go_hash2(step_key, (1ULL << 32) + slot));
       b->ep_return[i] = 0.0;
       b->ep_length[i] = 0;
     }
   }
   b->step_index += 1;
+}
+
+int64_t go_batch_step(go_batch *b, const int64_t *actions, double *reward, uint8_t *done,
+                      uint8_t *newly, uint32_t *info_time, uint8_t *info_floor) {
+  int fl[2];
+  int64_t rc = go_batch_step_a(b, actions, fl);
+  if (rc < 0) return rc;
+  int64_t k = go_batch_step_b(b, fl, reward, done, newly, info_time, info_floor);
+  go_batch_step_c(b, 0);
   return k;
+}
+
+/* the torch-glow flag of obs.py:236 for this shard (OR over shards = batch) */
+int go_state_any_dark(const go_state_t *s) { return gs_any_dark(s); }
+
+void go_state_encode_flag(const go_state_t *s, int dark, float *out) {
+  int L = s->classic ? 1345 : 8268;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < s->n; ++i) gs_encode_symbolic(s, i, dark, out + (size_t)i * L);
 }
 
 void go_batch_stats(const go_batch *b, int64_t *episodes, double *total_return,

@@ -107,6 +107,14 @@ void go_state_pixels(const go_state_t *s, int tile_px, uint8_t *out);
 typedef struct go_batch go_batch;
 go_batch *go_batch_create(int classic, int64_t n, uint64_t seed, int reset_ratio,
                           int64_t max_len, int threads);
+go_batch *go_batch_create_shard(int classic, int64_t n, int64_t env_offset, int64_t n_global,
+                                uint64_t seed, int reset_ratio, int64_t max_len, int threads);
+int64_t go_batch_step_a(go_batch *b, const int64_t *actions, int *flags);
+int64_t go_batch_step_b(go_batch *b, const int *flags, double *reward, uint8_t *done, uint8_t *newly,
+                        uint32_t *info_time, uint8_t *info_floor);
+void go_batch_step_c(go_batch *b, int64_t offset);
+int go_state_any_dark(const go_state_t *s);
+void go_state_encode_flag(const go_state_t *s, int dark, float *out);
 void go_batch_destroy(go_batch *b);
 go_state_t *go_batch_state(go_batch *b);
 int64_t go_batch_step(go_batch *b, const int64_t *actions, double *reward,

@@ -1,0 +1,248 @@
+"""GPU parity and API tests (run on a B200: pytest -m gpu).
+
+Parity: the CUDA path (through the C ABI) against the C oracle -- which
+tests/test_oracle_golden.py pins to the numpy reference -- on the same
+seeded inputs: every SimState field, reward, done, newly-unlocked flags,
+info, symbolic observations and pixel frames, bit for bit, including the
+auto-reset pool, reset-stress runs and scrambled states that reach the
+rare branches (enchanting, potions, ladders, boss waves, projectiles).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _shapes(O, tier, n):
+    return O.field_shapes(tier, n)
+
+
+def _cmp_state(O, gb, ob_state, tier, n, skip=()):
+    ex = gb.export_state(_shapes(O, tier, n))
+    ox = ob_state.export_fields()
+    bad = [f for f in O.FIELD_NAMES if f not in skip and not np.array_equal(ex[f], ox[f])]
+    assert not bad, f"state fields differ: {bad}"
+
+
+def _step_both(torch, gb, ob, a):
+    obs, rew, done, newly, tm, fl = gb.step(torch.from_numpy(a).cuda())
+    r2, d2, nw2, info = ob.step(a)
+    assert np.array_equal(rew.cpu().numpy(), r2.astype(np.float32))
+    assert np.array_equal(done.cpu().numpy().astype(bool), d2)
+    assert np.array_equal(newly.cpu().numpy().astype(bool), nw2)
+    assert np.array_equal(tm.cpu().numpy().view(np.uint32), info["time"])
+    assert np.array_equal(fl.cpu().numpy(), info["floor"])
+    return obs
+
+
+@pytest.mark.parametrize("tier,n", [("classic", 512), ("extended", 384)])
+def test_batch_reset_matches_oracle(torch_cuda, oracle_lib, tier, n):
+    from paper_2402_16801_b200 import GridrogueBatch
+    O = oracle_lib
+    gb = GridrogueBatch(n, tier, 11, "symbolic")
+    obs = gb.reset().cpu().numpy()
+    ob = O.OracleBatch(tier, n, 11, threads=8)
+    _cmp_state(O, gb, ob.state, tier, n)
+    assert np.array_equal(obs, ob.state.encode_symbolic())
+    assert np.array_equal(gb.level_seeds(), ob.state.export_fields()["params_seed"])
+
+
+@pytest.mark.parametrize("tier,n,steps,seed,max_len", [
+    ("classic", 256, 300, 0, None),
+    ("extended", 256, 300, 0, None),
+    ("extended", 128, 120, 3, 16),     # reset stress: every env resets every 16 steps
+    ("classic", 128, 120, 4, 16),
+    ("extended", 200, 150, 9, 40),
+])
+def test_rollout_parity(torch_cuda, oracle_lib, tier, n, steps, seed, max_len):
+    from paper_2402_16801_b200 import GridrogueBatch
+    O = oracle_lib
+    torch = torch_cuda
+    gb = GridrogueBatch(n, tier, seed, "symbolic", max_len)
+    gb.reset()
+    ob = O.OracleBatch(tier, n, seed, max_episode_length=max_len, threads=8)
+    na = O.TIERS[tier]["NA"]
+    for k in range(steps):
+        obs = _step_both(torch, gb, ob, O.random_actions(seed, k, n, na))
+        assert np.array_equal(obs.cpu().numpy(), ob.state.encode_symbolic()), f"obs step {k}"
+        if k % 25 == 0:
+            _cmp_state(O, gb, ob.state, tier, n)
+    _cmp_state(O, gb, ob.state, tier, n)
+    s1, s2 = gb.stats(), ob.stats()
+    assert s1["episodes"] == s2["episodes"] > 0
+    assert s1["total_steps"] == s2["total_steps"]
+    assert np.array_equal(s1["ach_episodes"], s2["ach_episodes"])
+    assert abs(s1["total_return"] - s2["total_return"]) <= 1e-9 * max(1.0, abs(s2["total_return"]))
+
+
+@pytest.mark.parametrize("tier,n,px,steps", [("classic", 64, 7, 60), ("extended", 64, 10, 60),
+                                             ("classic", 32, 16, 20), ("extended", 16, 16, 20)])
+def test_pixel_parity(torch_cuda, oracle_lib, tier, n, px, steps):
+    from paper_2402_16801_b200 import GridrogueBatch
+    O = oracle_lib
+    gb = GridrogueBatch(n, tier, 5, "pixels", 30, tile_px=px)
+    obs = gb.reset().cpu().numpy()
+    ob = O.OracleBatch(tier, n, 5, max_episode_length=30)
+    assert np.array_equal(obs, ob.state.render_pixels(px))
+    for k in range(steps):
+        obs = _step_both(torch_cuda, gb, ob, O.random_actions(5, k, n, O.TIERS[tier]["NA"]))
+        assert np.array_equal(obs.cpu().numpy(), ob.state.render_pixels(px)), f"pixels step {k}"
+
+
+@pytest.mark.parametrize("tier", ["classic", "extended"])
+def test_scrambled_state_parity(torch_cuda, oracle_lib, tier):
+    """Rare branches: import the scrambled states of the fuzz golden into both
+    sides and step them under batch semantics with the golden's actions."""
+    from paper_2402_16801_b200 import GridrogueBatch
+    O = oracle_lib
+    g = np.load(os.path.join(GOLD, f"fuzz_{tier}.npz"))
+    n = int(g["n"])
+    start = {f: g[f"start_{f}"] for f in O.FIELD_NAMES}
+    gb = GridrogueBatch(n, tier, 21, "symbolic")
+    gb.reset()
+    gb.import_state(start)
+    ob = O.OracleBatch(tier, n, 21)
+    ob.state.import_fields(start)
+    assert np.array_equal(gb.observe().cpu().numpy(), ob.state.encode_symbolic())
+    for k, a in enumerate(g["actions"]):
+        obs = _step_both(torch_cuda, gb, ob, a)
+        assert np.array_equal(obs.cpu().numpy(), ob.state.encode_symbolic()), f"obs step {k}"
+        _cmp_state(O, gb, ob.state, tier, n)
+
+
+def test_full_size_north_star_parity(torch_cuda, oracle_lib):
+    """65,536 extended envs (the bench workload): rewards, dones, obs digests
+    and non-map state against the oracle for 12 steps."""
+    from paper_2402_16801_b200 import GridrogueBatch
+    from tests._digest import digest
+    O = oracle_lib
+    torch = torch_cuda
+    n, seed = 65536, 0
+    gb = GridrogueBatch(n, "extended", seed, "symbolic")
+    gb.reset()
+    ob = O.OracleBatch("extended", n, seed, threads=os.cpu_count() or 8)
+    for k in range(12):
+        a = O.random_actions(seed, k, n, 43)
+        obs = _step_both(torch, gb, ob, a)
+        assert digest(obs.cpu().numpy()) == digest(ob.state.encode_symbolic()), f"obs step {k}"
+    _cmp_state(O, gb, ob.state, "extended", n, skip=("blocks", "items"))
+
+
+def test_batchenv_contract(torch_cuda, oracle_lib):
+    """gridrogue_gym.BatchEnv semantics (bindings/tests/test_bindings.py)."""
+    from paper_2402_16801_b200 import BatchEnv
+    O = oracle_lib
+    env = BatchEnv(4, tier="extended", seed=1)
+    obs = env.reset()
+    assert obs.shape == (4, 8268) and obs.dtype == np.float32
+    obs, reward, done, info = env.step(np.zeros(4, np.int64))
+    assert obs.shape == (4, 8268) and reward.dtype == np.float32 and reward.shape == (4,)
+    assert done.shape == (4,) and done.dtype == bool
+    assert info["newly_unlocked"].shape == (4, 67)
+    assert BatchEnv(3, tier="classic", seed=1).reset().shape == (3, 1345)
+    env = BatchEnv(4, tier="classic", seed=0)
+    env.reset()
+    with pytest.raises(ValueError, match="env 2"):
+        env.step(np.array([0, 1, 99, 3]))
+    with pytest.raises(ValueError, match="shape"):
+        env.step(np.zeros(5, np.int64))
+    with pytest.raises(RuntimeError, match="reset"):
+        BatchEnv(2, tier="classic").step(np.zeros(2, np.int64))
+    with pytest.raises(ValueError):
+        BatchEnv(2, tier="classic", obs_mode="rgb")
+    # bit parity of the host path with the oracle batch over 300 steps
+    n = 20
+    env = BatchEnv(n, tier="classic", seed=9)
+    ob = O.OracleBatch("classic", n, 9)
+    assert np.array_equal(env.reset(), ob.state.encode_symbolic())
+    rng = np.random.default_rng(4)
+    for _ in range(300):
+        acts = rng.integers(0, 17, size=n)
+        o1, r1, d1, i1 = env.step(acts)
+        r2, d2, nw2, i2 = ob.step(acts)
+        assert np.array_equal(r1, r2.astype(np.float32)) and np.array_equal(d1, d2)
+        assert np.array_equal(o1, ob.state.encode_symbolic())
+        assert np.array_equal(i1["newly_unlocked"], nw2) and np.array_equal(i1["time"], i2["time"])
+    assert i1["episodes_completed"] == ob.stats()["episodes"]
+
+
+def test_auto_reset_consumes_done(torch_cuda, oracle_lib):
+    from paper_2402_16801_b200 import GridrogueBatch
+    O = oracle_lib
+    gb = GridrogueBatch(4, "classic", 2, "symbolic")
+    gb.reset()
+    health = gb.export_field("health").view(np.float32).copy()
+    health[1] = 0.0
+    gb.import_field("health", health)
+    _, _, done, *_ = gb.step(torch_cuda.zeros(4, dtype=torch_cuda.int64, device="cuda"))
+    assert bool(done[1]) and not bool(done[0])
+    assert not gb.export_field("done").any()
+    assert gb.export_field("time").view(np.uint32)[1] == 0
+
+
+def test_device_validation_and_policy(torch_cuda, oracle_lib):
+    from paper_2402_16801_b200 import GridrogueBatch
+    from paper_2402_16801_b200.policies import RandomPolicy
+    torch = torch_cuda
+    gb = GridrogueBatch(1000, "extended", 3, "none")
+    gb.reset()
+    a = gb.random_actions(77, 5).cpu().numpy()
+    assert np.array_equal(a, RandomPolicy(77, 43).actions_at(5, 1000))
+    before = gb.export_field("time").copy()
+    bad = torch.zeros(1000, dtype=torch.int64, device="cuda")
+    bad[321] = 43
+    with pytest.raises(ValueError, match="env 321"):
+        gb.step(bad)
+    assert np.array_equal(before, gb.export_field("time"))   # nothing mutated
+
+
+def test_gymnax_facade(torch_cuda):
+    from paper_2402_16801_b200 import make_craftax_env_from_name, EnvParams
+    torch = torch_cuda
+    env = make_craftax_env_from_name("Craftax-Symbolic-v1")
+    params = EnvParams(n_envs=64)
+    obs, state = env.reset(0, params)
+    assert tuple(obs.shape) == (64, 8268)
+    action = torch.zeros(64, dtype=torch.int64, device="cuda")
+    obs, state, reward, done, info = env.step(1, state, action, params)
+    assert tuple(reward.shape) == (64,) and done.dtype == torch.bool
+    env = make_craftax_env_from_name("Craftax-Classic-Pixels-v1")
+    obs, state = env.reset(3, EnvParams(n_envs=8))
+    assert tuple(obs.shape) == (8, 63, 63, 3) and obs.dtype == torch.uint8
+
+
+def test_sharded_batch_world_one(torch_cuda, oracle_lib):
+    """ShardedBatch's exchange path (single rank) equals the plain step."""
+    import torch.distributed as dist
+    from paper_2402_16801_b200 import ShardedBatch
+    O = oracle_lib
+    torch = torch_cuda
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        sb = ShardedBatch(96, "extended", 13, "symbolic", max_episode_length=20)
+        sb.reset()
+        ob = O.OracleBatch("extended", 96, 13, max_episode_length=20)
+        for k in range(50):
+            a = O.random_actions(13, k, 96, 43)
+            obs, rew, done, *_ = sb.step(torch.from_numpy(a).cuda())
+            r2, d2, _, _ = ob.step(a)
+            assert np.array_equal(rew.cpu().numpy(), r2.astype(np.float32))
+            assert np.array_equal(obs.cpu().numpy(), ob.state.encode_symbolic())
+        assert sb.stats()["episodes"] == ob.stats()["episodes"]
+    finally:
+        dist.destroy_process_group()
