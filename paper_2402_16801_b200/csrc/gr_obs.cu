@@ -536,18 +536,23 @@ __global__ void __launch_bounds__(OBS_WARPS * 32) k_symbolic_desc(DS S, ObsArgs 
 // global byte written exactly once.
 template <bool EXT>
 __host__ __device__ constexpr int stage_warps() { return EXT ? 2 : 8; }
+// one chunk = one whole row (+ up to 3 floats of alignment shift); smaller
+// chunks (more resident warps) measured slower: 2048-float chunks 0.44 ms
+// vs 0.40 ms per 65,536-env launch
+template <bool EXT>
+__host__ __device__ constexpr int stage_floats() { return EXT ? 8272 : 1352; }
 
 template <bool EXT>
 __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S, ObsArgs a) {
   using O = OT<EXT>;
   constexpr int NW = stage_warps<EXT>();
-  constexpr int ROWF = (O::L + 4 + 3) & ~3;   // floats per staged row (+ alignment shift)
+  constexpr int SC = stage_floats<EXT>();   // floats per staged chunk
   extern __shared__ float4 dyn_smem[];
   __shared__ TileSmem<EXT> views[NW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   TileSmem<EXT>& v = views[warp];
-  float* stage = reinterpret_cast<float*>(dyn_smem) + (size_t)warp * ROWF;
-  for (int q = lane; q < ROWF / 4; q += 32) reinterpret_cast<float4*>(stage)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float* stage = reinterpret_cast<float*>(dyn_smem) + (size_t)warp * SC;
+  for (int q = lane; q < SC / 4; q += 32) reinterpret_cast<float4*>(stage)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncwarp();
   const bool glow = EXT && a.flags && (a.flags[0] & 4u);
   for (int64_t i = (int64_t)blockIdx.x * NW + warp; i < a.n; i += (int64_t)gridDim.x * NW) {
@@ -613,46 +618,72 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
     if (win && (v.tgt[cell] >> 16) != 0xFFu)
       v.tgt[cell] = (v.tgt[cell] & 0xFFFFu) | ((uint32_t)(O::BCH + O::ICH + (sl & 0xFF)) << 16);
     __syncwarp();
-    // scatter into the staged row; element p lives at stage[p + shift] so
-    // that 16-byte chunks line up with the destination row
+    // The row is produced in chunks of SC floats through the zero-invariant
+    // stage.  Element p of the row sits at q = p + shift (shift aligns the
+    // 16-byte groups of q with those of the destination address).
     float* row = (float*)a.out + (size_t)i * O::L;
     const int shift = (int)((reinterpret_cast<uintptr_t>(row) & 15u) >> 2);
-    float* sr = stage + shift;
-    for (int t = lane; t < O::T; t += 32) {
-      const uint32_t g = v.tgt[t];
-      float* tv = sr + t * O::STRIDE;
-      if ((g & 0xFF) != 0xFF) {
-        tv[g & 0xFF] = 1.0f;
-        if (EXT) tv[(g >> 8) & 0xFF] = 1.0f;
-        tv[g >> 16] = 1.0f;
+    for (int qc = 0; qc < O::L + shift; qc += SC) {
+      // scatter the non-zeros that fall into this chunk
+      for (int t = lane; t < O::T; t += 32) {
+        const uint32_t g = v.tgt[t];
+        const int tb = t * O::STRIDE + shift - qc;
+        if ((unsigned)(tb + O::STRIDE) <= (unsigned)(SC + O::STRIDE)) {   // tile overlaps the chunk
+          if ((g & 0xFF) != 0xFF) {
+            const int q0 = tb + (int)(g & 0xFF), q2 = tb + (int)(g >> 16);
+            if ((unsigned)q0 < (unsigned)SC) stage[q0] = 1.0f;
+            if (EXT) {
+              const int q1 = tb + (int)((g >> 8) & 0xFF);
+              if ((unsigned)q1 < (unsigned)SC) stage[q1] = 1.0f;
+            }
+            if ((unsigned)q2 < (unsigned)SC) stage[q2] = 1.0f;
+          }
+          const int ql = tb + O::STRIDE - 1;
+          if ((unsigned)ql < (unsigned)SC) stage[ql] = v.light[t];
+        }
       }
-      tv[O::STRIDE - 1] = v.light[t];
-    }
-    for (int k = lane; k < O::NINV; k += 32) sr[O::T * O::STRIDE + k] = __uint_as_float(v.desc[D_INV + k]);
-    __syncwarp();
-    // copy out: head floats, 16-byte body, tail
-    const int head = (4 - shift) & 3;
-    if (lane < head) row[lane] = sr[lane];
-    const int nv = (O::L - head) >> 2;
-    const float4* s4 = reinterpret_cast<const float4*>(sr + head);
-    float4* g4 = reinterpret_cast<float4*>(row + head);
-    for (int q = lane; q < nv; q += 32) g4[q] = s4[q];
-    const int t0 = head + nv * 4;
-    if (t0 + lane < O::L) row[t0 + lane] = sr[t0 + lane];
-    __syncwarp();
-    // scatter the zeros back
-    for (int t = lane; t < O::T; t += 32) {
-      const uint32_t g = v.tgt[t];
-      float* tv = sr + t * O::STRIDE;
-      if ((g & 0xFF) != 0xFF) {
-        tv[g & 0xFF] = 0.0f;
-        if (EXT) tv[(g >> 8) & 0xFF] = 0.0f;
-        tv[g >> 16] = 0.0f;
+      for (int k = lane; k < O::NINV; k += 32) {
+        const int q = O::T * O::STRIDE + k + shift - qc;
+        if ((unsigned)q < (unsigned)SC) stage[q] = __uint_as_float(v.desc[D_INV + k]);
       }
-      tv[O::STRIDE - 1] = 0.0f;
+      __syncwarp();
+      // copy out: 16-byte groups fully inside the row, element-wise edges
+      const float4* s4 = reinterpret_cast<const float4*>(stage);
+      for (int gi = lane; gi < SC / 4; gi += 32) {
+        const int q = qc + 4 * gi, p = q - shift;
+        if (p >= O::L) break;
+        if (p >= 0 && p + 4 <= O::L) {
+          *reinterpret_cast<float4*>(row + p) = s4[gi];
+        } else {
+          for (int j = 0; j < 4; ++j)
+            if (p + j >= 0 && p + j < O::L) row[p + j] = stage[4 * gi + j];
+        }
+      }
+      __syncwarp();
+      // scatter the zeros back
+      for (int t = lane; t < O::T; t += 32) {
+        const uint32_t g = v.tgt[t];
+        const int tb = t * O::STRIDE + shift - qc;
+        if ((unsigned)(tb + O::STRIDE) <= (unsigned)(SC + O::STRIDE)) {
+          if ((g & 0xFF) != 0xFF) {
+            const int q0 = tb + (int)(g & 0xFF), q2 = tb + (int)(g >> 16);
+            if ((unsigned)q0 < (unsigned)SC) stage[q0] = 0.0f;
+            if (EXT) {
+              const int q1 = tb + (int)((g >> 8) & 0xFF);
+              if ((unsigned)q1 < (unsigned)SC) stage[q1] = 0.0f;
+            }
+            if ((unsigned)q2 < (unsigned)SC) stage[q2] = 0.0f;
+          }
+          const int ql = tb + O::STRIDE - 1;
+          if ((unsigned)ql < (unsigned)SC) stage[ql] = 0.0f;
+        }
+      }
+      for (int k = lane; k < O::NINV; k += 32) {
+        const int q = O::T * O::STRIDE + k + shift - qc;
+        if ((unsigned)q < (unsigned)SC) stage[q] = 0.0f;
+      }
+      __syncwarp();
     }
-    for (int k = lane; k < O::NINV; k += 32) sr[O::T * O::STRIDE + k] = 0.0f;
-    __syncwarp();
   }
 }
 
@@ -663,7 +694,7 @@ void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (ext) {
     constexpr int NW = stage_warps<true>();
-    const size_t smem = (size_t)NW * ((OT<true>::L + 4 + 3) & ~3) * sizeof(float);
+    const size_t smem = (size_t)NW * stage_floats<true>() * sizeof(float);
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_symbolic_stage<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -673,7 +704,7 @@ void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
     k_symbolic_stage<true><<<grid, NW * 32, smem, st>>>(S, a);
   } else {
     constexpr int NW = stage_warps<false>();
-    const size_t smem = (size_t)NW * ((OT<false>::L + 4 + 3) & ~3) * sizeof(float);
+    const size_t smem = (size_t)NW * stage_floats<false>() * sizeof(float);
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_symbolic_stage<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
