@@ -260,6 +260,7 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.ep_return, e->n * sizeof(double));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.ep_length, e->n * sizeof(int32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.desc, e->n * 256);
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.torch_bits, e->n * sizeof(uint16_t));
   const int64_t cap = std::min(e->n, e->M);
   const size_t wbytes = (size_t)cap * e->d.F * e->d.H * e->d.W;
   e->pool.cap = cap;
@@ -606,6 +607,8 @@ int gr_import_field(gr_env* e, int32_t field, const void* host_src) {
   const int64_t comps = device_comps(field, e->d);
   const size_t bytes = (size_t)comps * e->n * fd.esz;
   e->have_reset = true;
+  // an imported map may hold torches anywhere: disable the no-torch shortcut
+  CK(cudaMemset(e->S.torch_bits, 0xFF, e->n * sizeof(uint16_t)));
   if (fd.kind == K_MAP) {
     CK(cudaMemcpy(e->S.f[field], host_src, bytes, cudaMemcpyHostToDevice));
     return GR_OK;

@@ -21,7 +21,7 @@ constexpr int DESC_WORDS = 64;
 constexpr int D_INV = 0;        // [0, 50): inventory section (float bits)
 constexpr int D_BASE = 50;      // base light (float bits)
 constexpr int D_POS = 51;       // (uint16)prow | (uint16)pcol << 16
-constexpr int D_FLAGS = 52;     // pfloor | sleeping << 8
+constexpr int D_FLAGS = 52;     // pfloor | sleeping << 8 | torch-possible-on-this-floor << 9
 constexpr int D_CRE = 53;       // 14 x u16 slot (cell << 8 | channel), 0xFFFF = none
 
 // obs.daylight (obs.py:191-195): float32, numpy's SIMD sin

@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(OBS_WARPS * 32) k_symbolic_desc(DS S, ObsArgs 
     }
     for (int k = lane; k < O::NINV; k += 32) v.inv[k] = __uint_as_float(v.desc[D_INV + k]);
     __syncwarp();
-    if (glow) {
+    if (glow && ((fl >> 9) & 1u)) {   // only floors this env ever put a torch on
       constexpr int WR = O::VR + 6, WC = O::VC + 6;
       for (int t = lane; t < WR * WC; t += 32) {
         const int wr = t / WC - 3, wc = t % WC - 3;
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
       if (t < O::T) v.light[t] = base;
     }
     __syncwarp();
-    if (glow) {
+    if (glow && ((fl >> 9) & 1u)) {   // only floors this env ever put a torch on
       constexpr int WR = O::VR + 6, WC = O::VC + 6;
       for (int t = lane; t < WR * WC; t += 32) {
         const int wr = t / WC - 3, wc = t % WC - 3;
@@ -623,6 +623,43 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
     // 16-byte groups of q with those of the destination address).
     float* row = (float*)a.out + (size_t)i * O::L;
     const int shift = (int)((reinterpret_cast<uintptr_t>(row) & 15u) >> 2);
+    if (SC >= O::L + 3) {   // the whole row fits: straight-line scatter / copy / unscatter
+      float* sr = stage + shift;
+      for (int t = lane; t < O::T; t += 32) {
+        const uint32_t g = v.tgt[t];
+        float* tv = sr + t * O::STRIDE;
+        if ((g & 0xFF) != 0xFF) {
+          tv[g & 0xFF] = 1.0f;
+          if (EXT) tv[(g >> 8) & 0xFF] = 1.0f;
+          tv[g >> 16] = 1.0f;
+        }
+        tv[O::STRIDE - 1] = v.light[t];
+      }
+      for (int k = lane; k < O::NINV; k += 32) sr[O::T * O::STRIDE + k] = __uint_as_float(v.desc[D_INV + k]);
+      __syncwarp();
+      const int head = (4 - shift) & 3;
+      if (lane < head) row[lane] = sr[lane];
+      const int nv = (O::L - head) >> 2;
+      const float4* s4 = reinterpret_cast<const float4*>(sr + head);
+      float4* g4 = reinterpret_cast<float4*>(row + head);
+      for (int q = lane; q < nv; q += 32) g4[q] = s4[q];
+      const int tl = head + nv * 4;
+      if (tl + lane < O::L) row[tl + lane] = sr[tl + lane];
+      __syncwarp();
+      for (int t = lane; t < O::T; t += 32) {
+        const uint32_t g = v.tgt[t];
+        float* tv = sr + t * O::STRIDE;
+        if ((g & 0xFF) != 0xFF) {
+          tv[g & 0xFF] = 0.0f;
+          if (EXT) tv[(g >> 8) & 0xFF] = 0.0f;
+          tv[g >> 16] = 0.0f;
+        }
+        tv[O::STRIDE - 1] = 0.0f;
+      }
+      for (int k = lane; k < O::NINV; k += 32) sr[O::T * O::STRIDE + k] = 0.0f;
+      __syncwarp();
+      continue;
+    }
     for (int qc = 0; qc < O::L + shift; qc += SC) {
       // scatter the non-zeros that fall into this chunk
       for (int t = lane; t < O::T; t += 32) {

@@ -169,6 +169,7 @@ __device__ void install_one(const DS& S, int64_t i, const WMeta& m, const uint8_
     GR_AT(S, GR_F_RNG_KEY, uint64_t, 0, i) = m.key;
     GR_AT(S, GR_F_BOSS_HP, float, 0, i) = EXT ? 60.0f : 0.0f;
     S.cd_pending[i] = 0;
+    S.torch_bits[i] = 0;
     S.ep_return[i] = 0.0;
     S.ep_length[i] = 0;
   }

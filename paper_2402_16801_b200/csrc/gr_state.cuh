@@ -73,6 +73,7 @@ struct DS {
   double* ep_return;          // batch.BatchState.ep_return
   int32_t* ep_length;         // batch.BatchState.ep_length
   uint32_t* desc;             // [ns][64] observation descriptors (gr_desc.cuh)
+  uint16_t* torch_bits;       // bit f: a torch may lie on floor f (torches are never removed)
 };
 
 // one generated world (worldgen.World) in a world buffer

@@ -72,6 +72,7 @@ struct Ctx {
   uint32_t time;
   uint64_t key;
   uint16_t visited, cleared;
+  uint16_t torch;     // floors that may hold a torch (DS.torch_bits)
   float boss_hp;
   uint8_t boss_wave, boss_vuln, boss_timer;
   uint16_t clocks[6];
@@ -273,6 +274,7 @@ __device__ void load_env(Ctx& e, const DS& S) {
   for (int k = 0; k < 3; ++k) e.ach[k] = LD(GR_F_ACH, uint32_t, k);
   e.time = LD(GR_F_TIME, uint32_t, 0);
   e.key = LD(GR_F_RNG_KEY, uint64_t, 0);
+  e.torch = EXT ? S.torch_bits[i] : 0;
   e.visited = 0;
   e.cleared = 0;
   if (EXT) {
@@ -370,6 +372,7 @@ __device__ void store_env(const Ctx& e, const DS& S) {
   for (int k = 0; k < 3; ++k) ST(GR_F_ACH, uint32_t, k, e.ach[k]);
   ST(GR_F_TIME, uint32_t, 0, e.time);
   if (EXT) {
+    S.torch_bits[i] = e.torch;
 #pragma unroll
     for (int f = 0; f < T::F; ++f) {
       ST(GR_F_FLOORS_VISITED, uint8_t, f, (uint8_t)((e.visited >> f) & 1));
@@ -563,6 +566,7 @@ __device__ void place_action(Ctx& e, int a, int af) {
     }
   } else if (EXT && a == 28 && e.inv_torch > 0 && in_set(WALK_SET, tb)) {
     e.itm[af * T::HW + tr * T::W + tc] = I_TORCH;
+    e.torch |= (uint16_t)(1u << af);
     e.inv_torch -= 1;
     award<EXT>(e, 24);
   }
@@ -1149,7 +1153,7 @@ __device__ void write_desc(const Ctx& e, uint32_t* d) {
   for (int k = 0; k < 50; ++k) w[k] = k < NINV ? __float_as_uint(inv[k]) : 0u;
   w[D_BASE] = __float_as_uint(e.pfloor == 0 ? daylight(e.time) : C_FLOOR_AMB[e.pfloor]);
   w[D_POS] = (uint32_t)(uint16_t)e.prow | ((uint32_t)(uint16_t)e.pcol << 16);
-  w[D_FLAGS] = (uint32_t)e.pfloor | ((uint32_t)e.sleeping << 8);
+  w[D_FLAGS] = (uint32_t)e.pfloor | ((uint32_t)e.sleeping << 8) | ((uint32_t)((e.torch >> e.pfloor) & 1u) << 9);
   uint32_t slot[14];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {

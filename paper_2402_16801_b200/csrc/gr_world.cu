@@ -147,6 +147,32 @@ __device__ unsigned long long block_or_u64(SM& sm, unsigned long long v) {
   return r;
 }
 
+// exclusive prefix sum over the threads of the CTA (thread order)
+template <class SM>
+__device__ int block_excl_scan(SM& sm, int v, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm.ri[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < WG_THREADS / 32 ? sm.ri[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    sm.ri[lane] = w;
+  }
+  __syncthreads();
+  const int r = (warp ? sm.ri[warp - 1] : 0) + x - v;
+  *total = sm.ri[WG_THREADS / 32 - 1];
+  __syncthreads();
+  return r;
+}
+
 template <bool EXT>
 __device__ unsigned long long census(WSmem<EXT>& sm) {
   unsigned long long m = 0;
@@ -429,22 +455,24 @@ __device__ void carve(WSmem<EXT>& sm, int r, int c, int tr, int tc) {
 template <bool EXT>
 __device__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo) {
   using T = WT<EXT>;
-  if (threadIdx.x == 0) {
-    Stream s = Stream::raw(seed).split(1000 + (uint64_t)attempt);
-    const int n = s.randint(4, 8);
-    sm.nrooms = n;
-    for (int k = 0; k < n; ++k) {
-      const int rh = s.randint(5, 10), rw = s.randint(5, 10);
-      const int r0 = s.randint(2, T::H - rh - 2), c0 = s.randint(2, T::W - rw - 2);
-      sm.cr[k] = r0 + rh / 2;
-      sm.cc[k] = c0 + rw / 2;
-      // stash room rectangles in rowcnt (4 ints per room)
-      sm.rowcnt[4 * k] = r0; sm.rowcnt[4 * k + 1] = r0 + rh;
-      sm.rowcnt[4 * k + 2] = c0; sm.rowcnt[4 * k + 3] = c0 + rw;
-    }
+  // The randint chain draws hash2(key, counter) with counter 0 for the room
+  // count and 1 + 4k .. 4 + 4k for room k, so the rooms are independent:
+  // thread k rolls room k.
+  const Stream s0 = Stream::raw(seed).split(1000 + (uint64_t)attempt);
+  const int n = 4 + (int)(hash2(s0.key, 0) % 4ull);
+  if (threadIdx.x < n) {
+    const int k = threadIdx.x;
+    const uint64_t c = 1 + 4 * (uint64_t)k;
+    const int rh = 5 + (int)(hash2(s0.key, c) % 5ull), rw = 5 + (int)(hash2(s0.key, c + 1) % 5ull);
+    const int r0 = 2 + (int)(hash2(s0.key, c + 2) % (uint64_t)(T::H - rh - 4));
+    const int c0 = 2 + (int)(hash2(s0.key, c + 3) % (uint64_t)(T::W - rw - 4));
+    sm.cr[k] = r0 + rh / 2;
+    sm.cc[k] = c0 + rw / 2;
+    // room rectangles stashed in rowcnt (4 ints per room)
+    sm.rowcnt[4 * k] = r0; sm.rowcnt[4 * k + 1] = r0 + rh;
+    sm.rowcnt[4 * k + 2] = c0; sm.rowcnt[4 * k + 3] = c0 + rw;
   }
   __syncthreads();
-  const int n = sm.nrooms;
   for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
     const int r = t / T::W, c = t % T::W;
     bool in = false;
@@ -454,8 +482,12 @@ __device__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floor, int attemp
     sm.itm[t] = 0;
   }
   __syncthreads();
-  if (threadIdx.x == 0)
-    for (int k = 0; k + 1 < n; ++k) carve<EXT>(sm, sm.cr[k], sm.cc[k], sm.cr[k + 1], sm.cc[k + 1]);
+  // L-corridors between consecutive rooms: every write is PATH, so the
+  // corridors can be carved concurrently, one thread each
+  if (threadIdx.x + 1 < n) {
+    const int k = threadIdx.x;
+    carve<EXT>(sm, sm.cr[k], sm.cc[k], sm.cr[k + 1], sm.cc[k + 1]);
+  }
   __syncthreads();
   const uint32_t k32 = (uint32_t)(hash2(hash2(seed, 7 + (uint64_t)attempt), 4) & 0xFFFFFFFFull);
   uint8_t nb[WT<EXT>::PER];
@@ -581,9 +613,11 @@ __device__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, 
   const uint8_t must2[3] = {B_COAL, B_IRON, B_SAPPHIRE};
   const uint8_t must5[4] = {B_COAL, B_IRON, B_DIAMOND, B_RUBY};
   const int nm = floor == 2 ? 3 : 4;
+  // each _ensure_block only ever adds its own ore, so one census serves all
+  const unsigned long long cen0 = census(sm);
   for (int k = 0; k < nm; ++k) {
     const uint8_t b = floor == 2 ? must2[k] : must5[k];
-    if ((census(sm) >> b) & 1ull) continue;
+    if ((cen0 >> b) & 1ull) continue;
     double bv = 0.0;
     int bi = INT_MAX;
     for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
@@ -708,32 +742,25 @@ __device__ void assign_chests(WSmem<EXT>& sm, uint64_t world_seed, int f, WMeta*
     if (threadIdx.x == 0) meta->nch[f] = 0;
     return;
   }
-  // PATH tiles per row (the list of np.nonzero, row-major)
-  for (int r = threadIdx.x; r < T::H; r += WG_THREADS) {
-    int c0 = 0;
-    for (int c = 0; c < T::W; ++c) c0 += sm.blk[r * T::W + c] == B_PATH;
-    sm.rowcnt[r] = c0;
-  }
+  // the row-major list of PATH tiles (np.nonzero) via a block scan; it
+  // lives in the u buffer, which is dead by now
+  uint16_t* list = reinterpret_cast<uint16_t*>(sm.u);
+  constexpr int PER = (T::HW + WG_THREADS - 1) / WG_THREADS;
+  const int t0 = threadIdx.x * PER, t1 = min(t0 + PER, T::HW);
+  int cnt = 0;
+  for (int t = t0; t < t1; ++t) cnt += sm.blk[t] == B_PATH;
+  int len;
+  int off = block_excl_scan(sm, cnt, &len);
+  for (int t = t0; t < t1; ++t)
+    if (sm.blk[t] == B_PATH) list[off++] = (uint16_t)t;
   __syncthreads();
   if (threadIdx.x == 0) {
-    int len = 0;
-    for (int r = 0; r < T::H; ++r) len += sm.rowcnt[r];
     int nl = 0;
     if (len) {
       Stream s = Stream::raw(world_seed).split(5000 + (uint64_t)f);
       const int lim = min(min(nc, 6), len);
       for (int k = 0; k < lim; ++k) {
-        int j = s.randint(0, len);
-        int r = 0;
-        while (j >= sm.rowcnt[r]) { j -= sm.rowcnt[r]; ++r; }
-        int t = r * T::W;
-        for (;; ++t) {
-          const uint8_t b = sm.blk[t];
-          if (b == B_PATH || b == B_CHEST) {   // chests placed here were PATH in the list
-            if (j == 0) break;
-            --j;
-          }
-        }
+        const int t = list[s.randint(0, len)];
         if (sm.blk[t] != B_PATH || sm.itm[t] != I_EMPTY) continue;
         sm.blk[t] = B_CHEST;
         int loot, qty;
