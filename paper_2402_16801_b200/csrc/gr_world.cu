@@ -1,5 +1,5 @@
 // gr_world.cu -- procedural world generation on device, one CTA per
-// (world, floor), staged in shared memory.
+// (world, floor), the floor staged in shared memory.
 //
 // Restates worldgen.py (and perlin.py) per floor:
 //   floor 0   overworld  worldgen.py:181-327  (+ make_level_params :75-87)
@@ -10,9 +10,14 @@
 //   fallback  template   worldgen.py:549-575 after 16 failed attempts (:578-595)
 //   chests    worldgen.py:598-633, potion permutation :647-649
 // The per-tile work (noise, thresholds, sprinkles) is spread over the
-// 256 threads; every argmax/argmin of the reference becomes a block
-// reduction with numpy's first-index tie-break; the inherently sequential
-// parts (room RNG chain, L-corridors, chest picks) run on thread 0.
+// threads; every argmax/argmin of the reference becomes a block reduction
+// with numpy's first-index tie-break; the sequential RNG parts are spread
+// over threads where the counter-based streams allow it.
+//
+// Shared memory holds only the floor's blocks/items and small tables: the
+// per-tile uniforms and noise values are recomputed where needed (hashing
+// is cheaper than the occupancy that storing them costs), so ~5 CTAs fit
+// per SM next to the observation writer.
 #include <cstdint>
 #include <climits>
 #include <algorithm>
@@ -22,41 +27,34 @@
 
 namespace gr {
 
-constexpr int WG_THREADS = 256;
+constexpr int WG_THREADS = 128;
+constexpr int WG_WARPS = WG_THREADS / 32;
 constexpr double PI_D = 3.141592653589793;
 
 template <bool EXT>
 struct WT {
   static constexpr int H = EXT ? 48 : 64, W = H, HW = H * W, F = EXT ? 9 : 1;
-  static constexpr int PER = (HW + WG_THREADS - 1) / WG_THREADS;   // tiles per thread
 };
 
 template <bool EXT>
 struct WSmem {
   alignas(16) uint8_t blk[WT<EXT>::HW];
   alignas(16) uint8_t itm[WT<EXT>::HW];
-  union {
-    float h32[WT<EXT>::HW];      // overworld height
-    double f64[EXT ? WT<EXT>::HW : 1];  // cave field
-  };
-  float u[WT<EXT>::HW];          // hashed per-tile uniforms
-  float gx[252], gy[252];        // overworld gradients
+  uint16_t list[EXT ? WT<EXT>::HW : 1];   // row-major PATH tiles (chests)
+  float gx[252], gy[252];                 // overworld / realm gradients
   double dgx[EXT ? 106 : 1], dgy[EXT ? 106 : 1];  // cave gradients
-  float prof[2][8][32];          // [coarse/fine][a1..a4,b0..b3][i]
+  float prof[2][8][32];                   // [coarse/fine][a1..a4,b0..b3][i]
   double dprof[EXT ? 2 : 1][8][12];
   float ang[252];
-  // reductions
-  float rf[32];
-  double rd[32];
+  float rf[WG_WARPS];
+  double rd[WG_WARPS];
   int ri[32];
-  unsigned long long ru[32];
+  unsigned long long ru[WG_WARPS];
   int res_i;
   unsigned long long res_u;
-  int fail;
   int spawn;
-  int cr[8], cc[8], nrooms;
-  int rowcnt[64];
-  int tmp[8];
+  int cr[8], cc[8];
+  int room[8][4];
 };
 
 // ------------------------------------------------------- block reductions
@@ -73,7 +71,7 @@ __device__ int block_argmax_f(SM& sm, float v, int idx) {   // idx = INT_MAX: no
   if (threadIdx.x == 0) {
     float bv = sm.rf[0];
     int bi = sm.ri[0];
-    for (int k = 1; k < WG_THREADS / 32; ++k) {
+    for (int k = 1; k < WG_WARPS; ++k) {
       int oi = sm.ri[k];
       float ov = sm.rf[k];
       if (oi != INT_MAX && (bi == INT_MAX || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
@@ -99,7 +97,7 @@ __device__ int block_argmax_d(SM& sm, double v, int idx) {
   if (threadIdx.x == 0) {
     double bv = sm.rd[0];
     int bi = sm.ri[0];
-    for (int k = 1; k < WG_THREADS / 32; ++k) {
+    for (int k = 1; k < WG_WARPS; ++k) {
       int oi = sm.ri[k];
       double ov = sm.rd[k];
       if (oi != INT_MAX && (bi == INT_MAX || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
@@ -122,7 +120,7 @@ __device__ unsigned long long block_min_u64(SM& sm, unsigned long long v) {
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long b = sm.ru[0];
-    for (int k = 1; k < WG_THREADS / 32; ++k) b = sm.ru[k] < b ? sm.ru[k] : b;
+    for (int k = 1; k < WG_WARPS; ++k) b = sm.ru[k] < b ? sm.ru[k] : b;
     sm.res_u = b;
   }
   __syncthreads();
@@ -138,7 +136,7 @@ __device__ unsigned long long block_or_u64(SM& sm, unsigned long long v) {
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long b = 0;
-    for (int k = 0; k < WG_THREADS / 32; ++k) b |= sm.ru[k];
+    for (int k = 0; k < WG_WARPS; ++k) b |= sm.ru[k];
     sm.res_u = b;
   }
   __syncthreads();
@@ -159,7 +157,7 @@ __device__ int block_excl_scan(SM& sm, int v, int* total) {
   if (lane == 31) sm.ri[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    int w = lane < WG_THREADS / 32 ? sm.ri[lane] : 0;
+    int w = lane < WG_WARPS ? sm.ri[lane] : 0;
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += y;
@@ -168,7 +166,7 @@ __device__ int block_excl_scan(SM& sm, int v, int* total) {
   }
   __syncthreads();
   const int r = (warp ? sm.ri[warp - 1] : 0) + x - v;
-  *total = sm.ri[WG_THREADS / 32 - 1];
+  *total = sm.ri[WG_WARPS - 1];
   __syncthreads();
   return r;
 }
@@ -182,15 +180,25 @@ __device__ unsigned long long census(WSmem<EXT>& sm) {
 
 __device__ __forceinline__ int cheb(int r0, int c0, int r1, int c1) { return max(abs(r0 - r1), abs(c0 - c1)); }
 
-// argmax of u over tiles satisfying pred(t) (worldgen._pick_tile)
-template <bool EXT, class P>
-__device__ int pick_u(WSmem<EXT>& sm, const float* score, P pred) {
+// worldgen._pick_tile: argmax of score(t) over tiles with pred(t)
+template <bool EXT, class P, class S>
+__device__ int pick(WSmem<EXT>& sm, P pred, S score) {
   float bv = 0.0f;
   int bi = INT_MAX;
   for (int t = threadIdx.x; t < WT<EXT>::HW; t += WG_THREADS)
-    if (pred(t) && (bi == INT_MAX || score[t] > bv)) { bv = score[t]; bi = t; }
+    if (pred(t)) {
+      const float s = score(t);
+      if (bi == INT_MAX || s > bv) { bv = s; bi = t; }
+    }
   return block_argmax_f(sm, bv, bi);
 }
+
+// the per-tile hashed uniform field (worldgen._tile_uniform) on demand
+struct UField {
+  uint32_t k32;
+  __device__ UField(uint64_t key, uint64_t salt) : k32((uint32_t)(hash2(key, salt) & 0xFFFFFFFFull)) {}
+  __device__ __forceinline__ float operator()(int t) const { return u32f(k32, (uint32_t)t); }
+};
 
 // ------------------------------------------------------------ noise
 // perlin._profiles (perlin.py:36-51) for both octave sizes, float32
@@ -233,6 +241,15 @@ __device__ __forceinline__ float octave_at(const WSmem<EXT>& sm, int o, const fl
   return __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(t0, b0), __fmul_rn(t1, b1)), __fmul_rn(t2, b2)), __fmul_rn(t3, b3));
 }
 
+// worldgen.overworld_fields height at one tile (recomputed on demand)
+template <bool EXT>
+__device__ __forceinline__ float height_at(const WSmem<EXT>& sm, int t) {
+  const int r = t / WT<EXT>::W, c = t % WT<EXT>::W;
+  const float coarse = octave_at<EXT>(sm, 0, sm.gx, sm.gy, 2, r, c);
+  const float f1 = octave_at<EXT>(sm, 1, sm.gx + 9, sm.gy + 9, 8, r, c);
+  return __fdiv_rn(__fadd_rn(coarse, __fmul_rn(0.35f, f1)), 1.35f);
+}
+
 // worldgen._overworld_blocks for one tile
 __device__ __forceinline__ uint8_t overworld_tile(float h, float forest, float special, float u) {
   uint8_t b = B_GRASS;
@@ -251,19 +268,16 @@ __device__ __forceinline__ uint8_t overworld_tile(float h, float forest, float s
   return b;
 }
 
-// worldgen._ensure_block with a float32 score (overworld / realm)
-template <bool EXT>
-__device__ bool ensure_f32(WSmem<EXT>& sm, uint8_t block, const float* hsrc, bool low, int spawn) {
+// worldgen._ensure_block with a float32 score (overworld / realm);
+// score(t) is the *height* argument, negated here when low
+template <bool EXT, class S>
+__device__ bool ensure_f32(WSmem<EXT>& sm, uint8_t block, S hfun, bool low, int spawn) {
   using T = WT<EXT>;
   const unsigned long long present = census(sm);
   if ((present >> block) & 1ull) return true;
-  auto score = [&](int t) { return low ? -hsrc[t] : hsrc[t]; };
+  auto score = [&](int t) { const float h = hfun(t); return low ? -h : h; };
   if (!low) {
-    float bv = 0.0f;
-    int bi = INT_MAX;
-    for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
-      if (sm.blk[t] == B_STONE && (bi == INT_MAX || score(t) > bv)) { bv = score(t); bi = t; }
-    int pos = block_argmax_f(sm, bv, bi);
+    const int pos = pick(sm, [&](int t) { return sm.blk[t] == B_STONE; }, score);
     if (pos >= 0) {
       if (threadIdx.x == 0) sm.blk[pos] = block;
       __syncthreads();
@@ -279,43 +293,21 @@ __device__ bool ensure_f32(WSmem<EXT>& sm, uint8_t block, const float* hsrc, boo
   }
   any_near = __syncthreads_or(any_near);
   any_grass = __syncthreads_or(any_grass);
-  float bv = 0.0f;
-  int bi = INT_MAX;
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+  const int pos = pick(sm, [&](int t) {
     const uint8_t b = sm.blk[t];
-    const bool host = any_near ? (b == B_GRASS && near(t)) : any_grass ? b == B_GRASS : (b == B_GRASS || b == B_TREE);
-    if (host && (bi == INT_MAX || score(t) > bv)) { bv = score(t); bi = t; }
-  }
-  int pos = block_argmax_f(sm, bv, bi);
+    return any_near ? (b == B_GRASS && near(t)) : any_grass ? b == B_GRASS : (b == B_GRASS || b == B_TREE);
+  }, score);
   if (pos < 0) return false;
   if (threadIdx.x == 0) sm.blk[pos] = block;
   __syncthreads();
   return true;
 }
 
-// worldgen._gen_overworld (:247-327) on angles already in sm.ang.
-// Returns false for _Degenerate.  Spawn written to sm.spawn, ladder to *ld.
+// first walkable tile of minimal Chebyshev distance to the centre
+// (worldgen.py:267-269, and _nearest_walkable :134-143)
 template <bool EXT>
-__device__ bool gen_overworld(WSmem<EXT>& sm, uint64_t seed0, bool extended, int attempt, int* ld) {
+__device__ int nearest_walkable(WSmem<EXT>& sm) {
   using T = WT<EXT>;
-  const uint64_t key = hash2(seed0, (uint64_t)attempt);
-  const uint32_t k32 = (uint32_t)(hash2(key, 1) & 0xFFFFFFFFull);
-  // fields + sprinkles + thresholds, one pass per tile
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
-    const int r = t / T::W, c = t % T::W;
-    const float coarse = octave_at<EXT>(sm, 0, sm.gx, sm.gy, 2, r, c);
-    const float f1 = octave_at<EXT>(sm, 1, sm.gx + 9, sm.gy + 9, 8, r, c);
-    const float forest = octave_at<EXT>(sm, 1, sm.gx + 90, sm.gy + 90, 8, r, c);
-    const float special = octave_at<EXT>(sm, 1, sm.gx + 171, sm.gy + 171, 8, r, c);
-    const float h = __fdiv_rn(__fadd_rn(coarse, __fmul_rn(0.35f, f1)), 1.35f);
-    const float u = u32f(k32, (uint32_t)t);
-    sm.h32[t] = h;
-    sm.u[t] = u;
-    sm.blk[t] = overworld_tile(h, forest, special, u);
-    sm.itm[t] = 0;
-  }
-  __syncthreads();
-  // spawn: first walkable tile of minimal Chebyshev distance to the centre
   unsigned long long best = ~0ull;
   for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
     if (in_set(WALK_SET, sm.blk[t])) {
@@ -323,38 +315,55 @@ __device__ bool gen_overworld(WSmem<EXT>& sm, uint64_t seed0, bool extended, int
       best = k < best ? k : best;
     }
   best = block_min_u64(sm, best);
-  if (best == ~0ull) return false;
-  const int spawn = (int)(best & 0xFFFFFFFFull);
+  return best == ~0ull ? -1 : (int)(best & 0xFFFFFFFFull);
+}
+
+// worldgen._gen_overworld (:247-327) on gradients already in sm.gx/gy.
+// Returns false for _Degenerate.  Spawn -> sm.spawn, ladder -> *ld.
+template <bool EXT>
+__device__ bool gen_overworld(WSmem<EXT>& sm, uint64_t seed0, bool extended, int attempt, int* ld) {
+  using T = WT<EXT>;
+  const UField u(hash2(seed0, (uint64_t)attempt), 1);
+  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+    const int r = t / T::W, c = t % T::W;
+    const float forest = octave_at<EXT>(sm, 1, sm.gx + 90, sm.gy + 90, 8, r, c);
+    const float special = octave_at<EXT>(sm, 1, sm.gx + 171, sm.gy + 171, 8, r, c);
+    sm.blk[t] = overworld_tile(height_at<EXT>(sm, t), forest, special, u(t));
+    sm.itm[t] = 0;
+  }
+  __syncthreads();
+  const int spawn = nearest_walkable(sm);
+  if (spawn < 0) return false;
   if (threadIdx.x == 0) { sm.blk[spawn] = B_GRASS; sm.spawn = spawn; }
   __syncthreads();
   const unsigned long long cen = census(sm);
+  auto height = [&](int t) { return height_at<EXT>(sm, t); };
   bool fixed_any = false;
   const uint8_t order[6] = {B_COAL, B_IRON, B_DIAMOND, B_LAVA, B_WATER, B_SAND};
   for (int k = 0; k < 6; ++k) {
     if (!((cen >> order[k]) & 1ull)) {
-      if (!ensure_f32<EXT>(sm, order[k], sm.h32, k >= 4, spawn)) return false;
+      if (!ensure_f32<EXT>(sm, order[k], height, k >= 4, spawn)) return false;
       fixed_any = true;
     }
   }
-  bool stone_now = (census(sm) >> B_STONE) & 1ull;
-  if (!((cen >> B_STONE) & 1ull) || (fixed_any && !stone_now))
-    if (!ensure_f32<EXT>(sm, B_STONE, sm.h32, false, spawn)) return false;
+  if (!((cen >> B_STONE) & 1ull) || (fixed_any && !((census(sm) >> B_STONE) & 1ull)))
+    if (!ensure_f32<EXT>(sm, B_STONE, height, false, spawn)) return false;
   const int sr = spawn / T::W, sc = spawn % T::W;
   if (!((cen >> B_TREE) & 1ull)) {
-    int pos = pick_u<EXT>(sm, sm.u, [&](int t) {
+    int pos = pick(sm, [&](int t) {
       return sm.blk[t] == B_GRASS && t != spawn && cheb(t / T::W, t % T::W, sr, sc) <= 8;
-    });
-    if (pos < 0) pos = pick_u<EXT>(sm, sm.u, [&](int t) { return sm.blk[t] == B_GRASS; });
+    }, u);
+    if (pos < 0) pos = pick(sm, [&](int t) { return sm.blk[t] == B_GRASS; }, u);
     if (pos < 0) return false;
     if (threadIdx.x == 0) sm.blk[pos] = B_TREE;
     __syncthreads();
   }
   *ld = -1;
   if (extended) {
-    int pos = pick_u<EXT>(sm, sm.u, [&](int t) {
+    int pos = pick(sm, [&](int t) {
       return in_set(WALK_SET, sm.blk[t]) && cheb(t / T::W, t % T::W, sr, sc) >= 10;
-    });
-    if (pos < 0) pos = pick_u<EXT>(sm, sm.u, [&](int t) { return in_set(WALK_SET, sm.blk[t]); });
+    }, u);
+    if (pos < 0) pos = pick(sm, [&](int t) { return in_set(WALK_SET, sm.blk[t]); }, u);
     if (pos < 0 || pos == spawn) return false;
     if (threadIdx.x == 0) sm.itm[pos] = I_LADDER_DOWN;
     __syncthreads();
@@ -388,7 +397,7 @@ __device__ bool gen_realm(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt,
   overworld_gradients<EXT>(sm);
   int ld_unused;
   if (!gen_overworld<EXT>(sm, hash2(seed, 4000 + (uint64_t)attempt), false, attempt, &ld_unused)) return false;
-  const uint32_t k32 = (uint32_t)(hash2(hash2(seed, 13 + (uint64_t)attempt), 6) & 0xFFFFFFFFull);
+  const UField u(hash2(seed, 13 + (uint64_t)attempt), 6);
   const uint8_t gem = floor == 6 ? B_RUBY : B_SAPPHIRE;
   for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
     uint8_t b = sm.blk[t], d = b;
@@ -399,41 +408,26 @@ __device__ bool gen_realm(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt,
       if (b == B_GRASS) d = B_ICE_GRASS; else if (b == B_TREE) d = B_ICE_SHRUB;
       else if (b == B_SAND) d = B_GRAVEL; else if (b == B_LAVA) d = B_WATER;
     }
-    const float u = u32f(k32, (uint32_t)t);
-    sm.u[t] = u;
-    if (d == B_STONE && u > 0.975f) d = gem;
+    if (d == B_STONE && u(t) > 0.975f) d = gem;
     sm.blk[t] = d;
   }
   __syncthreads();
-  if (!ensure_f32<EXT>(sm, gem, sm.u, false, -1)) return false;
-  unsigned long long best = ~0ull;
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
-    if (in_set(WALK_SET, sm.blk[t])) {
-      unsigned long long k = ((unsigned long long)cheb(t / T::W, t % T::W, T::H / 2, T::W / 2) << 32) | (unsigned)t;
-      best = k < best ? k : best;
-    }
-  best = block_min_u64(sm, best);
-  if (best == ~0ull) return false;
-  const int spawn = (int)(best & 0xFFFFFFFFull), sr = spawn / T::W, sc = spawn % T::W;
-  int tpos = pick_u<EXT>(sm, sm.u, [&](int t) {
+  if (!ensure_f32<EXT>(sm, gem, u, false, -1)) return false;
+  const int spawn = nearest_walkable(sm);
+  if (spawn < 0) return false;
+  const int sr = spawn / T::W, sc = spawn % T::W;
+  const int tpos = pick(sm, [&](int t) {
     return in_set(WALK_SET, sm.blk[t]) && cheb(t / T::W, t % T::W, sr, sc) <= 8;
-  });
+  }, u);
   if (tpos < 0 || tpos == spawn) return false;
   if (threadIdx.x == 0) sm.blk[tpos] = floor == 6 ? B_ENCHANT_FIRE : B_ENCHANT_ICE;
   __syncthreads();
-  int down = pick_u<EXT>(sm, sm.u, [&](int t) {
+  int down = pick(sm, [&](int t) {
     return in_set(WALK_SET, sm.blk[t]) && cheb(t / T::W, t % T::W, sr, sc) >= 10;
-  });
-  if (down < 0) {
-    // _pick_tile(out, walk, 1.0 - u)
-    float bv = 0.0f;
-    int bi = INT_MAX;
-    for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
-      const float v = __fsub_rn(1.0f, sm.u[t]);
-      if (in_set(WALK_SET, sm.blk[t]) && (bi == INT_MAX || v > bv)) { bv = v; bi = t; }
-    }
-    down = block_argmax_f(sm, bv, bi);
-  }
+  }, u);
+  if (down < 0)   // _pick_tile(out, walk, 1.0 - u)
+    down = pick(sm, [&](int t) { return in_set(WALK_SET, sm.blk[t]); },
+                [&](int t) { return __fsub_rn(1.0f, u(t)); });
   if (down < 0 || down == spawn) return false;
   for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) sm.itm[t] = 0;
   __syncthreads();
@@ -443,7 +437,7 @@ __device__ bool gen_realm(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt,
   return true;
 }
 
-// worldgen._carve_line on thread 0
+// worldgen._carve_line
 template <bool EXT>
 __device__ void carve(WSmem<EXT>& sm, int r, int c, int tr, int tc) {
   using T = WT<EXT>;
@@ -468,16 +462,14 @@ __device__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floor, int attemp
     const int c0 = 2 + (int)(hash2(s0.key, c + 3) % (uint64_t)(T::W - rw - 4));
     sm.cr[k] = r0 + rh / 2;
     sm.cc[k] = c0 + rw / 2;
-    // room rectangles stashed in rowcnt (4 ints per room)
-    sm.rowcnt[4 * k] = r0; sm.rowcnt[4 * k + 1] = r0 + rh;
-    sm.rowcnt[4 * k + 2] = c0; sm.rowcnt[4 * k + 3] = c0 + rw;
+    sm.room[k][0] = r0; sm.room[k][1] = r0 + rh; sm.room[k][2] = c0; sm.room[k][3] = c0 + rw;
   }
   __syncthreads();
   for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
     const int r = t / T::W, c = t % T::W;
     bool in = false;
     for (int k = 0; k < n; ++k)
-      in |= r >= sm.rowcnt[4 * k] && r < sm.rowcnt[4 * k + 1] && c >= sm.rowcnt[4 * k + 2] && c < sm.rowcnt[4 * k + 3];
+      in |= r >= sm.room[k][0] && r < sm.room[k][1] && c >= sm.room[k][2] && c < sm.room[k][3];
     sm.blk[t] = in ? B_PATH : B_WALL;
     sm.itm[t] = 0;
   }
@@ -489,38 +481,41 @@ __device__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floor, int attemp
     carve<EXT>(sm, sm.cr[k], sm.cc[k], sm.cr[k + 1], sm.cc[k + 1]);
   }
   __syncthreads();
-  const uint32_t k32 = (uint32_t)(hash2(hash2(seed, 7 + (uint64_t)attempt), 4) & 0xFFFFFFFFull);
-  uint8_t nb[WT<EXT>::PER];
+  // moss / sewer water / vault gravel read the pre-pass PATH mask: compute
+  // into registers first, write after the barrier
+  const UField u(hash2(seed, 7 + (uint64_t)attempt), 4);
+  constexpr int PER = (T::HW + WG_THREADS - 1) / WG_THREADS;
+  uint8_t nb[PER];
 #pragma unroll
-  for (int q = 0; q < WT<EXT>::PER; ++q) {
+  for (int q = 0; q < PER; ++q) {
     const int t = threadIdx.x + q * WG_THREADS;
     if (t >= T::HW) break;
     const int r = t / T::W, c = t % T::W;
-    const float u = u32f(k32, (uint32_t)t);
-    sm.u[t] = u;
+    const float uu = u(t);
     const uint8_t b = sm.blk[t];
     const bool path = b == B_PATH;
     const bool near_path = path || (r > 0 && sm.blk[t - T::W] == B_PATH) || (r < T::H - 1 && sm.blk[t + T::W] == B_PATH) ||
                            (c > 0 && sm.blk[t - 1] == B_PATH) || (c < T::W - 1 && sm.blk[t + 1] == B_PATH);
     uint8_t d = b;
-    if (b == B_WALL && near_path && u < 0.25f) d = B_WALL_MOSS;
-    if (floor == 3 && path && u > 0.82f) d = B_WATER;
-    if (floor == 4 && path && u > 0.85f) d = B_GRAVEL;
+    if (b == B_WALL && near_path && uu < 0.25f) d = B_WALL_MOSS;
+    if (floor == 3 && path && uu > 0.82f) d = B_WATER;
+    if (floor == 4 && path && uu > 0.85f) d = B_GRAVEL;
     nb[q] = d;
   }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < WT<EXT>::PER; ++q) {
+  for (int q = 0; q < PER; ++q) {
     const int t = threadIdx.x + q * WG_THREADS;
     if (t < T::HW) sm.blk[t] = nb[q];
   }
   __syncthreads();
-  const int fountain = pick_u<EXT>(sm, sm.u, [&](int t) { return sm.blk[t] == B_PATH; });
+  const int fountain = pick(sm, [&](int t) { return sm.blk[t] == B_PATH; }, u);
   if (fountain >= 0 && threadIdx.x == 0) sm.blk[fountain] = B_FOUNTAIN;
   __syncthreads();
   const int up = sm.cr[0] * T::W + sm.cc[0], down = sm.cr[n - 1] * T::W + sm.cc[n - 1];
-  if (sm.blk[up] != B_PATH || sm.blk[down] != B_PATH || up == down) return false;
+  const bool ok = sm.blk[up] == B_PATH && sm.blk[down] == B_PATH && up != down;
   __syncthreads();
+  if (!ok) return false;
   if (threadIdx.x == 0) { sm.itm[up] = I_LADDER_UP; sm.itm[down] = I_LADDER_DOWN; }
   __syncthreads();
   fo->spawn = up; fo->lu = up; fo->ld = down;
@@ -566,6 +561,15 @@ __device__ __forceinline__ double octave_at_d(const WSmem<EXT>& sm, int o, const
   return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(t0, b0), __dmul_rn(t1, b1)), __dmul_rn(t2, b2)), __dmul_rn(t3, b3));
 }
 
+// perlin.perlin with CAVE_OCTAVES in float64 at one tile
+template <bool EXT>
+__device__ __forceinline__ double cave_field_at(const WSmem<EXT>& sm, int t) {
+  const int r = t / WT<EXT>::W, c = t % WT<EXT>::W;
+  const double o1 = octave_at_d<EXT>(sm, 0, sm.dgx, sm.dgy, 4, r, c);
+  const double o2 = octave_at_d<EXT>(sm, 1, sm.dgx + 25, sm.dgy + 25, 8, r, c);
+  return __ddiv_rn(__dadd_rn(__dmul_rn(1.0, o1), __dmul_rn(0.5, o2)), 1.5);
+}
+
 // worldgen._gen_cave (:418-468)
 template <bool EXT>
 __device__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo, bool* fragile) {
@@ -579,30 +583,25 @@ __device__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, 
     sm.dgy[k] = sn;
   }
   __syncthreads();
-  const uint32_t k32 = (uint32_t)(hash2(hash2(seed, 11 + (uint64_t)attempt), 5) & 0xFFFFFFFFull);
+  const UField u(hash2(seed, 11 + (uint64_t)attempt), 5);
   int frag = 0;
   for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
-    const int r = t / T::W, c = t % T::W;
-    const double o1 = octave_at_d<EXT>(sm, 0, sm.dgx, sm.dgy, 4, r, c);
-    const double o2 = octave_at_d<EXT>(sm, 1, sm.dgx + 25, sm.dgy + 25, 8, r, c);
-    const double field = __ddiv_rn(__dadd_rn(__dmul_rn(1.0, o1), __dmul_rn(0.5, o2)), 1.5);
+    const double field = cave_field_at<EXT>(sm, t);
     frag |= fabs(field + 0.02) < 1e-12 || fabs(field + 0.62) < 1e-12;
-    sm.f64[t] = field;
-    const float u = u32f(k32, (uint32_t)t);
-    sm.u[t] = u;
+    const float uu = u(t);
     const bool open = field > -0.02;
     uint8_t b = open ? B_PATH : B_STONE;
-    if (open && u < 0.04f) b = B_STALAGMITE;
+    if (open && uu < 0.04f) b = B_STALAGMITE;
     if (b == B_STONE) {
       if (floor == 2) {
-        if (u < 0.06f) b = B_COAL;
-        if (u >= 0.90f && u < 0.93f) b = B_IRON;
-        if (u >= 0.975f) b = B_SAPPHIRE;
+        if (uu < 0.06f) b = B_COAL;
+        if (uu >= 0.90f && uu < 0.93f) b = B_IRON;
+        if (uu >= 0.975f) b = B_SAPPHIRE;
       } else {
-        if (u < 0.05f) b = B_COAL;
-        if (u >= 0.90f && u < 0.93f) b = B_IRON;
-        if (u >= 0.96f && u < 0.975f) b = B_DIAMOND;
-        if (u >= 0.985f) b = B_RUBY;
+        if (uu < 0.05f) b = B_COAL;
+        if (uu >= 0.90f && uu < 0.93f) b = B_IRON;
+        if (uu >= 0.96f && uu < 0.975f) b = B_DIAMOND;
+        if (uu >= 0.985f) b = B_RUBY;
       }
     }
     if (floor != 2 && field < -0.62) b = B_LAVA;
@@ -621,7 +620,10 @@ __device__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, 
     double bv = 0.0;
     int bi = INT_MAX;
     for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
-      if (sm.blk[t] == B_STONE && (bi == INT_MAX || -sm.f64[t] > bv)) { bv = -sm.f64[t]; bi = t; }
+      if (sm.blk[t] == B_STONE) {
+        const double sc = -cave_field_at<EXT>(sm, t);
+        if (bi == INT_MAX || sc > bv) { bv = sc; bi = t; }
+      }
     const int pos = block_argmax_d(sm, bv, bi);
     if (pos < 0) return false;   // no stone and caves hold no grass / trees
     if (threadIdx.x == 0) sm.blk[pos] = b;
@@ -629,22 +631,10 @@ __device__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, 
   }
   int cnt = 0;
   for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) cnt += sm.blk[t] == B_PATH;
-  {
-    // block sum of cnt
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
-    if ((threadIdx.x & 31) == 0) sm.ri[threadIdx.x >> 5] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int tot = 0;
-      for (int k = 0; k < WG_THREADS / 32; ++k) tot += sm.ri[k];
-      sm.res_i = tot;
-    }
-    __syncthreads();
-    cnt = sm.res_i;
-    __syncthreads();
-  }
-  if (cnt < 40) return false;
-  const int up = pick_u<EXT>(sm, sm.u, [&](int t) { return sm.blk[t] == B_PATH; });
+  int total;
+  block_excl_scan(sm, cnt, &total);
+  if (total < 40) return false;
+  const int up = pick(sm, [&](int t) { return sm.blk[t] == B_PATH; }, u);
   if (up < 0) return false;
   const int ur = up / T::W, uc = up % T::W;
   // argmax of chebyshev(up)/max over open tiles == argmax of the distance
@@ -732,7 +722,7 @@ __device__ void gen_template(WSmem<EXT>& sm, int floor, FloorOut* fo) {
   __syncthreads();
 }
 
-// worldgen._assign_chests for one floor (:598-623), thread 0
+// worldgen._assign_chests for one floor (:598-623)
 template <bool EXT>
 __device__ void assign_chests(WSmem<EXT>& sm, uint64_t world_seed, int f, WMeta* meta) {
   using T = WT<EXT>;
@@ -742,9 +732,7 @@ __device__ void assign_chests(WSmem<EXT>& sm, uint64_t world_seed, int f, WMeta*
     if (threadIdx.x == 0) meta->nch[f] = 0;
     return;
   }
-  // the row-major list of PATH tiles (np.nonzero) via a block scan; it
-  // lives in the u buffer, which is dead by now
-  uint16_t* list = reinterpret_cast<uint16_t*>(sm.u);
+  // the row-major list of PATH tiles (np.nonzero) via a block scan
   constexpr int PER = (T::HW + WG_THREADS - 1) / WG_THREADS;
   const int t0 = threadIdx.x * PER, t1 = min(t0 + PER, T::HW);
   int cnt = 0;
@@ -752,7 +740,7 @@ __device__ void assign_chests(WSmem<EXT>& sm, uint64_t world_seed, int f, WMeta*
   int len;
   int off = block_excl_scan(sm, cnt, &len);
   for (int t = t0; t < t1; ++t)
-    if (sm.blk[t] == B_PATH) list[off++] = (uint16_t)t;
+    if (sm.blk[t] == B_PATH) sm.list[off++] = (uint16_t)t;
   __syncthreads();
   if (threadIdx.x == 0) {
     int nl = 0;
@@ -760,7 +748,7 @@ __device__ void assign_chests(WSmem<EXT>& sm, uint64_t world_seed, int f, WMeta*
       Stream s = Stream::raw(world_seed).split(5000 + (uint64_t)f);
       const int lim = min(min(nc, 6), len);
       for (int k = 0; k < lim; ++k) {
-        const int t = list[s.randint(0, len)];
+        const int t = sm.list[s.randint(0, len)];
         if (sm.blk[t] != B_PATH || sm.itm[t] != I_EMPTY) continue;
         sm.blk[t] = B_CHEST;
         int loot, qty;
@@ -792,7 +780,7 @@ __device__ void assign_chests(WSmem<EXT>& sm, uint64_t world_seed, int f, WMeta*
 }
 
 template <bool EXT>
-__global__ void __launch_bounds__(WG_THREADS) k_worldgen(WorldJob job) {
+__global__ void __launch_bounds__(WG_THREADS, 8) k_worldgen(WorldJob job) {
   using T = WT<EXT>;
   __shared__ WSmem<EXT> sm;
   const int64_t nworlds = job.mode == 1 ? (int64_t)job.info->n_pool : job.count;
@@ -897,12 +885,12 @@ __global__ void __launch_bounds__(WG_THREADS) k_worldgen(WorldJob job) {
 }
 
 void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st) {
-  // persistent grid: a few CTAs per SM walk the (world, floor) items
+  // persistent grid: CTAs walk the (world, floor) items
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int64_t max_items = (j.mode == 0 ? j.count : j.out.cap) * (ext ? 9 : 1);
-  int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * 4);
+  int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * 8);
   if (grid <= 0) return;
   if (ext) k_worldgen<true><<<grid, WG_THREADS, 0, st>>>(j);
   else k_worldgen<false><<<grid, WG_THREADS, 0, st>>>(j);
