@@ -789,8 +789,11 @@ __global__ void __launch_bounds__(WG_THREADS, 8) k_worldgen(WorldJob job) {
   if (EXT) build_profiles_f64<EXT>(sm);
   __syncthreads();
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-    const int64_t w = it / T::F;
-    const int f = (int)(it % T::F);
+    // floor-major order: CTAs resident at the same time run the same floor
+    // generator, which keeps the instruction cache warm (no_instructions
+    // stalls dominated a world-major order)
+    const int64_t w = it % nworlds;
+    const int f = (int)(it / nworlds);
     uint64_t seed, key;
     if (job.mode == 0) {
       seed = hash2(job.env_key, hash2((uint64_t)(job.env_offset + w), 0));
