@@ -1210,7 +1210,7 @@ __device__ __forceinline__ void apply_pending(Ctx& e, uint8_t pend, uint32_t pre
 }
 
 template <bool EXT>
-__global__ void __launch_bounds__(128) k_step(DS S, StepArgs a) {
+__global__ void __launch_bounds__(128, 4) k_step(DS S, StepArgs a) {
   using T = TD<EXT>;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < a.n && !(a.bad && a.bad[0] >= 0);
