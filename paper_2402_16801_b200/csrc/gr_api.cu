@@ -152,6 +152,7 @@ struct gr_env {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   const uint8_t* last_done = nullptr;
   bool overlap = false;   // GR_OVERLAP=1: reset work on a side stream (measured slower so far)
+  bool tma = true;        // GR_TMA=0: plain 16-byte stores for the observation rows
   std::vector<void*> allocs;
 };
 
@@ -245,6 +246,7 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   e->cfg.n_envs_global = ng;
   if (e->cfg.max_episode_length <= 0) e->cfg.max_episode_length = 100000;
   if (const char* ov = getenv("GR_OVERLAP")) e->overlap = atoi(ov) != 0;
+  if (const char* tm = getenv("GR_TMA")) e->tma = atoi(tm) != 0;
   e->ext = cfg->tier == GR_TIER_EXTENDED;
   e->d = e->ext ? EXT_DIMS : CLASSIC_DIMS;
   e->n = cfg->n_envs;
@@ -323,7 +325,8 @@ static int observe(gr_env* e, void* obs_dev, cudaStream_t st, bool recompute_fla
     PTimer t(e, PK_OTHER, st);
     k_dark<<<(unsigned)e->nb, 128, 0, st>>>(e->S, e->n, e->cur_flags);
   }
-  ObsArgs oa{obs_dev, e->n, recompute_flags ? e->cur_flags : e->prev_flags, e->cfg.tile_px, e->last_done, sel};
+  ObsArgs oa{obs_dev, e->n, recompute_flags ? e->cur_flags : e->prev_flags, e->cfg.tile_px, e->last_done, sel,
+             e->tma ? 1 : 0};
   {
     PTimer t(e, PK_OBS, st);
     if (e->cfg.obs_mode == GR_OBS_SYMBOLIC) launch_symbolic(e->ext, e->S, oa, st);

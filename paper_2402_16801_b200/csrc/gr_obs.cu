@@ -636,16 +636,32 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
         tv[O::STRIDE - 1] = v.light[t];
       }
       for (int k = lane; k < O::NINV; k += 32) sr[O::T * O::STRIDE + k] = __uint_as_float(v.desc[D_INV + k]);
-      __syncwarp();
-      const int head = (4 - shift) & 3;
-      if (lane < head) row[lane] = sr[lane];
-      const int nv = (O::L - head) >> 2;
-      const float4* s4 = reinterpret_cast<const float4*>(sr + head);
-      float4* g4 = reinterpret_cast<float4*>(row + head);
-      for (int q = lane; q < nv; q += 32) g4[q] = s4[q];
-      const int tl = head + nv * 4;
-      if (tl + lane < O::L) row[tl + lane] = sr[tl + lane];
-      __syncwarp();
+      if (EXT && a.tma) {
+        // extended rows are 33,072 B = 16-byte multiple at 16-byte aligned
+        // addresses: one TMA bulk store (cp.async.bulk) per row, issued by
+        // one lane; the warp only waits until the stage has been read
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(sr);
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       :: "l"(row), "r"(saddr), "r"((uint32_t)(O::L * 4)) : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        __syncwarp();
+      } else {
+        __syncwarp();
+        const int head = (4 - shift) & 3;
+        if (lane < head) row[lane] = sr[lane];
+        const int nv = (O::L - head) >> 2;
+        const float4* s4 = reinterpret_cast<const float4*>(sr + head);
+        float4* g4 = reinterpret_cast<float4*>(row + head);
+        for (int q = lane; q < nv; q += 32) g4[q] = s4[q];
+        const int tl = head + nv * 4;
+        if (tl + lane < O::L) row[tl + lane] = sr[tl + lane];
+        __syncwarp();
+      }
       for (int t = lane; t < O::T; t += 32) {
         const uint32_t g = v.tgt[t];
         float* tv = sr + t * O::STRIDE;
@@ -722,6 +738,8 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
       __syncwarp();
     }
   }
+  // bulk stores must complete before the CTA retires
+  if (EXT && a.tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
