@@ -219,6 +219,7 @@ def main():
     clocks.start()
     time.sleep(0.3)
     gb.set_profiling(True)
+    episodes0 = gb.episodes_completed()
     launches0 = gb.kernel_launches()
     if dist:
         dist.barrier()
@@ -236,6 +237,7 @@ def main():
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     launches = gb.kernel_launches() - launches0
+    resets_per_step = (gb.episodes_completed() - episodes0) / args.steps
     gb.set_profiling(False)
     ktimes = gb.kernel_times()
     clk = clocks.stop()
@@ -251,7 +253,9 @@ def main():
     dom_ms, dom_n = ktimes[dom]
     key = (args.tier, args.obs)
     if dom == "obs" and key in OBS_KERNEL_BYTES:
-        bytes_per_launch = OBS_KERNEL_BYTES[key] * gb.n
+        # the main writer renders every env not reset this step; the reset
+        # envs are rendered by a small launch after their install (obs_reset)
+        bytes_per_launch = int(OBS_KERNEL_BYTES[key] * (gb.n - resets_per_step))
     else:
         bytes_per_launch = STEP_BYTES[key] * gb.n
     per_launch_ms = dom_ms / max(dom_n, 1)
@@ -267,6 +271,7 @@ def main():
                 "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
                 "bytes_per_launch": bytes_per_launch, "ms_per_launch": round(per_launch_ms, 5),
                 "share_of_step": round(dom_ms / ms, 3), "peak_source": peak_src,
+                "resets_per_step": round(resets_per_step, 1),
                 "step_frac": round(value / world * STEP_BYTES[key] / 1e9 / peak, 4)}
 
     # end to end through the host-buffer C ABI (pinned host memory)

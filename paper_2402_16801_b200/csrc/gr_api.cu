@@ -99,7 +99,7 @@ static int fail(int code, const char* fmt, ...) {
   } while (0)
 
 // per-kernel CUDA-event timing (gr_set_profiling / gr_kernel_times)
-enum { PK_STEP, PK_SCAN, PK_INFO, PK_WORLDGEN, PK_INSTALL, PK_OBS, PK_POLICY, PK_OTHER, PK_N };
+enum { PK_STEP, PK_SCAN, PK_INFO, PK_WORLDGEN, PK_INSTALL, PK_OBS, PK_POLICY, PK_OTHER, PK_OBS_RESET, PK_N };
 
 struct Prof {
   bool on = false;
@@ -151,8 +151,9 @@ struct gr_env {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   const uint8_t* last_done = nullptr;
-  bool overlap = false;   // GR_OVERLAP=1: reset work on a side stream (measured slower so far)
+  bool overlap = true;    // GR_OVERLAP=0: reset work serialised after the step on one stream
   bool tma = true;        // GR_TMA=0: plain 16-byte stores for the observation rows
+  int obs_ctas_overlap = 2;   // writer CTAs/SM while the reset work runs beside it
   std::vector<void*> allocs;
 };
 
@@ -247,6 +248,7 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (e->cfg.max_episode_length <= 0) e->cfg.max_episode_length = 100000;
   if (const char* ov = getenv("GR_OVERLAP")) e->overlap = atoi(ov) != 0;
   if (const char* tm = getenv("GR_TMA")) e->tma = atoi(tm) != 0;
+  if (const char* oc = getenv("GR_OBS_CTAS")) e->obs_ctas_overlap = atoi(oc);
   e->ext = cfg->tier == GR_TIER_EXTENDED;
   e->d = e->ext ? EXT_DIMS : CLASSIC_DIMS;
   e->n = cfg->n_envs;
@@ -326,9 +328,9 @@ static int observe(gr_env* e, void* obs_dev, cudaStream_t st, bool recompute_fla
     k_dark<<<(unsigned)e->nb, 128, 0, st>>>(e->S, e->n, e->cur_flags);
   }
   ObsArgs oa{obs_dev, e->n, recompute_flags ? e->cur_flags : e->prev_flags, e->cfg.tile_px, e->last_done, sel,
-             e->tma ? 1 : 0};
+             e->tma ? 1 : 0, sel == 1 ? e->obs_ctas_overlap : 0};
   {
-    PTimer t(e, PK_OBS, st);
+    PTimer t(e, sel == 2 ? PK_OBS_RESET : PK_OBS, st);
     if (e->cfg.obs_mode == GR_OBS_SYMBOLIC) launch_symbolic(e->ext, e->S, oa, st);
     else launch_pixels(e->ext, e->S, oa, st);
   }

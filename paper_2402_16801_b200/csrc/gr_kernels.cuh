@@ -66,6 +66,7 @@ struct ObsArgs {
   const uint8_t* done;      // this step's done flags (for sel 1/2)
   int sel;                  // 0: every env, 1: envs not reset this step, 2: envs reset this step
   int tma;                  // extended rows leave shared memory through TMA bulk stores
+  int ctas_per_sm;          // resident CTAs per SM of the writer (0 = default)
 };
 
 void launch_step(bool ext, const DS& S, const StepArgs& a, cudaStream_t st);

@@ -755,7 +755,8 @@ void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
       cudaFuncSetAttribute(k_symbolic_stage<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    const int grid = (int)std::min<int64_t>((a.n + NW - 1) / NW, (int64_t)sms * 3);
+    const int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm : 3;
+    const int grid = (int)std::min<int64_t>((a.n + NW - 1) / NW, (int64_t)sms * per_sm);
     k_symbolic_stage<true><<<grid, NW * 32, smem, st>>>(S, a);
   } else {
     constexpr int NW = stage_warps<false>();

@@ -207,7 +207,7 @@ class GridrogueBatch:
     def kernel_launches(self) -> int:
         return int(lib().gr_kernel_launches(self.h))
 
-    KERNEL_CLASSES = ("step", "scan", "info", "worldgen", "install", "obs", "policy", "other")
+    KERNEL_CLASSES = ("step", "scan", "info", "worldgen", "install", "obs", "policy", "other", "obs_reset")
 
     def set_profiling(self, on: bool) -> None:
         check(lib().gr_set_profiling(self.h, 1 if on else 0))
