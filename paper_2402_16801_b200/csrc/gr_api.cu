@@ -32,7 +32,8 @@ void launch_scan(const int32_t* block_done, int32_t* block_off, int nb, const ui
 void launch_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t step_key, StepInfo* info,
                         uint32_t* flags_out, cudaStream_t st);
 void launch_install_initial(bool ext, const DS& S, const WBuf& wb, int64_t n, cudaStream_t st);
-void launch_install_pool(bool ext, const DS& S, const InstallArgs& a, const int32_t* block_off, cudaStream_t st);
+void launch_install_pool(bool ext, const DS& S, const InstallArgs& a, cudaStream_t st);
+void launch_compact(const uint8_t* done, int64_t n, const int32_t* block_off, int32_t* list, cudaStream_t st);
 
 // policies.RandomPolicy.actions (policies.py:31-37)
 __global__ void k_random_actions(int64_t* out, int64_t n, int64_t env0, uint32_t key, int na) {
@@ -127,6 +128,7 @@ struct gr_env {
   WBuf pool;
   WMeta* init_meta = nullptr;
   int32_t *block_done = nullptr, *block_off = nullptr, *exchange = nullptr;
+  int32_t* done_list = nullptr;                 // this step's done envs, local rank order
   uint32_t *cur_flags = nullptr, *prev_flags = nullptr;
   StepInfo* info = nullptr;
   unsigned long long* bad = nullptr;
@@ -273,6 +275,7 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->pool.meta, cap * sizeof(WMeta));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->block_done, e->nb * sizeof(int32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->block_off, e->nb * sizeof(int32_t));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->done_list, e->n * sizeof(int32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->exchange, 4 * sizeof(int32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->cur_flags, sizeof(uint32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->prev_flags, sizeof(uint32_t));
@@ -328,7 +331,7 @@ static int observe(gr_env* e, void* obs_dev, cudaStream_t st, bool recompute_fla
     k_dark<<<(unsigned)e->nb, 128, 0, st>>>(e->S, e->n, e->cur_flags);
   }
   ObsArgs oa{obs_dev, e->n, recompute_flags ? e->cur_flags : e->prev_flags, e->cfg.tile_px, e->last_done, sel,
-             e->tma ? 1 : 0, sel == 1 ? e->obs_ctas_overlap : 0};
+             e->tma ? 1 : 0, sel == 1 ? e->obs_ctas_overlap : 0, e->done_list, e->info};
   {
     PTimer t(e, sel == 2 ? PK_OBS_RESET : PK_OBS, st);
     if (e->cfg.obs_mode == GR_OBS_SYMBOLIC) launch_symbolic(e->ext, e->S, oa, st);
@@ -454,6 +457,10 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
     CK(cudaEventRecord(e->ev_fork, st));
     CK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
   }
+  {
+    PTimer t(e, PK_SCAN, rs);
+    launch_compact((const uint8_t*)e->S.f[GR_F_DONE], e->n, e->block_off, e->done_list, rs);
+  }
   WorldJob j{};
   j.mode = 1;
   j.info = e->info;
@@ -467,6 +474,7 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
   InstallArgs ia{};
   ia.mode = 1;
   ia.n = e->n;
+  ia.done_list = e->done_list;
   ia.info = e->info;
   ia.pool = e->pool;
   ia.M = e->M;
@@ -476,7 +484,7 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
   ia.st_ach = e->st_ach;
   {
     PTimer t(e, PK_INSTALL, rs);
-    launch_install_pool(e->ext, e->S, ia, e->block_off, rs);
+    launch_install_pool(e->ext, e->S, ia, rs);
   }
   CK(cudaGetLastError());
   e->step_index += 1;

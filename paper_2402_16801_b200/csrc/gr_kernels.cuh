@@ -47,7 +47,7 @@ struct WorldJob {
 struct InstallArgs {
   int mode;                   // 0: initial (world w -> env w, maps already in place), 1: pool
   int64_t n;                  // mode 0 env count
-  const int64_t* done_list;   // mode 1: env index per local done rank
+  const int32_t* done_list;   // mode 1: env index per local done rank (k_compact)
   const StepInfo* info;
   WBuf pool;
   int64_t M;
@@ -67,6 +67,8 @@ struct ObsArgs {
   int sel;                  // 0: every env, 1: envs not reset this step, 2: envs reset this step
   int tma;                  // extended rows leave shared memory through TMA bulk stores
   int ctas_per_sm;          // resident CTAs per SM of the writer (0 = default)
+  const int32_t* list;      // sel 2: the done list (k_compact) ...
+  const StepInfo* info;     // ... of info->k_local entries
 };
 
 void launch_step(bool ext, const DS& S, const StepArgs& a, cudaStream_t st);

@@ -318,8 +318,10 @@ __global__ void __launch_bounds__(128) k_pixels(DS S, ObsArgs a) {
   const int FH = (O::VR + 2) * px, FW = (O::VC + side) * px;
   const int inset = max(1, px / 4);
   const int64_t frame = (int64_t)FH * FW * 3;
-  for (int64_t i = blockIdx.x; i < a.n; i += gridDim.x) {
-    if (a.sel && (a.done[i] != 0) != (a.sel == 2)) continue;   // CTA-uniform env filter
+  const int64_t count = a.sel == 2 ? (int64_t)a.info->k_local : a.n;
+  for (int64_t j = blockIdx.x; j < count; j += gridDim.x) {
+    const int64_t i = a.sel == 2 ? (int64_t)a.list[j] : j;   // sel 2: reset envs only
+    if (a.sel == 1 && a.done[i]) continue;                      // CTA-uniform env filter
     if (threadIdx.x < 32) {
       // render_tiles sees a one-env batch: glow iff this env's floor is dark
       const int pf = EXT ? GR_AT(S, GR_F_PFLOOR, uint8_t, 0, i) : 0;
@@ -555,8 +557,10 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
   for (int q = lane; q < SC / 4; q += 32) reinterpret_cast<float4*>(stage)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncwarp();
   const bool glow = EXT && a.flags && (a.flags[0] & 4u);
-  for (int64_t i = (int64_t)blockIdx.x * NW + warp; i < a.n; i += (int64_t)gridDim.x * NW) {
-    if (a.sel && (a.done[i] != 0) != (a.sel == 2)) continue;   // warp-uniform env filter
+  const int64_t count = a.sel == 2 ? (int64_t)a.info->k_local : a.n;
+  for (int64_t j = (int64_t)blockIdx.x * NW + warp; j < count; j += (int64_t)gridDim.x * NW) {
+    const int64_t i = a.sel == 2 ? (int64_t)a.list[j] : j;   // sel 2: reset envs only
+    if (a.sel == 1 && a.done[i]) continue;                      // warp-uniform env filter
     const uint2 dw = reinterpret_cast<const uint2*>(S.desc + (size_t)i * DESC_WORDS)[lane];
     v.desc[2 * lane] = dw.x;
     v.desc[2 * lane + 1] = dw.y;

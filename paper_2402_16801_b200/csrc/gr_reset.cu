@@ -205,39 +205,37 @@ __global__ void __launch_bounds__(128) k_install_initial(DS S, WBuf wb, int64_t 
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) install_one<EXT>(S, i, wb.meta[i], nullptr, nullptr);
 }
 
-// auto-reset: each CTA owns 128 consecutive envs; done envs get their
-// global rank from the block scan, record EpisodeStats, then install.
-template <bool EXT>
-__global__ void __launch_bounds__(128) k_install_pool(DS S, InstallArgs a, const int32_t* block_off) {
-  constexpr int F = EXT ? 9 : 1, HW = EXT ? 48 * 48 : 64 * 64, A = EXT ? 67 : 22;
-  __shared__ int32_t list[128];
-  __shared__ int cnt;
-  const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
-  const bool d = i < a.n && GR_AT(S, GR_F_DONE, uint8_t, 0, i);
-  const unsigned bal = __ballot_sync(0xffffffffu, d);
+// done envs in ascending order: local rank = block offset (k_scan) + rank
+// inside the 128-env block (ballots)
+__global__ void __launch_bounds__(128) k_compact(const uint8_t* done, int64_t n, const int32_t* block_off,
+                                                 int32_t* list) {
   __shared__ int wcnt[4];
+  const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const bool d = i < n && done[i];
+  const unsigned bal = __ballot_sync(0xffffffffu, d);
   if ((threadIdx.x & 31) == 0) wcnt[threadIdx.x >> 5] = __popc(bal);
-  if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
   int pre = 0;
   for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) pre += wcnt[w];
-  const int local = pre + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
-  if (d) list[local] = threadIdx.x;
-  if (threadIdx.x == 0) cnt = wcnt[0] + wcnt[1] + wcnt[2] + wcnt[3];
-  __syncthreads();
-  const int n_here = cnt;
-  const int base_rank = block_off[blockIdx.x];
-  for (int q = 0; q < n_here; ++q) {
-    const int64_t env = (int64_t)blockIdx.x * 128 + list[q];
-    const int64_t r = base_rank + q;             // local done rank
+  if (d) list[block_off[blockIdx.x] + pre + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = (int32_t)i;
+}
+
+// auto-reset: one CTA per done env (persistent grid over the done list):
+// EpisodeStats, then install_worlds from pool entry rank % M
+template <bool EXT>
+__global__ void __launch_bounds__(128) k_install_pool(DS S, InstallArgs a) {
+  constexpr int F = EXT ? 9 : 1, HW = EXT ? 48 * 48 : 64 * 64, A = EXT ? 67 : 22;
+  const int k = a.info->k_local;
+  for (int r = blockIdx.x; r < k; r += gridDim.x) {
+    const int64_t env = a.done_list[r];
     const int64_t p = r % a.M;                   // pool entry
     if (threadIdx.x == 0) {
       atomicAdd(a.st_episodes, 1ull);
       atomicAdd(a.st_steps, (unsigned long long)S.ep_length[env]);
       atomicAdd(a.st_return, S.ep_return[env]);
     }
-    for (int k = threadIdx.x; k < A; k += blockDim.x)
-      if ((GR_AT(S, GR_F_ACH, uint32_t, k >> 5, env) >> (k & 31)) & 1u) atomicAdd(&a.st_ach[k], 1ull);
+    for (int q = threadIdx.x; q < A; q += blockDim.x)
+      if ((GR_AT(S, GR_F_ACH, uint32_t, q >> 5, env) >> (q & 31)) & 1u) atomicAdd(&a.st_ach[q], 1ull);
     __syncthreads();
     install_one<EXT>(S, env, a.pool.meta[p], a.pool.blocks + (size_t)p * F * HW, a.pool.items + (size_t)p * F * HW);
     __syncthreads();
@@ -261,11 +259,19 @@ void launch_install_initial(bool ext, const DS& S, const WBuf& wb, int64_t n, cu
   else k_install_initial<false><<<grid, 128, 0, st>>>(S, wb, n);
 }
 
-void launch_install_pool(bool ext, const DS& S, const InstallArgs& a, const int32_t* block_off, cudaStream_t st) {
-  const int grid = (int)((a.n + 127) / 128);
+void launch_compact(const uint8_t* done, int64_t n, const int32_t* block_off, int32_t* list, cudaStream_t st) {
+  const int grid = (int)((n + 127) / 128);
+  if (grid > 0) k_compact<<<grid, 128, 0, st>>>(done, n, block_off, list);
+}
+
+void launch_install_pool(bool ext, const DS& S, const InstallArgs& a, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>(a.n, (int64_t)sms * 4);
   if (grid <= 0) return;
-  if (ext) k_install_pool<true><<<grid, 128, 0, st>>>(S, a, block_off);
-  else k_install_pool<false><<<grid, 128, 0, st>>>(S, a, block_off);
+  if (ext) k_install_pool<true><<<grid, 128, 0, st>>>(S, a);
+  else k_install_pool<false><<<grid, 128, 0, st>>>(S, a);
 }
 
 }  // namespace gr
