@@ -156,6 +156,10 @@ struct gr_env {
   bool overlap = true;    // GR_OVERLAP=0: reset work serialised after the step on one stream
   bool tma = true;        // GR_TMA=0: plain 16-byte stores for the observation rows
   int obs_ctas_overlap = 2;   // writer CTAs/SM while the reset work runs beside it
+  int obs_ctas_solo = 0;      // writer CTAs/SM otherwise (0: launcher default)
+  int wg_ctas = 0;            // worldgen CTAs/SM (0: launcher default)
+  bool obs_first = false;     // enqueue the big obs launch before the reset work
+  int side_prio = 0;          // side stream priority (0 default, >0 lowest)
   std::vector<void*> allocs;
 };
 
@@ -251,6 +255,10 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (const char* ov = getenv("GR_OVERLAP")) e->overlap = atoi(ov) != 0;
   if (const char* tm = getenv("GR_TMA")) e->tma = atoi(tm) != 0;
   if (const char* oc = getenv("GR_OBS_CTAS")) e->obs_ctas_overlap = atoi(oc);
+  if (const char* oc = getenv("GR_OBS_CTAS0")) e->obs_ctas_solo = atoi(oc);
+  if (const char* wc = getenv("GR_WG_CTAS")) e->wg_ctas = atoi(wc);
+  if (const char* of = getenv("GR_OBS_FIRST")) e->obs_first = atoi(of) != 0;
+  if (const char* sp = getenv("GR_SIDE_PRIO")) e->side_prio = atoi(sp);
   e->ext = cfg->tier == GR_TIER_EXTENDED;
   e->d = e->ext ? EXT_DIMS : CLASSIC_DIMS;
   e->n = cfg->n_envs;
@@ -287,7 +295,9 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->st_ach, 67 * sizeof(unsigned long long));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->st_return, sizeof(double));
   if (rc == GR_OK) {
-    if (cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking) != cudaSuccess ||
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);   // lo: least urgent
+    if (cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, e->side_prio > 0 ? lo : 0) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess)
       rc = fail(GR_E_CUDA, "stream/event creation failed");
@@ -331,7 +341,7 @@ static int observe(gr_env* e, void* obs_dev, cudaStream_t st, bool recompute_fla
     k_dark<<<(unsigned)e->nb, 128, 0, st>>>(e->S, e->n, e->cur_flags);
   }
   ObsArgs oa{obs_dev, e->n, recompute_flags ? e->cur_flags : e->prev_flags, e->cfg.tile_px, e->last_done, sel,
-             e->tma ? 1 : 0, sel == 1 ? e->obs_ctas_overlap : 0, e->done_list, e->info};
+             e->tma ? 1 : 0, sel == 1 ? e->obs_ctas_overlap : e->obs_ctas_solo, e->done_list, e->info};
   {
     PTimer t(e, sel == 2 ? PK_OBS_RESET : PK_OBS, st);
     if (e->cfg.obs_mode == GR_OBS_SYMBOLIC) launch_symbolic(e->ext, e->S, oa, st);
@@ -456,6 +466,10 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
   if (split) {
     CK(cudaEventRecord(e->ev_fork, st));
     CK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+    if (e->obs_first) {   // the non-reset obs reaches the block scheduler first
+      const int rc = observe(e, obs_dev, st, false, 1);
+      if (rc) return rc;
+    }
   }
   {
     PTimer t(e, PK_SCAN, rs);
@@ -467,6 +481,7 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
   j.M = e->M;
   j.out = e->pool;
   j.counters = e->counters;
+  j.ctas_per_sm = e->wg_ctas;
   {
     PTimer t(e, PK_WORLDGEN, rs);
     launch_worldgen(e->ext, j, rs);
@@ -491,8 +506,10 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
   if (!split) return observe(e, obs_dev, st, false);
   int rc = observe(e, obs_dev, rs, false, 2);   // reset envs, after their install
   if (rc) return rc;
-  rc = observe(e, obs_dev, st, false, 1);       // everyone else, concurrently
-  if (rc) return rc;
+  if (!e->obs_first) {
+    rc = observe(e, obs_dev, st, false, 1);     // everyone else, concurrently
+    if (rc) return rc;
+  }
   CK(cudaEventRecord(e->ev_join, e->side));
   CK(cudaStreamWaitEvent(st, e->ev_join, 0));
   return GR_OK;

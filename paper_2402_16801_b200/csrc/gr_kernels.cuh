@@ -42,6 +42,7 @@ struct WorldJob {
   int64_t M;              // pool size (mode 1)
   WBuf out;
   unsigned long long* counters;  // [5] diagnostics
+  int ctas_per_sm;               // resident CTAs per SM (0 = default)
 };
 
 struct InstallArgs {

@@ -202,75 +202,6 @@ __device__ void build_view(const DS& S, int64_t i, bool glow, ViewSmem<EXT>& v) 
   __syncwarp();
 }
 
-template <bool EXT>
-__device__ __forceinline__ float sym_value(const ViewSmem<EXT>& v, int p) {
-  using O = OT<EXT>;
-  if (p < O::T * O::STRIDE) {
-    const int t = p / O::STRIDE, ch = p - t * O::STRIDE;
-    const float l = v.light[t];
-    if (ch == O::STRIDE - 1) return l;
-    const bool lit = l >= 0.05f;
-    const int bch = EXT ? v.blk[t] : C_CLASSIC_LOCAL[v.blk[t]];
-    const bool on = ch == bch || (EXT && ch == O::BCH + v.itm[t]) || ch == O::BCH + O::ICH + v.cre[t];
-    return lit && on ? 1.0f : 0.0f;
-  }
-  const int k = p - O::T * O::STRIDE;
-  return k < O::NINV ? v.inv[k] : 0.0f;
-}
-
-// zero one obs row with 16-byte stores (head/tail peeled: classic rows are
-// only 4-byte aligned)
-__device__ __forceinline__ void zero_row(float* row, int L, int lane) {
-  const uintptr_t addr = reinterpret_cast<uintptr_t>(row);
-  const int head = (int)(((16u - (unsigned)(addr & 15u)) & 15u) >> 2);
-  if (lane < head && lane < L) row[lane] = 0.0f;
-  const int nv = (L - head) >> 2;
-  float4* r4 = reinterpret_cast<float4*>(row + head);
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int q = lane; q < nv; q += 32) r4[q] = z;
-  const int t0 = head + nv * 4;
-  if (t0 + lane < L) row[t0 + lane] = 0.0f;
-}
-
-// the non-zero entries of encode_symbolic_batch (obs.py:364-385)
-template <bool EXT>
-__device__ __forceinline__ void scatter_row(const ViewSmem<EXT>& v, float* row, int lane) {
-  using O = OT<EXT>;
-  for (int t = lane; t < O::T; t += 32) {
-    float* tv = row + t * O::STRIDE;
-    const float l = v.light[t];
-    if (l >= 0.05f) {
-      tv[EXT ? v.blk[t] : C_CLASSIC_LOCAL[v.blk[t]]] = 1.0f;
-      if (EXT) tv[O::BCH + v.itm[t]] = 1.0f;
-      tv[O::BCH + O::ICH + v.cre[t]] = 1.0f;
-    }
-    tv[O::STRIDE - 1] = l;
-  }
-  for (int k = lane; k < O::NINV; k += 32) row[O::T * O::STRIDE + k] = v.inv[k];
-}
-
-template <bool EXT>
-__global__ void __launch_bounds__(OBS_WARPS * 32) k_symbolic(DS S, ObsArgs a) {
-  using O = OT<EXT>;
-  __shared__ ViewSmem<EXT> views[OBS_WARPS];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  ViewSmem<EXT>& v = views[warp];
-  const bool glow = EXT && a.flags && (a.flags[0] & 4u);
-  for (int64_t i = (int64_t)blockIdx.x * OBS_WARPS + warp; i < a.n; i += (int64_t)gridDim.x * OBS_WARPS) {
-    if (a.sel && (a.done[i] != 0) != (a.sel == 2)) continue;   // warp-uniform env filter
-    float* row = (float*)a.out + (size_t)i * O::L;
-    // 1) the row is ~95% zeros: stream zeros with 16-byte stores first
-    //    (fire-and-forget; they overlap the view loads below)
-    zero_row(row, O::L, lane);
-    // 2) egocentric view + inventory into shared memory
-    build_view<EXT>(S, i, glow, v);
-    __syncwarp();   // orders the zero stores before the scatter (same lines)
-    // 3) scatter the <= 4 non-zeros per tile and the inventory section
-    scatter_row<EXT>(v, row, lane);
-    __syncwarp();
-  }
-}
-
 // ----------------------------------------------------------------- pixels
 __constant__ uint8_t C_PALETTE[37][3] = {
     {0, 0, 0}, {10, 10, 10}, {64, 160, 66}, {48, 92, 190}, {120, 120, 120}, {28, 100, 38}, {134, 97, 55},
@@ -408,147 +339,60 @@ __global__ void __launch_bounds__(128) k_pixels(DS S, ObsArgs a) {
   }
 }
 
-// ---------------------------------------------------- descriptor writer
-// One warp per env: the 256-byte descriptor + the view window of the maps
-// become, per tile, three one-hot channel targets (pre-masked by the light
-// threshold) and the light scalar in shared memory; the row is then
-// produced as 16-byte vectors, each value computed in registers and every
-// byte of the row written exactly once with full-line stores.
+// ---------------------------------------------------- symbolic writer
+// One warp per env.  The 256-byte descriptor (k_step / install write it)
+// plus the egocentric window of the block / item maps become, per tile, the
+// <= 3 one-hot channel targets (pre-masked by the light threshold) and the
+// light scalar.  The row is ~95% zeros: each warp keeps one zero-initialised
+// copy of a row in shared memory, scatters the non-zeros into it, streams it
+// out (one TMA bulk store for extended rows, 16-byte stores otherwise) and
+// scatters the zeros back -- O(non-zeros) shared-memory work per env and
+// every global byte written exactly once.
+//
+// The loop is software-pipelined: the descriptor of the next env is loaded
+// while the current one is built, and the next env's map window is loaded
+// while the current row drains, so the two dependent global loads per env
+// (descriptor -> window) overlap the store instead of serialising with it.
 template <bool EXT>
 struct TileSmem {
   uint32_t tgt[OT<EXT>::T];   // on-channels: 3 x 8 bits (0xFF = none)
   float light[OT<EXT>::T];
-  float inv[OT<EXT>::NINV];
   uint32_t desc[DESC_WORDS];
 };
 
 template <bool EXT>
-__device__ __forceinline__ float desc_value(const TileSmem<EXT>& v, int p) {
-  using O = OT<EXT>;
-  if (p < O::T * O::STRIDE) {
-    const int t = p / O::STRIDE, o = p - t * O::STRIDE;
-    const uint32_t g = v.tgt[t];
-    if (o == O::STRIDE - 1) return v.light[t];
-    return (o == (int)(g & 0xFF) || o == (int)((g >> 8) & 0xFF) || o == (int)(g >> 16)) ? 1.0f : 0.0f;
-  }
-  const int k = p - O::T * O::STRIDE;
-  return k < O::NINV ? v.inv[k] : 0.0f;
-}
-
-template <bool EXT>
-__global__ void __launch_bounds__(OBS_WARPS * 32) k_symbolic_desc(DS S, ObsArgs a) {
-  using O = OT<EXT>;
-  __shared__ TileSmem<EXT> views[OBS_WARPS];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  TileSmem<EXT>& v = views[warp];
-  const bool glow = EXT && a.flags && (a.flags[0] & 4u);
-  for (int64_t i = (int64_t)blockIdx.x * OBS_WARPS + warp; i < a.n; i += (int64_t)gridDim.x * OBS_WARPS) {
-    if (a.sel && (a.done[i] != 0) != (a.sel == 2)) continue;   // warp-uniform env filter
-    // descriptor: 256 contiguous bytes, 8 per lane
-    const uint2 dw = reinterpret_cast<const uint2*>(S.desc + (size_t)i * DESC_WORDS)[lane];
-    v.desc[2 * lane] = dw.x;
-    v.desc[2 * lane + 1] = dw.y;
-    __syncwarp();
-    const uint32_t pos = v.desc[D_POS], fl = v.desc[D_FLAGS];
-    const int pr = (int16_t)(pos & 0xFFFF), pc = (int16_t)(pos >> 16), pf = fl & 0xFF;
-    const bool sleeping = (fl >> 8) & 1;
-    const float base = __uint_as_float(v.desc[D_BASE]);
-    const uint8_t* blk = (const uint8_t*)S.f[GR_F_BLOCKS] + ((size_t)i * O::F + pf) * O::HW;
-    const uint8_t* itm = (const uint8_t*)S.f[GR_F_ITEMS] + ((size_t)i * O::F + pf) * O::HW;
-    const int r0 = pr - O::VR / 2, c0 = pc - O::VC / 2;
-    uint8_t bq[(O::T + 31) / 32], iq[(O::T + 31) / 32];
-#pragma unroll
-    for (int q = 0; q < (O::T + 31) / 32; ++q) {
-      const int t = lane + 32 * q;
-      const int r = r0 + t / O::VC, c = c0 + t % O::VC;
-      const bool inb = t < O::T && r >= 0 && r < O::H && c >= 0 && c < O::W;
-      bq[q] = inb ? blk[r * O::W + c] : B_OOB;
-      iq[q] = inb && EXT ? itm[r * O::W + c] : 0;
-    }
-#pragma unroll
-    for (int q = 0; q < (O::T + 31) / 32; ++q) {
-      const int t = lane + 32 * q;
-      if (t < O::T) v.light[t] = base;
-    }
-    for (int k = lane; k < O::NINV; k += 32) v.inv[k] = __uint_as_float(v.desc[D_INV + k]);
-    __syncwarp();
-    if (glow && ((fl >> 9) & 1u)) {   // only floors this env ever put a torch on
-      constexpr int WR = O::VR + 6, WC = O::VC + 6;
-      for (int t = lane; t < WR * WC; t += 32) {
-        const int wr = t / WC - 3, wc = t % WC - 3;
-        const int r = r0 + wr, c = c0 + wc;
-        if (r < 0 || r >= O::H || c < 0 || c >= O::W || itm[r * O::W + c] != I_TORCH) continue;
-        for (int aa = max(wr - 3, 0); aa <= min(wr + 3, O::VR - 1); ++aa)
-          for (int bb = max(wc - 3, 0); bb <= min(wc + 3, O::VC - 1); ++bb) {
-            const int d = max(abs(aa - wr), abs(bb - wc));
-            atomicMax(reinterpret_cast<int*>(&v.light[aa * O::VC + bb]), __float_as_int(1.0f - 0.25f * (float)d));
-          }
-      }
-      __syncwarp();
-    }
-    // creature cells: slot lane < 14; the highest slot wins a cell
-    constexpr int NSLOT = EXT ? 14 : 11;
-    uint32_t sl = 0xFFFFu;
-    if (lane < NSLOT) sl = (v.desc[D_CRE + (lane >> 1)] >> (16 * (lane & 1))) & 0xFFFFu;
-    int cell = sl == 0xFFFFu ? -1 : (int)(sl >> 8);
-    bool win = cell >= 0;
-    for (int s = 1; s < NSLOT; ++s) {
-      const int oc = __shfl_down_sync(0xffffffffu, cell, s);
-      if (lane + s < NSLOT && oc == cell) win = false;
-    }
-    // per-tile channel targets, masked by the light threshold
-#pragma unroll
-    for (int q = 0; q < (O::T + 31) / 32; ++q) {
-      const int t = lane + 32 * q;
-      if (t < O::T) {
-        if (sleeping) v.light[t] = 0.0f;
-        const bool lit = v.light[t] >= 0.05f;
-        const uint32_t bc = EXT ? bq[q] : (uint32_t)C_CLASSIC_LOCAL[bq[q]];
-        const uint32_t ic = EXT ? (uint32_t)(O::BCH + iq[q]) : 0xFFu;
-        v.tgt[t] = lit ? (bc | ic << 8 | (uint32_t)(O::BCH + O::ICH) << 16) : 0xFFFFFFu;
-      }
-    }
-    __syncwarp();
-    if (win && (v.tgt[cell] >> 16) != 0xFFu)
-      v.tgt[cell] = (v.tgt[cell] & 0xFFFFu) | ((uint32_t)(O::BCH + O::ICH + (sl & 0xFF)) << 16);
-    __syncwarp();
-    // stream the row out
-    float* row = (float*)a.out + (size_t)i * O::L;
-    const uintptr_t addr = reinterpret_cast<uintptr_t>(row);
-    const int head = (int)(((16u - (unsigned)(addr & 15u)) & 15u) >> 2);
-    if (lane < head) row[lane] = desc_value<EXT>(v, lane);
-    const int nv = (O::L - head) >> 2;
-    float4* r4 = reinterpret_cast<float4*>(row + head);
-    for (int q = lane; q < nv; q += 32) {
-      const int p = head + 4 * q;
-      r4[q] = make_float4(desc_value<EXT>(v, p), desc_value<EXT>(v, p + 1), desc_value<EXT>(v, p + 2),
-                          desc_value<EXT>(v, p + 3));
-    }
-    const int t0 = head + nv * 4;
-    if (t0 + lane < O::L) row[t0 + lane] = desc_value<EXT>(v, t0 + lane);
-    __syncwarp();
-  }
-}
-
-// ---------------------------------------------- shared-memory row staging
-// The row is ~95% zeros.  Each warp keeps one zero-initialised copy of a row
-// in shared memory, scatters the <= 4 non-zeros per tile and the inventory
-// into it, copies it out with full-line 16-byte stores, and scatters the
-// zeros back -- O(non-zeros) work per env instead of O(row), and every
-// global byte written exactly once.
-template <bool EXT>
 __host__ __device__ constexpr int stage_warps() { return EXT ? 2 : 8; }
-// one chunk = one whole row (+ up to 3 floats of alignment shift); smaller
-// chunks (more resident warps) measured slower: 2048-float chunks 0.44 ms
-// vs 0.40 ms per 65,536-env launch
+// one stage = one whole row + up to 3 floats of alignment shift
 template <bool EXT>
 __host__ __device__ constexpr int stage_floats() { return EXT ? 8272 : 1352; }
+
+// the window of env i's current floor: lane t (+32q) holds tile t's block and item
+template <bool EXT>
+__device__ __forceinline__ void load_window(const DS& S, int64_t i, uint32_t pos, uint32_t fl, int lane,
+                                            uint8_t (&bq)[(OT<EXT>::T + 31) / 32],
+                                            uint8_t (&iq)[(OT<EXT>::T + 31) / 32]) {
+  using O = OT<EXT>;
+  const int pr = (int16_t)(pos & 0xFFFF), pc = (int16_t)(pos >> 16), pf = fl & 0xFF;
+  const uint8_t* blk = (const uint8_t*)S.f[GR_F_BLOCKS] + ((size_t)i * O::F + pf) * O::HW;
+  const uint8_t* itm = (const uint8_t*)S.f[GR_F_ITEMS] + ((size_t)i * O::F + pf) * O::HW;
+  const int r0 = pr - O::VR / 2, c0 = pc - O::VC / 2;
+#pragma unroll
+  for (int q = 0; q < (O::T + 31) / 32; ++q) {
+    const int t = lane + 32 * q;
+    const int r = r0 + t / O::VC, c = c0 + t % O::VC;
+    const bool inb = t < O::T && r >= 0 && r < O::H && c >= 0 && c < O::W;
+    bq[q] = inb ? __ldg(blk + r * O::W + c) : B_OOB;
+    iq[q] = inb && EXT ? __ldg(itm + r * O::W + c) : 0;
+  }
+}
 
 template <bool EXT>
 __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S, ObsArgs a) {
   using O = OT<EXT>;
   constexpr int NW = stage_warps<EXT>();
-  constexpr int SC = stage_floats<EXT>();   // floats per staged chunk
+  constexpr int SC = stage_floats<EXT>();
+  constexpr int TQ = (O::T + 31) / 32;
+  static_assert(SC >= O::L + 3, "a stage holds a whole row");
   extern __shared__ float4 dyn_smem[];
   __shared__ TileSmem<EXT> views[NW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -557,34 +401,57 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
   for (int q = lane; q < SC / 4; q += 32) reinterpret_cast<float4*>(stage)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncwarp();
   const bool glow = EXT && a.flags && (a.flags[0] & 4u);
+  const bool tma = EXT && a.tma;
   const int64_t count = a.sel == 2 ? (int64_t)a.info->k_local : a.n;
-  for (int64_t j = (int64_t)blockIdx.x * NW + warp; j < count; j += (int64_t)gridDim.x * NW) {
-    const int64_t i = a.sel == 2 ? (int64_t)a.list[j] : j;   // sel 2: reset envs only
-    if (a.sel == 1 && a.done[i]) continue;                      // warp-uniform env filter
-    const uint2 dw = reinterpret_cast<const uint2*>(S.desc + (size_t)i * DESC_WORDS)[lane];
-    v.desc[2 * lane] = dw.x;
-    v.desc[2 * lane + 1] = dw.y;
+  const int64_t stride = (int64_t)gridDim.x * NW;
+  // env at list position jj and its descriptor words 2*lane, 2*lane+1; the
+  // done flag (sel 1 skips the envs reset this step) is loaded beside the
+  // descriptor and only checked once the descriptor is needed (settle)
+  auto issue = [&](int64_t jj, int64_t& ii, uint2& dw, int& dn) {
+    ii = a.sel == 2 ? (int64_t)a.list[jj] : jj;
+    dn = a.sel == 1 ? a.done[ii] : 0;
+    dw = reinterpret_cast<const uint2*>(S.desc + (size_t)ii * DESC_WORDS)[lane];
+  };
+  auto settle = [&](int64_t& jj, int64_t& ii, uint2& dw, int& dn) -> bool {
+    while (jj < count && dn) {   // warp-uniform
+      jj += stride;
+      if (jj < count) issue(jj, ii, dw, dn);
+    }
+    return jj < count;
+  };
+  int64_t jn = (int64_t)blockIdx.x * NW + warp, in = 0;
+  uint2 dwn = make_uint2(0, 0);
+  int dn = 0;
+  uint8_t bqn[TQ], iqn[TQ];
+  if (jn < count) issue(jn, in, dwn, dn);
+  bool have = settle(jn, in, dwn, dn);
+  if (have)
+    load_window<EXT>(S, in, __shfl_sync(0xffffffffu, dwn.y, D_POS / 2), __shfl_sync(0xffffffffu, dwn.x, D_FLAGS / 2),
+                     lane, bqn, iqn);
+  while (have) {
+    const int64_t i = in;
+    uint8_t bq[TQ], iq[TQ];
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) { bq[q] = bqn[q]; iq[q] = iqn[q]; }
+    v.desc[2 * lane] = dwn.x;
+    v.desc[2 * lane + 1] = dwn.y;
+    // the descriptor of the next env is in flight while this one is built
+    jn += stride;
+    if (jn < count) issue(jn, in, dwn, dn);
     __syncwarp();
     const uint32_t pos = v.desc[D_POS], fl = v.desc[D_FLAGS];
     const int pr = (int16_t)(pos & 0xFFFF), pc = (int16_t)(pos >> 16), pf = fl & 0xFF;
     const bool sleeping = (fl >> 8) & 1;
     const float base = __uint_as_float(v.desc[D_BASE]);
-    const uint8_t* blk = (const uint8_t*)S.f[GR_F_BLOCKS] + ((size_t)i * O::F + pf) * O::HW;
-    const uint8_t* itm = (const uint8_t*)S.f[GR_F_ITEMS] + ((size_t)i * O::F + pf) * O::HW;
     const int r0 = pr - O::VR / 2, c0 = pc - O::VC / 2;
-    constexpr int TQ = (O::T + 31) / 32;
-    uint8_t bq[TQ], iq[TQ];
 #pragma unroll
     for (int q = 0; q < TQ; ++q) {
       const int t = lane + 32 * q;
-      const int r = r0 + t / O::VC, c = c0 + t % O::VC;
-      const bool inb = t < O::T && r >= 0 && r < O::H && c >= 0 && c < O::W;
-      bq[q] = inb ? blk[r * O::W + c] : B_OOB;
-      iq[q] = inb && EXT ? itm[r * O::W + c] : 0;
       if (t < O::T) v.light[t] = base;
     }
     __syncwarp();
     if (glow && ((fl >> 9) & 1u)) {   // only floors this env ever put a torch on
+      const uint8_t* itm = (const uint8_t*)S.f[GR_F_ITEMS] + ((size_t)i * O::F + pf) * O::HW;
       constexpr int WR = O::VR + 6, WC = O::VC + 6;
       for (int t = lane; t < WR * WC; t += 32) {
         const int wr = t / WC - 3, wc = t % WC - 3;
@@ -598,6 +465,7 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
       }
       __syncwarp();
     }
+    // creature cells: slot lane < NSLOT; the highest slot wins a cell
     constexpr int NSLOT = EXT ? 14 : 11;
     uint32_t sl = 0xFFFFu;
     if (lane < NSLOT) sl = (v.desc[D_CRE + (lane >> 1)] >> (16 * (lane & 1))) & 0xFFFFu;
@@ -622,128 +490,71 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
     if (win && (v.tgt[cell] >> 16) != 0xFFu)
       v.tgt[cell] = (v.tgt[cell] & 0xFFFFu) | ((uint32_t)(O::BCH + O::ICH + (sl & 0xFF)) << 16);
     __syncwarp();
-    // The row is produced in chunks of SC floats through the zero-invariant
-    // stage.  Element p of the row sits at q = p + shift (shift aligns the
-    // 16-byte groups of q with those of the destination address).
+    // element p of the row sits at stage[p + shift]: shift aligns the
+    // 16-byte groups of the stage with those of the destination
     float* row = (float*)a.out + (size_t)i * O::L;
     const int shift = (int)((reinterpret_cast<uintptr_t>(row) & 15u) >> 2);
-    if (SC >= O::L + 3) {   // the whole row fits: straight-line scatter / copy / unscatter
-      float* sr = stage + shift;
-      for (int t = lane; t < O::T; t += 32) {
-        const uint32_t g = v.tgt[t];
-        float* tv = sr + t * O::STRIDE;
-        if ((g & 0xFF) != 0xFF) {
-          tv[g & 0xFF] = 1.0f;
-          if (EXT) tv[(g >> 8) & 0xFF] = 1.0f;
-          tv[g >> 16] = 1.0f;
-        }
-        tv[O::STRIDE - 1] = v.light[t];
+    float* sr = stage + shift;
+    for (int t = lane; t < O::T; t += 32) {
+      const uint32_t g = v.tgt[t];
+      float* tv = sr + t * O::STRIDE;
+      if ((g & 0xFF) != 0xFF) {
+        tv[g & 0xFF] = 1.0f;
+        if (EXT) tv[(g >> 8) & 0xFF] = 1.0f;
+        tv[g >> 16] = 1.0f;
       }
-      for (int k = lane; k < O::NINV; k += 32) sr[O::T * O::STRIDE + k] = __uint_as_float(v.desc[D_INV + k]);
-      if (EXT && a.tma) {
-        // extended rows are 33,072 B = 16-byte multiple at 16-byte aligned
-        // addresses: one TMA bulk store (cp.async.bulk) per row, issued by
-        // one lane; the warp only waits until the stage has been read
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(sr);
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                       :: "l"(row), "r"(saddr), "r"((uint32_t)(O::L * 4)) : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        }
-        __syncwarp();
-      } else {
-        __syncwarp();
-        const int head = (4 - shift) & 3;
-        if (lane < head) row[lane] = sr[lane];
-        const int nv = (O::L - head) >> 2;
-        const float4* s4 = reinterpret_cast<const float4*>(sr + head);
-        float4* g4 = reinterpret_cast<float4*>(row + head);
-        for (int q = lane; q < nv; q += 32) g4[q] = s4[q];
-        const int tl = head + nv * 4;
-        if (tl + lane < O::L) row[tl + lane] = sr[tl + lane];
-        __syncwarp();
-      }
-      for (int t = lane; t < O::T; t += 32) {
-        const uint32_t g = v.tgt[t];
-        float* tv = sr + t * O::STRIDE;
-        if ((g & 0xFF) != 0xFF) {
-          tv[g & 0xFF] = 0.0f;
-          if (EXT) tv[(g >> 8) & 0xFF] = 0.0f;
-          tv[g >> 16] = 0.0f;
-        }
-        tv[O::STRIDE - 1] = 0.0f;
-      }
-      for (int k = lane; k < O::NINV; k += 32) sr[O::T * O::STRIDE + k] = 0.0f;
-      __syncwarp();
-      continue;
+      tv[O::STRIDE - 1] = v.light[t];
     }
-    for (int qc = 0; qc < O::L + shift; qc += SC) {
-      // scatter the non-zeros that fall into this chunk
-      for (int t = lane; t < O::T; t += 32) {
-        const uint32_t g = v.tgt[t];
-        const int tb = t * O::STRIDE + shift - qc;
-        if ((unsigned)(tb + O::STRIDE) <= (unsigned)(SC + O::STRIDE)) {   // tile overlaps the chunk
-          if ((g & 0xFF) != 0xFF) {
-            const int q0 = tb + (int)(g & 0xFF), q2 = tb + (int)(g >> 16);
-            if ((unsigned)q0 < (unsigned)SC) stage[q0] = 1.0f;
-            if (EXT) {
-              const int q1 = tb + (int)((g >> 8) & 0xFF);
-              if ((unsigned)q1 < (unsigned)SC) stage[q1] = 1.0f;
-            }
-            if ((unsigned)q2 < (unsigned)SC) stage[q2] = 1.0f;
-          }
-          const int ql = tb + O::STRIDE - 1;
-          if ((unsigned)ql < (unsigned)SC) stage[ql] = v.light[t];
-        }
-      }
-      for (int k = lane; k < O::NINV; k += 32) {
-        const int q = O::T * O::STRIDE + k + shift - qc;
-        if ((unsigned)q < (unsigned)SC) stage[q] = __uint_as_float(v.desc[D_INV + k]);
-      }
+    for (int k = lane; k < O::NINV; k += 32) sr[O::T * O::STRIDE + k] = __uint_as_float(v.desc[D_INV + k]);
+    have = settle(jn, in, dwn, dn);
+    if (tma) {
+      // extended rows are 33,072 B = a 16-byte multiple at 16-byte aligned
+      // addresses: one TMA bulk store (cp.async.bulk) per row, issued by one
+      // lane; the warp waits only until the stage has been read
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      // copy out: 16-byte groups fully inside the row, element-wise edges
-      const float4* s4 = reinterpret_cast<const float4*>(stage);
-      for (int gi = lane; gi < SC / 4; gi += 32) {
-        const int q = qc + 4 * gi, p = q - shift;
-        if (p >= O::L) break;
-        if (p >= 0 && p + 4 <= O::L) {
-          *reinterpret_cast<float4*>(row + p) = s4[gi];
-        } else {
-          for (int j = 0; j < 4; ++j)
-            if (p + j >= 0 && p + j < O::L) row[p + j] = stage[4 * gi + j];
-        }
+      if (lane == 0) {
+        const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(sr);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     :: "l"(row), "r"(saddr), "r"((uint32_t)(O::L * 4)) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
+      // the next env's window loads overlap the drain of this row
+      if (have)
+        load_window<EXT>(S, in, __shfl_sync(0xffffffffu, dwn.y, D_POS / 2),
+                         __shfl_sync(0xffffffffu, dwn.x, D_FLAGS / 2), lane, bqn, iqn);
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncwarp();
-      // scatter the zeros back
-      for (int t = lane; t < O::T; t += 32) {
-        const uint32_t g = v.tgt[t];
-        const int tb = t * O::STRIDE + shift - qc;
-        if ((unsigned)(tb + O::STRIDE) <= (unsigned)(SC + O::STRIDE)) {
-          if ((g & 0xFF) != 0xFF) {
-            const int q0 = tb + (int)(g & 0xFF), q2 = tb + (int)(g >> 16);
-            if ((unsigned)q0 < (unsigned)SC) stage[q0] = 0.0f;
-            if (EXT) {
-              const int q1 = tb + (int)((g >> 8) & 0xFF);
-              if ((unsigned)q1 < (unsigned)SC) stage[q1] = 0.0f;
-            }
-            if ((unsigned)q2 < (unsigned)SC) stage[q2] = 0.0f;
-          }
-          const int ql = tb + O::STRIDE - 1;
-          if ((unsigned)ql < (unsigned)SC) stage[ql] = 0.0f;
-        }
-      }
-      for (int k = lane; k < O::NINV; k += 32) {
-        const int q = O::T * O::STRIDE + k + shift - qc;
-        if ((unsigned)q < (unsigned)SC) stage[q] = 0.0f;
-      }
+    } else {
+      if (have)
+        load_window<EXT>(S, in, __shfl_sync(0xffffffffu, dwn.y, D_POS / 2),
+                         __shfl_sync(0xffffffffu, dwn.x, D_FLAGS / 2), lane, bqn, iqn);
+      __syncwarp();
+      const int head = (4 - shift) & 3;
+      if (lane < head) row[lane] = sr[lane];
+      const int nv = (O::L - head) >> 2;
+      const float4* s4 = reinterpret_cast<const float4*>(sr + head);
+      float4* g4 = reinterpret_cast<float4*>(row + head);
+      for (int q = lane; q < nv; q += 32) g4[q] = s4[q];
+      const int tl = head + nv * 4;
+      if (tl + lane < O::L) row[tl + lane] = sr[tl + lane];
       __syncwarp();
     }
+    for (int t = lane; t < O::T; t += 32) {
+      const uint32_t g = v.tgt[t];
+      float* tv = sr + t * O::STRIDE;
+      if ((g & 0xFF) != 0xFF) {
+        tv[g & 0xFF] = 0.0f;
+        if (EXT) tv[(g >> 8) & 0xFF] = 0.0f;
+        tv[g >> 16] = 0.0f;
+      }
+      tv[O::STRIDE - 1] = 0.0f;
+    }
+    for (int k = lane; k < O::NINV; k += 32) sr[O::T * O::STRIDE + k] = 0.0f;
+    __syncwarp();
   }
   // bulk stores must complete before the CTA retires
-  if (EXT && a.tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {

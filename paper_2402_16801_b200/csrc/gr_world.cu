@@ -58,8 +58,11 @@ struct WSmem {
 };
 
 // ------------------------------------------------------- block reductions
+// The reductions, the per-floor generators and the other multi-call-site
+// helpers are __noinline__: fully inlined, k_worldgen<true> was 361 KB of
+// SASS and 42% of its warp stalls were no_instructions (icache misses).
 template <class SM>
-__device__ int block_argmax_f(SM& sm, float v, int idx) {   // idx = INT_MAX: no candidate
+__device__ __noinline__ int block_argmax_f(SM& sm, float v, int idx) {   // idx = INT_MAX: no candidate
   for (int o = 16; o > 0; o >>= 1) {
     float ov = __shfl_down_sync(0xffffffffu, v, o);
     int oi = __shfl_down_sync(0xffffffffu, idx, o);
@@ -85,7 +88,7 @@ __device__ int block_argmax_f(SM& sm, float v, int idx) {   // idx = INT_MAX: no
 }
 
 template <class SM>
-__device__ int block_argmax_d(SM& sm, double v, int idx) {
+__device__ __noinline__ int block_argmax_d(SM& sm, double v, int idx) {
   for (int o = 16; o > 0; o >>= 1) {
     double ov = __shfl_down_sync(0xffffffffu, v, o);
     int oi = __shfl_down_sync(0xffffffffu, idx, o);
@@ -111,7 +114,7 @@ __device__ int block_argmax_d(SM& sm, double v, int idx) {
 }
 
 template <class SM>
-__device__ unsigned long long block_min_u64(SM& sm, unsigned long long v) {
+__device__ __noinline__ unsigned long long block_min_u64(SM& sm, unsigned long long v) {
   for (int o = 16; o > 0; o >>= 1) {
     unsigned long long ov = __shfl_down_sync(0xffffffffu, v, o);
     v = ov < v ? ov : v;
@@ -130,7 +133,7 @@ __device__ unsigned long long block_min_u64(SM& sm, unsigned long long v) {
 }
 
 template <class SM>
-__device__ unsigned long long block_or_u64(SM& sm, unsigned long long v) {
+__device__ __noinline__ unsigned long long block_or_u64(SM& sm, unsigned long long v) {
   for (int o = 16; o > 0; o >>= 1) v |= __shfl_down_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0) sm.ru[threadIdx.x >> 5] = v;
   __syncthreads();
@@ -147,7 +150,7 @@ __device__ unsigned long long block_or_u64(SM& sm, unsigned long long v) {
 
 // exclusive prefix sum over the threads of the CTA (thread order)
 template <class SM>
-__device__ int block_excl_scan(SM& sm, int v, int* total) {
+__device__ __noinline__ int block_excl_scan(SM& sm, int v, int* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int x = v;
   for (int o = 1; o < 32; o <<= 1) {
@@ -172,7 +175,7 @@ __device__ int block_excl_scan(SM& sm, int v, int* total) {
 }
 
 template <bool EXT>
-__device__ unsigned long long census(WSmem<EXT>& sm) {
+__device__ __noinline__ unsigned long long census(WSmem<EXT>& sm) {
   unsigned long long m = 0;
   for (int t = threadIdx.x; t < WT<EXT>::HW; t += WG_THREADS) m |= 1ull << sm.blk[t];
   return block_or_u64(sm, m);
@@ -306,7 +309,7 @@ __device__ bool ensure_f32(WSmem<EXT>& sm, uint8_t block, S hfun, bool low, int 
 // first walkable tile of minimal Chebyshev distance to the centre
 // (worldgen.py:267-269, and _nearest_walkable :134-143)
 template <bool EXT>
-__device__ int nearest_walkable(WSmem<EXT>& sm) {
+__device__ __noinline__ int nearest_walkable(WSmem<EXT>& sm) {
   using T = WT<EXT>;
   unsigned long long best = ~0ull;
   for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
@@ -321,7 +324,7 @@ __device__ int nearest_walkable(WSmem<EXT>& sm) {
 // worldgen._gen_overworld (:247-327) on gradients already in sm.gx/gy.
 // Returns false for _Degenerate.  Spawn -> sm.spawn, ladder -> *ld.
 template <bool EXT>
-__device__ bool gen_overworld(WSmem<EXT>& sm, uint64_t seed0, bool extended, int attempt, int* ld) {
+__device__ __noinline__ bool gen_overworld(WSmem<EXT>& sm, uint64_t seed0, bool extended, int attempt, int* ld) {
   using T = WT<EXT>;
   const UField u(hash2(seed0, (uint64_t)attempt), 1);
   for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
@@ -340,6 +343,7 @@ __device__ bool gen_overworld(WSmem<EXT>& sm, uint64_t seed0, bool extended, int
   auto height = [&](int t) { return height_at<EXT>(sm, t); };
   bool fixed_any = false;
   const uint8_t order[6] = {B_COAL, B_IRON, B_DIAMOND, B_LAVA, B_WATER, B_SAND};
+#pragma unroll 1
   for (int k = 0; k < 6; ++k) {
     if (!((cen >> order[k]) & 1ull)) {
       if (!ensure_f32<EXT>(sm, order[k], height, k >= 4, spawn)) return false;
@@ -389,7 +393,7 @@ struct FloorOut { int spawn, ld, lu; };
 
 // worldgen._gen_realm (:479-520)
 template <bool EXT>
-__device__ bool gen_realm(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo) {
+__device__ __noinline__ bool gen_realm(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo) {
   using T = WT<EXT>;
   const Stream s = Stream::raw(seed).split(3000 + (uint64_t)attempt);
   for (int k = threadIdx.x; k < 252; k += WG_THREADS) sm.ang[k] = angle_of(s.at((uint64_t)k));
@@ -447,7 +451,7 @@ __device__ void carve(WSmem<EXT>& sm, int r, int c, int tr, int tc) {
 
 // worldgen._gen_dungeon (:367-406)
 template <bool EXT>
-__device__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo) {
+__device__ __noinline__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo) {
   using T = WT<EXT>;
   // The randint chain draws hash2(key, counter) with counter 0 for the room
   // count and 1 + 4k .. 4 + 4k for room k, so the rooms are independent:
@@ -572,7 +576,7 @@ __device__ __forceinline__ double cave_field_at(const WSmem<EXT>& sm, int t) {
 
 // worldgen._gen_cave (:418-468)
 template <bool EXT>
-__device__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo, bool* fragile) {
+__device__ __noinline__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo, bool* fragile) {
   using T = WT<EXT>;
   const Stream s = Stream::raw(seed).split(2000 + (uint64_t)attempt);
   for (int k = threadIdx.x; k < 106; k += WG_THREADS) {
@@ -661,7 +665,7 @@ __device__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, 
 
 // worldgen._gen_graveyard (:523-546)
 template <bool EXT>
-__device__ void gen_graveyard(WSmem<EXT>& sm, FloorOut* fo) {
+__device__ __noinline__ void gen_graveyard(WSmem<EXT>& sm, FloorOut* fo) {
   using T = WT<EXT>;
   const int cr = T::H / 2, cc = T::W / 2;
   for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
@@ -691,7 +695,7 @@ __device__ void gen_graveyard(WSmem<EXT>& sm, FloorOut* fo) {
 
 // worldgen._template_floor (:549-575)
 template <bool EXT>
-__device__ void gen_template(WSmem<EXT>& sm, int floor, FloorOut* fo) {
+__device__ __noinline__ void gen_template(WSmem<EXT>& sm, int floor, FloorOut* fo) {
   using T = WT<EXT>;
   const int H = T::H, W = T::W, cr = H / 2, cc = W / 2;
   for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
@@ -724,7 +728,7 @@ __device__ void gen_template(WSmem<EXT>& sm, int floor, FloorOut* fo) {
 
 // worldgen._assign_chests for one floor (:598-623)
 template <bool EXT>
-__device__ void assign_chests(WSmem<EXT>& sm, uint64_t world_seed, int f, WMeta* meta) {
+__device__ __noinline__ void assign_chests(WSmem<EXT>& sm, uint64_t world_seed, int f, WMeta* meta) {
   using T = WT<EXT>;
   const int per_floor[9] = {0, 4, 2, 3, 3, 2, 2, 2, 0};
   const int nc = per_floor[f];
@@ -893,7 +897,7 @@ void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int64_t max_items = (j.mode == 0 ? j.count : j.out.cap) * (ext ? 9 : 1);
-  int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * 8);
+  int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * (j.ctas_per_sm > 0 ? j.ctas_per_sm : 8));
   if (grid <= 0) return;
   if (ext) k_worldgen<true><<<grid, WG_THREADS, 0, st>>>(j);
   else k_worldgen<false><<<grid, WG_THREADS, 0, st>>>(j);
