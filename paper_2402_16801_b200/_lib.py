@@ -66,12 +66,18 @@ def lib() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB):
+    # GR_LIB_VARIANT=name loads lib/ab/name.so instead (A/B timing of two
+    # builds in one process tree on one box; still the in-tree CUDA library)
+    path = LIB
+    variant = os.environ.get("GR_LIB_VARIANT")
+    if variant:
+        path = os.path.join(os.path.dirname(LIB), "ab", variant + ".so")
+    if not os.path.exists(path):
         raise ImportError(
-            f"{LIB} is missing: the CUDA extension has not been built "
+            f"{path} is missing: the CUDA extension has not been built "
             "(run `python -m paper_2402_16801_b200._build` or __graft_entry__.build()); "
             "there is no CPU fallback")
-    L = ctypes.CDLL(LIB)
+    L = ctypes.CDLL(path)
     P, I32, I64, U64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
     sig = {
         "gr_create": (I32, [ctypes.POINTER(GrConfig), ctypes.POINTER(P)]),

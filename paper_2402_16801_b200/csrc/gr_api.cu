@@ -5,13 +5,14 @@
 // One step (BatchEnv.step, bindings/.../__init__.py:63-84) on the handle's
 // stream:
 //   k_step        game logic for every env, rewards/done/info, per-block
-//                 done counts, batch-wide flags             (gr_step.cu)
-//   k_scan        exclusive scan of done counts -> local done ranks
-//   [all-gather of the 4 x int32 exchange record -- multi-GPU only]
-//   k_finish_info global rank offset, OR of flags, pool size for this step
+//                 done counts, batch-wide flags; its last CTA scans the
+//                 done counts -> local done ranks + exchange record, and
+//                 for one shard combines StepInfo       (gr_step.cu)
+//   [all-gather of the 4 x int32 exchange record + k_finish_info -- multi-GPU only]
+//   k_compact     done list (side stream from here on, beside the obs)
 //   k_worldgen    fresh worlds for the pool slots this shard consumes
 //   k_install_pool  EpisodeStats + install_worlds for done envs
-//   k_symbolic / k_pixels  post-reset observation
+//   k_symbolic_stage / k_pixels  post-reset observation
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -27,8 +28,6 @@
 #include "gr_kernels.cuh"
 
 namespace gr {
-void launch_scan(const int32_t* block_done, int32_t* block_off, int nb, const uint32_t* cur_flags, int32_t* exchange,
-                 cudaStream_t st);
 void launch_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t step_key, StepInfo* info,
                         uint32_t* flags_out, cudaStream_t st);
 void launch_install_initial(bool ext, const DS& S, const WBuf& wb, int64_t n, cudaStream_t st);
@@ -128,7 +127,8 @@ struct gr_env {
   WBuf pool;
   WMeta* init_meta = nullptr;
   int32_t *block_done = nullptr, *block_off = nullptr, *exchange = nullptr;
-  int32_t* done_list = nullptr;                 // this step's done envs, local rank order
+  int32_t* done_list = nullptr;     // this step's done envs, local rank order
+  unsigned int* arrive = nullptr;   // k_step CTA arrival counter
   uint32_t *cur_flags = nullptr, *prev_flags = nullptr;
   StepInfo* info = nullptr;
   unsigned long long* bad = nullptr;
@@ -285,6 +285,7 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->block_off, e->nb * sizeof(int32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->done_list, e->n * sizeof(int32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->exchange, 4 * sizeof(int32_t));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->arrive, sizeof(unsigned int));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->cur_flags, sizeof(uint32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->prev_flags, sizeof(uint32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->info, sizeof(StepInfo));
@@ -398,8 +399,11 @@ int gr_random_actions(gr_env* e, uint32_t seed, uint64_t t, int64_t* actions_dev
   return GR_OK;
 }
 
-int gr_step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, uint8_t* done_dev, uint8_t* newly_dev,
-                  uint32_t* time_dev, uint8_t* floor_dev, int32_t* exchange_dev, void* stream) {
+// the env update; its last CTA also runs the done-count scan and, for a
+// one-shard step (fuse_info), the StepInfo combine
+static int step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, uint8_t* done_dev,
+                      uint8_t* newly_dev, uint32_t* time_dev, uint8_t* floor_dev, int32_t* exchange_dev, void* stream,
+                      bool fuse_info) {
   if (!e) return fail(GR_E_INVALID, "null env");
   if (!e->have_reset) return fail(GR_E_STATE, "call reset() before step()");
   if (!actions_dev || !reward_dev || !done_dev) return fail(GR_E_INVALID, "actions/reward/done are required");
@@ -435,27 +439,39 @@ int gr_step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, uint
   a.cur_flags = e->cur_flags;
   a.block_done = e->block_done;
   a.bad = nullptr;
+  a.arrive = e->arrive;
+  a.block_off = e->block_off;
+  a.nb = (int)e->nb;
+  a.exchange = exchange_dev ? exchange_dev : e->exchange;
+  if (fuse_info) {
+    // WorldPool(pool_key, step_index + 1, M) (batch.py:217)
+    a.info = e->info;
+    a.step_key = hash2(e->pool_key, (uint64_t)(e->step_index + 1));
+    a.M = e->M;
+    a.flags_out = e->prev_flags;
+  }
   e->last_done = done_dev;
   {
     PTimer t(e, PK_STEP, st);
     launch_step(e->ext, e->S, a, st);
   }
-  {
-    PTimer t(e, PK_SCAN, st);
-    launch_scan(e->block_done, e->block_off, (int)e->nb, e->cur_flags, exchange_dev ? exchange_dev : e->exchange, st);
-  }
   CK(cudaGetLastError());
   return GR_OK;
 }
 
-int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int32_t world, void* obs_dev,
-                   void* stream) {
+int gr_step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, uint8_t* done_dev, uint8_t* newly_dev,
+                  uint32_t* time_dev, uint8_t* floor_dev, int32_t* exchange_dev, void* stream) {
+  return step_local(e, actions_dev, reward_dev, done_dev, newly_dev, time_dev, floor_dev, exchange_dev, stream, false);
+}
+
+static int step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int32_t world, void* obs_dev,
+                       void* stream, bool info_done) {
   if (!e) return fail(GR_E_INVALID, "null env");
   if (world < 1 || rank < 0 || rank >= world) return fail(GR_E_INVALID, "bad rank %d / world %d", rank, world);
   cudaStream_t st = (cudaStream_t)stream;
-  // WorldPool(pool_key, step_index + 1, M) (batch.py:217)
-  const uint64_t step_key = hash2(e->pool_key, (uint64_t)(e->step_index + 1));
-  {
+  if (!info_done) {
+    // WorldPool(pool_key, step_index + 1, M) (batch.py:217)
+    const uint64_t step_key = hash2(e->pool_key, (uint64_t)(e->step_index + 1));
     PTimer t(e, PK_INFO, st);
     launch_finish_info(exchange_all_dev ? exchange_all_dev : e->exchange, rank, world, e->M, step_key, e->info,
                        e->prev_flags, st);
@@ -515,11 +531,16 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
   return GR_OK;
 }
 
+int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int32_t world, void* obs_dev,
+                   void* stream) {
+  return step_finish(e, exchange_all_dev, rank, world, obs_dev, stream, false);
+}
+
 int gr_step(gr_env* e, const int64_t* actions_dev, void* obs_dev, float* reward_dev, uint8_t* done_dev,
             uint8_t* newly_dev, uint32_t* time_dev, uint8_t* floor_dev, void* stream) {
-  int rc = gr_step_local(e, actions_dev, reward_dev, done_dev, newly_dev, time_dev, floor_dev, nullptr, stream);
+  int rc = step_local(e, actions_dev, reward_dev, done_dev, newly_dev, time_dev, floor_dev, nullptr, stream, true);
   if (rc) return rc;
-  return gr_step_finish(e, nullptr, 0, 1, obs_dev, stream);
+  return step_finish(e, nullptr, 0, 1, obs_dev, stream, true);
 }
 
 static int ensure_host_scratch(gr_env* e) {

@@ -6,6 +6,7 @@
 
 namespace gr {
 
+struct StepInfo;
 struct StepArgs {
   const int64_t* actions;   // int64[n]
   float* reward;            // float32[n]
@@ -20,6 +21,17 @@ struct StepArgs {
   uint32_t* cur_flags;         // this step: bit0 melee alive, bit1 ranged alive, bit2 dark floor
   int32_t* block_done;         // done count per 128-env block
   const int64_t* bad;          // >=0: validation failed, do nothing
+  // step tail run by the last CTA to finish (arrive != null): done-count
+  // scan -> block_off, exchange record; with info != null (one shard) also
+  // the StepInfo combine of k_finish_info
+  unsigned int* arrive;        // CTA arrival counter, 0 between steps
+  int32_t* block_off;
+  int nb;
+  int32_t* exchange;
+  StepInfo* info;
+  uint64_t step_key;
+  int64_t M;
+  uint32_t* flags_out;
 };
 
 // step bookkeeping shared by the post-step kernels (device memory)

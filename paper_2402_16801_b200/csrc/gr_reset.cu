@@ -13,65 +13,14 @@
 #include "gr_state.cuh"
 #include "gr_kernels.cuh"
 #include "gr_desc.cuh"
+#include "gr_tail.cuh"
 
 namespace gr {
-
-// exclusive scan of per-block done counts (one CTA), + exchange record
-__global__ void __launch_bounds__(1024) k_scan(const int32_t* block_done, int32_t* block_off, int nb,
-                                                const uint32_t* cur_flags, int32_t* exchange) {
-  __shared__ int32_t warp_tot[32];
-  __shared__ int32_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < nb; base += 1024) {
-    const int i = base + threadIdx.x;
-    const int v = i < nb ? block_done[i] : 0;
-    int x = v;
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, x, o);
-      if ((threadIdx.x & 31) >= o) x += y;
-    }
-    if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = x;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      int w = warp_tot[threadIdx.x];
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, w, o);
-        if (threadIdx.x >= o) w += y;
-      }
-      warp_tot[threadIdx.x] = w;
-    }
-    __syncthreads();
-    const int wpre = (threadIdx.x >> 5) ? warp_tot[(threadIdx.x >> 5) - 1] : 0;
-    if (i < nb) block_off[i] = carry + wpre + x - v;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += warp_tot[31];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    exchange[0] = carry;
-    exchange[1] = (int32_t)cur_flags[0];
-    exchange[2] = 0;
-    exchange[3] = 0;
-  }
-}
 
 // combine the all-gathered exchange records of every rank
 __global__ void k_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t step_key,
                               StepInfo* info, uint32_t* flags_out) {
-  int off = 0;
-  uint32_t fl = 0;
-  for (int r = 0; r < world; ++r) {
-    if (r < rank) off += ex_all[4 * r];
-    fl |= (uint32_t)ex_all[4 * r + 1];
-  }
-  const int k = ex_all[4 * rank];
-  info->k_local = k;
-  info->offset = off;
-  info->n_pool = (int32_t)(k < M ? k : M);
-  info->flags = fl;
-  info->step_key = step_key;
-  *flags_out = fl;
+  combine_info(ex_all, rank, world, M, step_key, info, flags_out);
 }
 
 // install_worlds for one env (state.py:198-249); all threads of the CTA
@@ -240,11 +189,6 @@ __global__ void __launch_bounds__(128) k_install_pool(DS S, InstallArgs a) {
     install_one<EXT>(S, env, a.pool.meta[p], a.pool.blocks + (size_t)p * F * HW, a.pool.items + (size_t)p * F * HW);
     __syncthreads();
   }
-}
-
-void launch_scan(const int32_t* block_done, int32_t* block_off, int nb, const uint32_t* cur_flags, int32_t* exchange,
-                 cudaStream_t st) {
-  k_scan<<<1, 1024, 0, st>>>(block_done, block_off, nb, cur_flags, exchange);
 }
 
 void launch_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t step_key, StepInfo* info,

@@ -31,6 +31,7 @@
 #include "gr_state.cuh"
 #include "gr_kernels.cuh"
 #include "gr_desc.cuh"
+#include "gr_tail.cuh"
 
 namespace gr {
 
@@ -1294,10 +1295,30 @@ __global__ void __launch_bounds__(128, 4) k_step(DS S, StepArgs a) {
   const int fl_mel = __syncthreads_or(my_flags & 1u);
   const int fl_ran = __syncthreads_or(my_flags & 2u);
   const int fl_dark = __syncthreads_or(my_flags & 4u);
+  __shared__ int last;
   if (threadIdx.x == 0) {
     if (a.block_done) a.block_done[blockIdx.x] = cnt;
     uint32_t f = (fl_mel ? 1u : 0u) | (fl_ran ? 2u : 0u) | (fl_dark ? 4u : 0u);
     if (f) atomicOr(a.cur_flags, f);
+    last = 0;
+    if (a.arrive) {
+      __threadfence();   // this CTA's count and flags before its arrival
+      last = atomicAdd(a.arrive, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!last) return;
+  // the last CTA: every other CTA's block_done / cur_flags are visible
+  __threadfence();
+  const int32_t total = cta_scan_blocks(a.block_done, a.block_off, a.nb);
+  if (threadIdx.x == 0) {
+    const uint32_t fl = *(volatile const uint32_t*)a.cur_flags;
+    a.exchange[0] = total;
+    a.exchange[1] = (int32_t)fl;
+    a.exchange[2] = 0;
+    a.exchange[3] = 0;
+    if (a.info) combine_info(a.exchange, 0, 1, a.M, a.step_key, a.info, a.flags_out);
+    *a.arrive = 0u;
   }
 }
 
