@@ -109,16 +109,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_baseline(tier: str, obs: str, n_envs: int, budget_s: float = 15.0) -> dict:
+def cpu_baseline(tier: str, obs: str, n_envs: int, budget_s: float = 15.0, tile_px=None,
+                 max_episode_length=None) -> dict:
     """The oracle port on the host cores, bounded sample (BatchEnv semantics)."""
     import numpy as np
     import oracle as O
     threads = os.cpu_count() or 1
     t0 = time.time()
-    b = O.OracleBatch(tier, n_envs, SEED, threads=threads)
+    b = O.OracleBatch(tier, n_envs, SEED, threads=threads, max_episode_length=max_episode_length or 0)
     init_s = time.time() - t0
     na = O.TIERS[tier]["NA"]
-    px = 7 if tier == "classic" else 10
+    px = tile_px or (7 if tier == "classic" else 10)
     steps = 0
     t0 = time.time()
     while True:
@@ -141,7 +142,7 @@ def run_reference(args, world: int, rank: int):
     if rank != 0:
         return
     budget = float(os.environ.get("GR_REF_BUDGET_S", "60"))
-    cb = cpu_baseline(args.tier, args.obs, args.envs, budget)
+    cb = cpu_baseline(args.tier, args.obs, args.envs, budget, args.tile_px, args.max_episode_length)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
             "steps": None, "warmup": 0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (procedural worlds, seed 0)",
@@ -153,9 +154,16 @@ def run_reference(args, world: int, rank: int):
 
 def workload_config(args, world):
     name = {"extended": "Craftax", "classic": "Craftax-Classic"}[args.tier]
+    extra = ""
+    if args.obs == "pixels":
+        extra += f", tile_px {args.tile_px or (7 if args.tier == 'classic' else 10)}"
+    if args.max_episode_length:
+        extra += f", max_episode_length {args.max_episode_length}"
     return {"workload": f"{name}-{args.obs.capitalize()} random-action rollout with auto-reset "
-                        f"({args.envs} envs per GPU, reset_ratio 16, symbolic obs post-reset)",
+                        f"({args.envs} envs per GPU, reset_ratio 16{extra}, {args.obs} obs post-reset)",
             "tier": args.tier, "obs": args.obs, "n_envs_per_gpu": args.envs,
+            "tile_px": args.tile_px if args.obs == "pixels" else None,
+            "max_episode_length": args.max_episode_length,
             "global_envs": args.envs * world, "seed": SEED,
             "l2_policy": "no flush: per-step state+obs (>4.9 GB/GPU) exceed the 126 MB L2",
             "parallelism": f"dp{world} (contiguous env shards, NCCL all-gather of a 16 B record/step)"}
@@ -170,6 +178,9 @@ def main():
     ap.add_argument("--envs", type=int, default=65536, help="envs per GPU")
     ap.add_argument("--tier", default="extended", choices=["extended", "classic"])
     ap.add_argument("--obs", default="symbolic", choices=["symbolic", "pixels", "none"])
+    ap.add_argument("--tile-px", type=int, default=None, help="pixels: tile size (default 7 classic, 10 extended)")
+    ap.add_argument("--max-episode-length", type=int, default=None,
+                    help="BatchConfig.max_episode_length (reset stress: 16 or 32, SURVEY.md 8(d) config 4)")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -196,10 +207,12 @@ def main():
     from paper_2402_16801_b200.policies import RandomPolicy
 
     if world > 1:
-        env = ShardedBatch(args.envs * world, args.tier, SEED, args.obs)
+        env = ShardedBatch(args.envs * world, args.tier, SEED, args.obs, max_episode_length=args.max_episode_length,
+                           tile_px=args.tile_px)
         gb = env.batch
     else:
-        env = gb = GridrogueBatch(args.envs, args.tier, SEED, args.obs, newly=False, info=False)
+        env = gb = GridrogueBatch(args.envs, args.tier, SEED, args.obs, max_episode_length=args.max_episode_length,
+                                  tile_px=args.tile_px, newly=False, info=False)
     gb.set_validate(False)   # actions come from the device policy: valid by construction
     stream = torch.cuda.current_stream()
 
@@ -282,7 +295,8 @@ def main():
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_baseline(args.tier, args.obs, args.envs, float(os.environ.get("GR_CPU_BUDGET_S", "15")))
+            cb = cpu_baseline(args.tier, args.obs, args.envs, float(os.environ.get("GR_CPU_BUDGET_S", "15")),
+                              args.tile_px, args.max_episode_length)
         except Exception as ex:   # the oracle is only the reported baseline
             cb = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
 

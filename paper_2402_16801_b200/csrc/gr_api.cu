@@ -129,6 +129,7 @@ struct gr_env {
   int32_t *block_done = nullptr, *block_off = nullptr, *exchange = nullptr;
   int32_t* done_list = nullptr;     // this step's done envs, local rank order
   unsigned int* arrive = nullptr;   // k_step CTA arrival counter
+  uint32_t* pix = nullptr;          // pixels: k_pixprep -> k_pixels scratch
   uint32_t *cur_flags = nullptr, *prev_flags = nullptr;
   StepInfo* info = nullptr;
   unsigned long long* bad = nullptr;
@@ -286,6 +287,8 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->done_list, e->n * sizeof(int32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->exchange, 4 * sizeof(int32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->arrive, sizeof(unsigned int));
+  if (rc == GR_OK && cfg->obs_mode == GR_OBS_PIXELS)
+    rc = dev_alloc(e, (void**)&e->pix, (size_t)e->n * pix_scratch_words(e->ext) * sizeof(uint32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->cur_flags, sizeof(uint32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->prev_flags, sizeof(uint32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->info, sizeof(StepInfo));
@@ -342,11 +345,16 @@ static int observe(gr_env* e, void* obs_dev, cudaStream_t st, bool recompute_fla
     k_dark<<<(unsigned)e->nb, 128, 0, st>>>(e->S, e->n, e->cur_flags);
   }
   ObsArgs oa{obs_dev, e->n, recompute_flags ? e->cur_flags : e->prev_flags, e->cfg.tile_px, e->last_done, sel,
-             e->tma ? 1 : 0, sel == 1 ? e->obs_ctas_overlap : e->obs_ctas_solo, e->done_list, e->info};
+             e->tma ? 1 : 0, sel == 1 ? e->obs_ctas_overlap : e->obs_ctas_solo, e->done_list, e->info,
+             e->pix};
   {
     PTimer t(e, sel == 2 ? PK_OBS_RESET : PK_OBS, st);
-    if (e->cfg.obs_mode == GR_OBS_SYMBOLIC) launch_symbolic(e->ext, e->S, oa, st);
-    else launch_pixels(e->ext, e->S, oa, st);
+    if (e->cfg.obs_mode == GR_OBS_SYMBOLIC) {
+      launch_symbolic(e->ext, e->S, oa, st);
+    } else {
+      launch_pixels(e->ext, e->S, oa, st);   // k_pixprep + k_pixels
+      e->launches++;
+    }
   }
   CK(cudaGetLastError());
   return GR_OK;

@@ -82,7 +82,12 @@ struct ObsArgs {
   int ctas_per_sm;          // resident CTAs per SM of the writer (0 = default)
   const int32_t* list;      // sel 2: the done list (k_compact) ...
   const StepInfo* info;     // ... of info->k_local entries
+  uint32_t* pix;            // pixels: per-env scratch of k_pixprep (pix_words per env)
 };
+
+// words per env of the pixel scratch (k_pixprep -> k_pixels): tile colours,
+// inset colours, bar fills, padded to a 16-byte multiple
+__host__ __device__ constexpr int pix_scratch_words(bool ext) { return ext ? 212 : 140; }
 
 void launch_step(bool ext, const DS& S, const StepArgs& a, cudaStream_t st);
 void launch_make_desc(bool ext, const DS& S, int64_t n, cudaStream_t st);

@@ -27,7 +27,6 @@ struct OT {
   static constexpr int NINV = EXT ? 50 : 18;
 };
 
-constexpr int OBS_WARPS = 4;
 
 template <bool EXT>
 struct ViewSmem {
@@ -202,6 +201,26 @@ __device__ void build_view(const DS& S, int64_t i, bool glow, ViewSmem<EXT>& v) 
   __syncwarp();
 }
 
+// the window of env i's current floor: lane t (+32q) holds tile t's block and item
+template <bool EXT>
+__device__ __forceinline__ void load_window(const DS& S, int64_t i, uint32_t pos, uint32_t fl, int lane,
+                                            uint8_t (&bq)[(OT<EXT>::T + 31) / 32],
+                                            uint8_t (&iq)[(OT<EXT>::T + 31) / 32]) {
+  using O = OT<EXT>;
+  const int pr = (int16_t)(pos & 0xFFFF), pc = (int16_t)(pos >> 16), pf = fl & 0xFF;
+  const uint8_t* blk = (const uint8_t*)S.f[GR_F_BLOCKS] + ((size_t)i * O::F + pf) * O::HW;
+  const uint8_t* itm = (const uint8_t*)S.f[GR_F_ITEMS] + ((size_t)i * O::F + pf) * O::HW;
+  const int r0 = pr - O::VR / 2, c0 = pc - O::VC / 2;
+#pragma unroll
+  for (int q = 0; q < (O::T + 31) / 32; ++q) {
+    const int t = lane + 32 * q;
+    const int r = r0 + t / O::VC, c = c0 + t % O::VC;
+    const bool inb = t < O::T && r >= 0 && r < O::H && c >= 0 && c < O::W;
+    bq[q] = inb ? __ldg(blk + r * O::W + c) : B_OOB;
+    iq[q] = inb && EXT ? __ldg(itm + r * O::W + c) : 0;
+  }
+}
+
 // ----------------------------------------------------------------- pixels
 __constant__ uint8_t C_PALETTE[37][3] = {
     {0, 0, 0}, {10, 10, 10}, {64, 160, 66}, {48, 92, 190}, {120, 120, 120}, {28, 100, 38}, {134, 97, 55},
@@ -239,104 +258,383 @@ struct PixSmem {
   int fill[12];                    // bar fills: 5 strip + 7 side
 };
 
-template <bool EXT>
-__global__ void __launch_bounds__(128) k_pixels(DS S, ObsArgs a) {
+// frame geometry of one tier and tile size (tiles.py:85-133)
+template <bool EXT, int PX>
+struct PG {
   using O = OT<EXT>;
-  __shared__ ViewSmem<EXT> view;
-  __shared__ PixSmem<EXT> pm;
-  const int px = a.tile_px;
-  const int side = EXT ? 2 : 0;
-  const int FH = (O::VR + 2) * px, FW = (O::VC + side) * px;
-  const int inset = max(1, px / 4);
-  const int64_t frame = (int64_t)FH * FW * 3;
-  const int64_t count = a.sel == 2 ? (int64_t)a.info->k_local : a.n;
-  for (int64_t j = blockIdx.x; j < count; j += gridDim.x) {
-    const int64_t i = a.sel == 2 ? (int64_t)a.list[j] : j;   // sel 2: reset envs only
-    if (a.sel == 1 && a.done[i]) continue;                      // CTA-uniform env filter
-    if (threadIdx.x < 32) {
-      // render_tiles sees a one-env batch: glow iff this env's floor is dark
-      const int pf = EXT ? GR_AT(S, GR_F_PFLOOR, uint8_t, 0, i) : 0;
-      build_view<EXT>(S, i, EXT && C_FLOOR_AMB[pf] < 1.0f, view);
+  static constexpr int FH = (O::VR + 2) * PX, FW = (O::VC + (EXT ? 2 : 0)) * PX;
+  static constexpr int RB = FW * 3, FB = FH * RB;                  // bytes per frame row / frame
+  static constexpr int INSET = PX / 4 > 1 ? PX / 4 : 1;
+  static constexpr int NS = EXT ? 5 : 4;
+  static constexpr int BAR_H = (2 * PX) / (NS + 1) > 2 ? (2 * PX) / (NS + 1) : 2;
+  static constexpr int Y0 = O::VR * PX;
+  static constexpr int NCLASS = O::VR * 4 + 6;                     // row classes (see row_class)
+  static constexpr int PS = ((RB + 20) + ((RB + 20) >> 7) * 4 + 15) / 16 * 16;   // padded pattern row stride
+  static constexpr int SMEM = NCLASS * PS;
+};
+
+// Pattern rows are stored with one pad word after every 32 words, so that
+// lanes reading words 16 bytes apart (consecutive 16-byte chunks) hit
+// distinct shared-memory banks: logical byte B of a row sits at pix_off(B).
+__device__ __forceinline__ int pix_off(int B) { return B + ((B >> 7) << 2); }
+
+// The frame rows fall into a few classes that depend on the geometry only:
+// within a tile row, the rows outside / inside the inset squares, with or
+// without the side-panel gear bar; in the bottom strip, each vital bar and
+// the blank rows.  Rows of one class are byte-identical.
+template <bool EXT, int PX>
+__device__ __forceinline__ int row_class(int y) {
+  using G = PG<EXT, PX>;
+  if (y < G::Y0) {
+    const int R = y / PX, iy = y % PX;
+    const bool ins = iy >= G::INSET && iy < PX - G::INSET;
+    const bool bar = EXT && R < 7 && iy >= 1 && iy < PX - 1;
+    return R * 4 + (ins ? 1 : 0) + (bar ? 2 : 0);
+  }
+  const int r = y - G::Y0 - 1;
+  if (r >= 0 && r / G::BAR_H < G::NS && r % G::BAR_H < G::BAR_H - 1) return OT<EXT>::VR * 4 + r / G::BAR_H;
+  return OT<EXT>::VR * 4 + 5;
+}
+
+// the 12 bar fills (f64, rounded half-even like Python round)
+template <bool EXT>
+__device__ __forceinline__ void bar_fills(const DS& S, int64_t i, int px, int* fill) {
+  // vital bars (tiles.py:147-166) and gear panel (:169-186), float64
+  using O = OT<EXT>;
+  const float str_ = (float)GR_AT(S, GR_F_STR, uint8_t, 0, i), dex = (float)GR_AT(S, GR_F_DEX, uint8_t, 0, i);
+  const float intel = (float)GR_AT(S, GR_F_INTEL, uint8_t, 0, i);
+  const double hmax = (double)__fadd_rn(9.0f, str_), fmax = (double)__fadd_rn(12.0f, dex);
+  double st[5] = {(double)GR_AT(S, GR_F_HEALTH, float, 0, i) / hmax, (double)GR_AT(S, GR_F_FOOD, float, 0, i) / fmax,
+                  (double)GR_AT(S, GR_F_DRINK, float, 0, i) / fmax, (double)GR_AT(S, GR_F_ENERGY, float, 0, i) / fmax,
+                  EXT ? (double)GR_AT(S, GR_F_MANA, float, 0, i) / (double)__fadd_rn(16.0f, intel) : 0.0};
+  const int width = O::VC * px - 2;
+  for (int k = 0; k < 5; ++k) {
+    const double f = st[k] < 0.0 ? 0.0 : (st[k] > 1.0 ? 1.0 : st[k]);
+    fill[k] = (int)rint(__dmul_rn(f, (double)width));
+  }
+  if (EXT) {
+    const int arm = GR_AT(S, GR_F_ARMOUR, uint8_t, 0, i) + GR_AT(S, GR_F_ARMOUR, uint8_t, 1, i) +
+                    GR_AT(S, GR_F_ARMOUR, uint8_t, 2, i) + GR_AT(S, GR_F_ARMOUR, uint8_t, 3, i);
+    double gr[7] = {(double)GR_AT(S, GR_F_SWORD_TIER, uint8_t, 0, i) / 4.0,
+                    (double)GR_AT(S, GR_F_PICK_TIER, uint8_t, 0, i) / 4.0, (double)arm / 8.0,
+                    (double)GR_AT(S, GR_F_XP, uint8_t, 0, i) / 8.0, (double)dex / 5.0, (double)str_ / 5.0,
+                    (double)intel / 5.0};
+    for (int k = 0; k < 7; ++k) {
+      const double f = gr[k] < 0.0 ? 0.0 : (gr[k] > 1.0 ? 1.0 : gr[k]);
+      fill[5 + k] = (int)rint(__dmul_rn(f, (double)(2 * px - 2)));
     }
-    __syncthreads();
-    for (int t = threadIdx.x; t < O::T; t += blockDim.x) {
-      const float l = view.light[t];
+  }
+}
+
+// Per-env pixel inputs, written by k_pixprep into global scratch and read
+// by k_pixels with one 16-byte-vector copy: shaded tile colours, inset
+// colours (0xFF000000 = none) and the 12 bar fills.
+template <bool EXT>
+__host__ __device__ constexpr int pix_words() { return pix_scratch_words(EXT); }
+
+// One warp per env: the view (obs.view_window / light_window / creature
+// grid) from the env's 256-byte descriptor (k_step / install write it) and
+// its map window, the shaded tile colours (tiles.py:113-133) and the bar
+// fills.  A separate, massively parallel pass so the frame writer never
+// waits on these dependent state loads.
+template <bool EXT>
+__global__ void __launch_bounds__(128) k_pixprep(DS S, ObsArgs a) {
+  using O = OT<EXT>;
+  constexpr int TQ = (O::T + 31) / 32;
+  __shared__ float light_s[4][O::T];
+  __shared__ uint8_t cre_s[4][O::T];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* light = light_s[warp];
+  uint8_t* cre = cre_s[warp];
+  const int64_t count = a.sel == 2 ? (int64_t)a.info->k_local : a.n;
+  for (int64_t j = (int64_t)blockIdx.x * 4 + warp; j < count; j += (int64_t)gridDim.x * 4) {
+    const int64_t i = a.sel == 2 ? (int64_t)a.list[j] : j;   // sel 2: reset envs only
+    if (a.sel == 1 && a.done[i]) continue;                      // warp-uniform env filter
+    const uint2 dw = reinterpret_cast<const uint2*>(S.desc + (size_t)i * DESC_WORDS)[lane];
+    PixSmem<EXT>* dst = reinterpret_cast<PixSmem<EXT>*>(a.pix + (size_t)i * pix_words<EXT>());
+    if (lane == 0) bar_fills<EXT>(S, i, a.tile_px, dst->fill);   // independent loads, in flight meanwhile
+    const uint32_t pos = __shfl_sync(0xffffffffu, dw.y, D_POS / 2), fl = __shfl_sync(0xffffffffu, dw.x, D_FLAGS / 2);
+    const float base = __uint_as_float(__shfl_sync(0xffffffffu, dw.x, D_BASE / 2));
+    const int pr = (int16_t)(pos & 0xFFFF), pc = (int16_t)(pos >> 16), pf = fl & 0xFF;
+    uint8_t bq[TQ], iq[TQ];
+    load_window<EXT>(S, i, pos, fl, lane, bq, iq);
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) {
+      const int t = lane + 32 * q;
+      if (t < O::T) { light[t] = base; cre[t] = 0; }
+    }
+    __syncwarp();
+    // render_tiles sees a one-env batch: glow iff this env's floor is dark
+    // (and only floors this env ever put a torch on can have one)
+    if (EXT && C_FLOOR_AMB[pf] < 1.0f && ((fl >> 9) & 1u)) {
+      const uint8_t* itm = (const uint8_t*)S.f[GR_F_ITEMS] + ((size_t)i * O::F + pf) * O::HW;
+      constexpr int WR = O::VR + 6, WC = O::VC + 6;
+      const int r0 = pr - O::VR / 2, c0 = pc - O::VC / 2;
+      for (int t = lane; t < WR * WC; t += 32) {
+        const int wr = t / WC - 3, wc = t % WC - 3;
+        const int r = r0 + wr, c = c0 + wc;
+        if (r < 0 || r >= O::H || c < 0 || c >= O::W || itm[r * O::W + c] != I_TORCH) continue;
+        for (int aa = max(wr - 3, 0); aa <= min(wr + 3, O::VR - 1); ++aa)
+          for (int bb = max(wc - 3, 0); bb <= min(wc + 3, O::VC - 1); ++bb) {
+            const int d = max(abs(aa - wr), abs(bb - wc));
+            atomicMax(reinterpret_cast<int*>(&light[aa * O::VC + bb]), __float_as_int(1.0f - 0.25f * (float)d));
+          }
+      }
+      __syncwarp();
+    }
+    // creature cells: slot lane < NSLOT; the highest slot wins a cell
+    constexpr int NSLOT = EXT ? 14 : 11;
+    uint32_t sl = 0xFFFFu;
+    {
+      // gather descriptor word D_CRE + (lane >> 1) into every lane
+      const int wi = D_CRE + ((lane < NSLOT ? lane : 0) >> 1);
+      const uint32_t lo = __shfl_sync(0xffffffffu, dw.x, wi >> 1), hi = __shfl_sync(0xffffffffu, dw.y, wi >> 1);
+      const uint32_t word = (wi & 1) ? hi : lo;
+      if (lane < NSLOT) sl = (word >> (16 * (lane & 1))) & 0xFFFFu;
+    }
+    const int cell = sl == 0xFFFFu ? -1 : (int)(sl >> 8);
+    bool win = cell >= 0;
+    for (int s = 1; s < NSLOT; ++s) {
+      const int oc = __shfl_down_sync(0xffffffffu, cell, s);
+      if (lane + s < NSLOT && oc == cell) win = false;
+    }
+    if (win) cre[cell] = (uint8_t)(sl & 0xFF);
+    const bool sleeping = (fl >> 8) & 1;
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) {
+      const int t = lane + 32 * q;
+      if (t >= O::T) continue;
+      const float l = sleeping ? 0.0f : light[t];
       const float sh = l < 0.0f ? 0.0f : (l > 1.0f ? 1.0f : l);
       const bool dark = l < 0.05f;
-      const int b = view.blk[t];
+      const int b = bq[q];
       uint32_t rgb = 0;
       if (!dark)
         for (int k = 0; k < 3; ++k)
           rgb |= (uint32_t)(uint8_t)(int)__fmul_rn((float)C_PALETTE[b][k], sh) << (16 - 8 * k);
-      pm.tile_rgb[t] = rgb;
+      dst->tile_rgb[t] = rgb;
       uint32_t ins = 0xFF000000u;
       if (!dark) {
-        const int it = view.itm[t];
+        const int it = iq[q];
         if (it) ins = ((uint32_t)C_ITEMC[it][0] << 16) | ((uint32_t)C_ITEMC[it][1] << 8) | C_ITEMC[it][2];
-        if (view.cre[t]) ins = creature_rgb(EXT, view.cre[t]);
+        if (cre[t]) ins = creature_rgb(EXT, cre[t]);
       }
       if (t == (O::VR / 2) * O::VC + O::VC / 2) ins = 0xFA3C3Cu;   // the player
-      pm.inset_rgb[t] = ins;
+      dst->inset_rgb[t] = ins;
     }
-    if (threadIdx.x == 0) {
-      // vital bars (tiles.py:147-166) and gear panel (:169-186), float64
-      const float str_ = (float)GR_AT(S, GR_F_STR, uint8_t, 0, i), dex = (float)GR_AT(S, GR_F_DEX, uint8_t, 0, i);
-      const float intel = (float)GR_AT(S, GR_F_INTEL, uint8_t, 0, i);
-      const double hmax = (double)__fadd_rn(9.0f, str_), fmax = (double)__fadd_rn(12.0f, dex);
-      double st[5] = {(double)GR_AT(S, GR_F_HEALTH, float, 0, i) / hmax, (double)GR_AT(S, GR_F_FOOD, float, 0, i) / fmax,
-                      (double)GR_AT(S, GR_F_DRINK, float, 0, i) / fmax, (double)GR_AT(S, GR_F_ENERGY, float, 0, i) / fmax,
-                      EXT ? (double)GR_AT(S, GR_F_MANA, float, 0, i) / (double)__fadd_rn(16.0f, intel) : 0.0};
-      const int width = O::VC * px - 2;
-      for (int k = 0; k < 5; ++k) {
-        const double f = st[k] < 0.0 ? 0.0 : (st[k] > 1.0 ? 1.0 : st[k]);
-        pm.fill[k] = (int)rint(__dmul_rn(f, (double)width));
-      }
-      if (EXT) {
-        const int arm = GR_AT(S, GR_F_ARMOUR, uint8_t, 0, i) + GR_AT(S, GR_F_ARMOUR, uint8_t, 1, i) +
-                        GR_AT(S, GR_F_ARMOUR, uint8_t, 2, i) + GR_AT(S, GR_F_ARMOUR, uint8_t, 3, i);
-        double g[7] = {(double)GR_AT(S, GR_F_SWORD_TIER, uint8_t, 0, i) / 4.0,
-                       (double)GR_AT(S, GR_F_PICK_TIER, uint8_t, 0, i) / 4.0, (double)arm / 8.0,
-                       (double)GR_AT(S, GR_F_XP, uint8_t, 0, i) / 8.0, (double)dex / 5.0, (double)str_ / 5.0,
-                       (double)intel / 5.0};
-        for (int k = 0; k < 7; ++k) {
-          const double f = g[k] < 0.0 ? 0.0 : (g[k] > 1.0 ? 1.0 : g[k]);
-          pm.fill[5 + k] = (int)rint(__dmul_rn(f, (double)(2 * px - 2)));
-        }
-      }
-    }
-    __syncthreads();
-    uint8_t* out = (uint8_t*)a.out + (size_t)i * frame;
-    const int ns = EXT ? 5 : 4;
-    const int bar_h = max(2, (2 * px) / (ns + 1));
-    const int y0 = O::VR * px;
-    for (int64_t byte = threadIdx.x; byte < frame; byte += blockDim.x) {
-      const int p = (int)(byte / 3), ch = (int)(byte % 3);
-      const int y = p / FW, x = p % FW;
-      uint32_t rgb = 0;
-      if (y < O::VR * px && x < O::VC * px) {
-        const int t = (y / px) * O::VC + x / px, iy = y % px, ix = x % px;
-        rgb = pm.tile_rgb[t];
-        if (iy >= inset && iy < px - inset && ix >= inset && ix < px - inset && pm.inset_rgb[t] != 0xFF000000u)
-          rgb = pm.inset_rgb[t];
-      } else if (y >= y0 && x < O::VC * px) {
-        const int k = (y - y0 - 1) / bar_h, yy = (y - y0 - 1) % bar_h;
-        if (y - y0 - 1 >= 0 && k < ns && yy < bar_h - 1 && x >= 1 && x < 1 + O::VC * px - 2) {
-          rgb = x < 1 + pm.fill[k]
-                    ? ((uint32_t)C_BARC[k][0] << 16) | ((uint32_t)C_BARC[k][1] << 8) | C_BARC[k][2]
-                    : 0x1E1E1Eu;
-        }
-      } else if (EXT && x >= O::VC * px) {
-        const int k = y / px, yy = y % px, xx = x - O::VC * px;
-        if (k < 7 && k * px + px <= FH && yy >= 1 && yy < px - 1 && xx >= 1 && xx < 2 * px - 1) {
-          rgb = xx < 1 + pm.fill[5 + k]
-                    ? ((uint32_t)C_GEARC[k][0] << 16) | ((uint32_t)C_GEARC[k][1] << 8) | C_GEARC[k][2]
-                    : 0x1E1E1Eu;
-        }
-      }
-      out[byte] = (uint8_t)(rgb >> (16 - 8 * ch));
-    }
-    __syncthreads();
+    __syncwarp();
   }
+}
+
+// The frame writer: one CTA per env at a time, software-pipelined over the
+// CTA's envs.
+//  1. one byte row per row class present (<= 31 rows, ~1/4 of the frame):
+//     tile rows per tile segment, side panel and bottom strip per pixel
+//  2. the frame streamed out as 16-byte stores of the globally 16-byte
+//     aligned chunks of the env's byte range (frames are 42,900 / 11,907 B,
+//     not 16-byte multiples), each the funnel shift of 5 words of its class
+//     row (stored with a pad word per 32 so the lanes' loads are free of
+//     bank conflicts); the <= 1 chunk per frame-row boundary that straddles
+//     two rows and the head / tail bytes outside the aligned chunks are a
+//     separate, small pass.  A warp store covers 512 contiguous bytes;
+//     meanwhile the next env's inputs (k_pixprep scratch) arrive in the
+//     other buffer by cp.async.  (4-byte words per lane measured slower:
+//     4x the loop overhead.)
+template <bool EXT, int PX>
+__global__ void __launch_bounds__(128) k_pixels(DS S, ObsArgs a) {
+  using O = OT<EXT>;
+  using G = PG<EXT, PX>;
+  constexpr int PW = pix_words<EXT>();
+  static_assert(sizeof(PixSmem<EXT>) <= PW * 4, "scratch layout");
+  extern __shared__ uint4 pix_dyn[];
+  uint8_t* pat = reinterpret_cast<uint8_t*>(pix_dyn);   // [NCLASS][PS]
+  __shared__ __align__(16) uint32_t pmw[2][PW];
+  __shared__ uint8_t rowcls[G::FH];
+  __shared__ int16_t rep[G::NCLASS];
+  __shared__ uint8_t ucls[G::NCLASS];
+  __shared__ int nused;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // row class of every frame row, one representative row per class and the
+  // list of classes present (geometry only: once per CTA); rows of a class
+  // are identical, so any representative will do
+  for (int c = threadIdx.x; c < G::NCLASS; c += blockDim.x) rep[c] = -1;
+  __syncthreads();
+  for (int y = threadIdx.x; y < G::FH; y += blockDim.x) {
+    const int c = row_class<EXT, PX>(y);
+    rowcls[y] = (uint8_t)c;
+    rep[c] = (int16_t)y;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int u = 0;
+    for (int c = 0; c < G::NCLASS; ++c)
+      if (rep[c] >= 0) ucls[u++] = (uint8_t)c;
+    nused = u;
+  }
+  const int64_t count = a.sel == 2 ? (int64_t)a.info->k_local : a.n;
+  const int64_t stride = gridDim.x;
+  // the CTA's next env at or after list position jj (-1: none)
+  auto next_env = [&](int64_t jj) -> int64_t {
+    for (; jj < count; jj += stride) {
+      const int64_t ii = a.sel == 2 ? (int64_t)a.list[jj] : jj;
+      if (a.sel == 1 && a.done[ii]) continue;   // CTA-uniform env filter
+      return jj;
+    }
+    return -1;
+  };
+  auto env_of = [&](int64_t jj) -> int64_t { return a.sel == 2 ? (int64_t)a.list[jj] : jj; };
+  // env ii's scratch -> pmw[b] (warp 0, asynchronous)
+  auto fetch = [&](int64_t ii, int b) {
+    const char* src = reinterpret_cast<const char*>(a.pix + (size_t)ii * PW);
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&pmw[b][0]);
+    for (int q = lane; q < PW / 4; q += 32)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(src + 16 * q) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int64_t j = next_env(blockIdx.x);
+  if (j >= 0 && warp == 0) {
+    fetch(env_of(j), 0);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  }
+  __syncthreads();
+  int cur = 0;
+  uint8_t* out = (uint8_t*)a.out;
+  while (j >= 0) {
+    const int64_t i = env_of(j);
+    const int64_t jn = next_env(j + stride);
+    const PixSmem<EXT>& pm = *reinterpret_cast<const PixSmem<EXT>*>(&pmw[cur][0]);
+    // 1. class rows
+    {
+      const int nu = nused;
+      constexpr int NTC = O::VR * 4;   // tile-row classes are [0, NTC)
+      // tile segments: (class, tile column) -> PX pixels
+      for (int q = threadIdx.x; q < nu * O::VC; q += blockDim.x) {
+        const int c = ucls[q / O::VC], C = q % O::VC;
+        if (c >= NTC) continue;
+        const int t = (c >> 2) * O::VC + C;
+        const uint32_t tc = pm.tile_rgb[t], ic = pm.inset_rgb[t];
+        const bool ins = (c & 1) && ic != 0xFF000000u;
+        uint8_t* p = pat + c * G::PS;
+        const int B0 = 3 * PX * C;
+#pragma unroll
+        for (int ix = 0; ix < PX; ++ix) {
+          const uint32_t rgb = ins && ix >= G::INSET && ix < PX - G::INSET ? ic : tc;
+          p[pix_off(B0 + 3 * ix)] = (uint8_t)(rgb >> 16);
+          p[pix_off(B0 + 3 * ix + 1)] = (uint8_t)(rgb >> 8);
+          p[pix_off(B0 + 3 * ix + 2)] = (uint8_t)rgb;
+        }
+      }
+      // side panel of the tile-row classes (gear bar k = tile row, per
+      // pixel, byte stores: the panel is not word-aligned) ...
+      constexpr int SW = G::FW - O::VC * PX;   // side panel width (0 classic)
+      for (int q = threadIdx.x; q < nu * SW; q += blockDim.x) {
+        const int c = ucls[q / SW], xx = q % SW;
+        if (c >= NTC) continue;
+        const int k = c >> 2;
+        uint32_t rgb = 0u;
+        if ((c & 2) && xx >= 1 && xx < 2 * PX - 1)   // (c & 2): a gear-bar row (row_class)
+          rgb = xx < 1 + pm.fill[5 + k] ? ((uint32_t)C_GEARC[k][0] << 16) | ((uint32_t)C_GEARC[k][1] << 8) | C_GEARC[k][2]
+                                        : 0x1E1E1Eu;
+        uint8_t* p = pat + c * G::PS;
+        const int B0 = 3 * (O::VC * PX + xx);
+        p[pix_off(B0)] = (uint8_t)(rgb >> 16);
+        p[pix_off(B0 + 1)] = (uint8_t)(rgb >> 8);
+        p[pix_off(B0 + 2)] = (uint8_t)rgb;
+      }
+      // ... and the bottom-strip classes (vital bar k, or blank), 4 pixels
+      // -> 3 words per task
+      constexpr int NG = (G::FW + 3) / 4;
+      for (int q = threadIdx.x; q < 6 * NG; q += blockDim.x) {
+        const int k = q / NG, x0 = 4 * (q - k * NG), c = NTC + k;
+        if (rep[c] < 0) continue;
+        const uint32_t barc = k < G::NS ? ((uint32_t)C_BARC[k][0] << 16) | ((uint32_t)C_BARC[k][1] << 8) | C_BARC[k][2] : 0u;
+        const int fl = k < G::NS ? pm.fill[k] : 0;
+        uint32_t cl[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int x = x0 + m;
+          cl[m] = k < G::NS && x >= 1 && x < 1 + O::VC * PX - 2 ? (x < 1 + fl ? barc : 0x1E1E1Eu) : 0u;
+        }
+        // bytes r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3 (little-endian words)
+        uint8_t* p = pat + c * G::PS;
+        const int B0 = 3 * x0;   // a multiple of 4
+        *reinterpret_cast<uint32_t*>(p + pix_off(B0)) = __byte_perm(cl[0], cl[1], 0x6012);
+        *reinterpret_cast<uint32_t*>(p + pix_off(B0 + 4)) = __byte_perm(cl[1], cl[2], 0x5601);
+        *reinterpret_cast<uint32_t*>(p + pix_off(B0 + 8)) = __byte_perm(cl[2], cl[3], 0x4560);
+      }
+    }
+    __syncthreads();
+    if (warp == 0 && jn >= 0) fetch(env_of(jn), cur ^ 1);   // the next env's inputs, under this env's stores
+    // 2. stream the frame: bytes [f0, f0 + FB) of the output
+    const int64_t f0 = i * (int64_t)G::FB;
+    const int64_t c0 = (f0 + 15) & ~(int64_t)15, c1 = (f0 + G::FB) & ~(int64_t)15;
+    const int nchunk = (int)((c1 - c0) >> 4);
+    auto byte_at = [&](int b) -> uint32_t {
+      const int y = b / G::RB;
+      return pat[rowcls[y] * G::PS + pix_off(b - y * G::RB)];
+    };
+    // straddling chunks (one per frame-row boundary not on a 16-byte
+    // boundary) and the head / tail bytes
+    for (int q = threadIdx.x; q < G::FH - 1 + 32; q += blockDim.x) {
+      if (q < G::FH - 1) {
+        const int64_t bnd = f0 + (int64_t)(q + 1) * G::RB;
+        const int64_t c = bnd & ~(int64_t)15;
+        if (c == bnd || c < c0 || c >= c1) continue;
+        const int b = (int)(c - f0);
+        uint32_t wv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          wv[k] = byte_at(b + 4 * k) | byte_at(b + 4 * k + 1) << 8 | byte_at(b + 4 * k + 2) << 16 |
+                  byte_at(b + 4 * k + 3) << 24;
+        *reinterpret_cast<uint4*>(out + c) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      } else {
+        const int r = q - (G::FH - 1);
+        const int head = (int)(c0 - f0), tail = (int)(f0 + G::FB - c1);
+        if (r < 16) {
+          if (r < head) out[f0 + r] = (uint8_t)byte_at(r);
+        } else if (r - 16 < tail) {
+          out[c1 + r - 16] = (uint8_t)byte_at((int)(c1 - f0) + r - 16);
+        }
+      }
+    }
+    // the aligned chunks inside one frame row: lane-consecutive, so a warp
+    // store covers 512 contiguous bytes; a chunk at row offset o is the
+    // funnel shift of the 5 pattern words from o & ~3 (padded layout: the
+    // lanes' loads hit distinct banks)
+    for (int q = threadIdx.x; q < nchunk; q += blockDim.x) {
+      const int b = (int)(c0 - f0) + 16 * q;
+      const int y = b / G::RB, o = b - y * G::RB;
+      if (o + 16 <= G::RB) {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(pat + rowcls[y] * G::PS);
+        const int L = o >> 2, sh = (o & 3) * 8;
+        uint32_t x[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) x[k] = w[(L + k) + ((L + k) >> 5)];
+        *reinterpret_cast<uint4*>(out + c0 + 16 * (int64_t)q) =
+            make_uint4(__funnelshift_r(x[0], x[1], sh), __funnelshift_r(x[1], x[2], sh), __funnelshift_r(x[2], x[3], sh),
+                       __funnelshift_r(x[3], x[4], sh));
+      }
+    }
+    if (warp == 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    j = jn;
+    cur ^= 1;
+  }
+}
+
+template <bool EXT, int PX>
+static void launch_pixels_px(const DS& S, const ObsArgs& a, int sms, cudaStream_t st) {
+  constexpr int smem = PG<EXT, PX>::SMEM;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_pixels<EXT, PX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pixels<EXT, PX>, 128, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  // persistent grids: every CTA resident from the start
+  k_pixprep<EXT><<<(int)std::min<int64_t>((a.n + 3) / 4, (int64_t)sms * 16), 128, 0, st>>>(S, a);
+  k_pixels<EXT, PX><<<(int)std::min<int64_t>(a.n, (int64_t)sms * per_sm), 128, smem, st>>>(S, a);
 }
 
 // ---------------------------------------------------- symbolic writer
@@ -365,26 +663,6 @@ __host__ __device__ constexpr int stage_warps() { return EXT ? 2 : 8; }
 // one stage = one whole row + up to 3 floats of alignment shift
 template <bool EXT>
 __host__ __device__ constexpr int stage_floats() { return EXT ? 8272 : 1352; }
-
-// the window of env i's current floor: lane t (+32q) holds tile t's block and item
-template <bool EXT>
-__device__ __forceinline__ void load_window(const DS& S, int64_t i, uint32_t pos, uint32_t fl, int lane,
-                                            uint8_t (&bq)[(OT<EXT>::T + 31) / 32],
-                                            uint8_t (&iq)[(OT<EXT>::T + 31) / 32]) {
-  using O = OT<EXT>;
-  const int pr = (int16_t)(pos & 0xFFFF), pc = (int16_t)(pos >> 16), pf = fl & 0xFF;
-  const uint8_t* blk = (const uint8_t*)S.f[GR_F_BLOCKS] + ((size_t)i * O::F + pf) * O::HW;
-  const uint8_t* itm = (const uint8_t*)S.f[GR_F_ITEMS] + ((size_t)i * O::F + pf) * O::HW;
-  const int r0 = pr - O::VR / 2, c0 = pc - O::VC / 2;
-#pragma unroll
-  for (int q = 0; q < (O::T + 31) / 32; ++q) {
-    const int t = lane + 32 * q;
-    const int r = r0 + t / O::VC, c = c0 + t % O::VC;
-    const bool inb = t < O::T && r >= 0 && r < O::H && c >= 0 && c < O::W;
-    bq[q] = inb ? __ldg(blk + r * O::W + c) : B_OOB;
-    iq[q] = inb && EXT ? __ldg(itm + r * O::W + c) : 0;
-  }
-}
 
 template <bool EXT>
 __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S, ObsArgs a) {
@@ -591,9 +869,15 @@ void launch_pixels(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (int)std::min<int64_t>(a.n, (int64_t)sms * 16);
-  if (ext) k_pixels<true><<<grid, 128, 0, st>>>(S, a);
-  else k_pixels<false><<<grid, 128, 0, st>>>(S, a);
+  switch ((ext ? 100 : 0) + a.tile_px) {
+    case 7: launch_pixels_px<false, 7>(S, a, sms, st); break;
+    case 10: launch_pixels_px<false, 10>(S, a, sms, st); break;
+    case 16: launch_pixels_px<false, 16>(S, a, sms, st); break;
+    case 107: launch_pixels_px<true, 7>(S, a, sms, st); break;
+    case 110: launch_pixels_px<true, 10>(S, a, sms, st); break;
+    case 116: launch_pixels_px<true, 16>(S, a, sms, st); break;
+    default: break;   // gr_create admits 7, 10, 16 only
+  }
 }
 
 }  // namespace gr

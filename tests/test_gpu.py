@@ -89,7 +89,8 @@ def test_rollout_parity(torch_cuda, oracle_lib, tier, n, steps, seed, max_len):
 
 
 @pytest.mark.parametrize("tier,n,px,steps", [("classic", 64, 7, 60), ("extended", 64, 10, 60),
-                                             ("classic", 32, 16, 20), ("extended", 16, 16, 20)])
+                                             ("classic", 32, 16, 20), ("extended", 16, 16, 20),
+                                             ("classic", 24, 10, 20), ("extended", 24, 7, 20)])
 def test_pixel_parity(torch_cuda, oracle_lib, tier, n, px, steps):
     from paper_2402_16801_b200 import GridrogueBatch
     O = oracle_lib
