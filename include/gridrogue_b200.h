@@ -161,6 +161,14 @@ int gr_reset_host(gr_env *env, void *obs_host);
  * bookkeeping so the device state equals the imported SimState exactly. */
 int gr_export_field(gr_env *env, int32_t field, void *host_dst);
 int gr_import_field(gr_env *env, int32_t field, const void *host_src);
+/* BatchState bookkeeping outside SimState (batch.py:144-153): the running
+ * episode return (f64[N]) / length (i64[N]) and the step counter that keys
+ * the reset pool (WorldPool(pool_key, step_index + 1)).  Checkpoint/resume
+ * and the rollout report (bench.run_rollout_report, bench.py:67-107). */
+int gr_export_episode(gr_env *env, double *ep_return_host, int64_t *ep_length_host);
+int gr_import_episode(gr_env *env, const double *ep_return_host, const int64_t *ep_length_host);
+int gr_get_step_index(gr_env *env, int64_t *out);
+int gr_set_step_index(gr_env *env, int64_t step_index);
 /* encode the current state (no step): symbolic or pixels per obs_mode */
 int gr_observe(gr_env *env, void *obs_dev, void *stream);
 

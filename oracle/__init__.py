@@ -316,6 +316,13 @@ class OracleBatch:
             raise ValueError(f"invalid action {int(a[bad])} for env {bad}")
         return reward, done, newly, {"time": itime, "floor": ifloor}
 
+    def episode_progress(self) -> tuple:
+        """BatchState.ep_return (f64[N]) and ep_length (i64[N])."""
+        ret = np.zeros(self.n, np.float64)
+        length = np.zeros(self.n, np.int64)
+        lib().go_batch_ep(self.h, _ptr(ret), _ptr(length))
+        return ret, length
+
     def stats(self) -> dict:
         ep = ctypes.c_int64()
         tr = ctypes.c_double()

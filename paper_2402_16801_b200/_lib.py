@@ -103,6 +103,10 @@ def lib() -> ctypes.CDLL:
         "gr_stats_get": (I32, [P, ctypes.POINTER(GrStats)]),
         "gr_level_seeds": (I32, [P, P]),
         "gr_episodes_completed": (I32, [P, ctypes.POINTER(I64)]),
+        "gr_export_episode": (I32, [P, P, P]),
+        "gr_import_episode": (I32, [P, P, P]),
+        "gr_get_step_index": (I32, [P, ctypes.POINTER(I64)]),
+        "gr_set_step_index": (I32, [P, I64]),
         "gr_kernel_launches": (I64, [P]),
         "gr_worldgen_counters": (I32, [P, ctypes.POINTER(I64)]),
         "gr_set_profiling": (I32, [P, I32]),

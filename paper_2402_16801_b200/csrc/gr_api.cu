@@ -18,6 +18,7 @@
 #include <cstring>
 #include <cstdarg>
 #include <cstdlib>
+#include <climits>
 #include <string>
 #include <vector>
 #include <algorithm>
@@ -28,8 +29,8 @@
 #include "gr_kernels.cuh"
 
 namespace gr {
-void launch_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t step_key, StepInfo* info,
-                        uint32_t* flags_out, cudaStream_t st);
+void launch_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t pool_key,
+                        unsigned long long* dstep, StepInfo* info, uint32_t* flags_out, cudaStream_t st);
 void launch_install_initial(bool ext, const DS& S, const WBuf& wb, int64_t n, cudaStream_t st);
 void launch_install_pool(bool ext, const DS& S, const InstallArgs& a, cudaStream_t st);
 void launch_compact(const uint8_t* done, int64_t n, const int32_t* block_off, int32_t* list, cudaStream_t st);
@@ -117,6 +118,12 @@ struct Prof {
   }
 };
 
+struct StepGraph {
+  const void* key[7];   // actions, obs, reward, done, newly, time, floor
+  cudaGraphExec_t exec;
+  int64_t launches;     // kernels per replay
+};
+
 struct gr_env {
   Prof prof;
   gr_config cfg;
@@ -130,6 +137,7 @@ struct gr_env {
   int32_t* done_list = nullptr;     // this step's done envs, local rank order
   unsigned int* arrive = nullptr;   // k_step CTA arrival counter
   uint32_t* pix = nullptr;          // pixels: k_pixprep -> k_pixels scratch
+  unsigned long long* dstep = nullptr;   // device step counter (pool of step s = WorldPool(s + 1))
   uint32_t *cur_flags = nullptr, *prev_flags = nullptr;
   StepInfo* info = nullptr;
   unsigned long long* bad = nullptr;
@@ -159,8 +167,12 @@ struct gr_env {
   int obs_ctas_overlap = 2;   // writer CTAs/SM while the reset work runs beside it
   int obs_ctas_solo = 0;      // writer CTAs/SM otherwise (0: launcher default)
   int wg_ctas = 0;            // worldgen CTAs/SM (0: launcher default)
-  bool obs_first = false;     // enqueue the big obs launch before the reset work
+  bool obs_first = true;      // enqueue the big obs launch before the reset work (GR_OBS_FIRST=0: after);
+                              // inside a step graph the other order starves the writer (0.55 vs 0.49 ms)
   int side_prio = 0;          // side stream priority (0 default, >0 lowest)
+  bool graphs = true;         // GR_GRAPH=0: launch the step kernel by kernel
+  cudaStream_t cap_stream = nullptr;
+  std::vector<StepGraph> step_graphs;
   std::vector<void*> allocs;
 };
 
@@ -226,6 +238,8 @@ void gr_destroy(gr_env* e) {
   for (void* p : e->allocs) cudaFree(p);
   if (e->h_stream) cudaStreamDestroy(e->h_stream);
   if (e->side) cudaStreamDestroy(e->side);
+  for (auto& g : e->step_graphs) cudaGraphExecDestroy(g.exec);
+  if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   if (e->ev_fork) cudaEventDestroy(e->ev_fork);
   if (e->ev_join) cudaEventDestroy(e->ev_join);
   for (auto x : e->prof.pool) cudaEventDestroy(x);
@@ -260,6 +274,7 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (const char* wc = getenv("GR_WG_CTAS")) e->wg_ctas = atoi(wc);
   if (const char* of = getenv("GR_OBS_FIRST")) e->obs_first = atoi(of) != 0;
   if (const char* sp = getenv("GR_SIDE_PRIO")) e->side_prio = atoi(sp);
+  if (const char* gg = getenv("GR_GRAPH")) e->graphs = atoi(gg) != 0;
   e->ext = cfg->tier == GR_TIER_EXTENDED;
   e->d = e->ext ? EXT_DIMS : CLASSIC_DIMS;
   e->n = cfg->n_envs;
@@ -287,6 +302,7 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->done_list, e->n * sizeof(int32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->exchange, 4 * sizeof(int32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->arrive, sizeof(unsigned int));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->dstep, sizeof(unsigned long long));
   if (rc == GR_OK && cfg->obs_mode == GR_OBS_PIXELS)
     rc = dev_alloc(e, (void**)&e->pix, (size_t)e->n * pix_scratch_words(e->ext) * sizeof(uint32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->cur_flags, sizeof(uint32_t));
@@ -387,6 +403,7 @@ int gr_reset(gr_env* e, void* obs_dev, void* stream) {
     launch_install_initial(e->ext, e->S, j.out, e->n, st);
   }
   CK(cudaMemsetAsync(e->prev_flags, 0, sizeof(uint32_t), st));
+  CK(cudaMemsetAsync(e->dstep, 0, sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(e->st_episodes, 0, sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(e->st_steps, 0, sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(e->st_ach, 0, 67 * sizeof(unsigned long long), st));
@@ -407,31 +424,38 @@ int gr_random_actions(gr_env* e, uint32_t seed, uint64_t t, int64_t* actions_dev
   return GR_OK;
 }
 
+// engine.py:715-717: the first invalid action raises before any mutation
+static int validate_actions(gr_env* e, const int64_t* actions_dev, cudaStream_t st) {
+  CK(cudaMemsetAsync(e->bad, 0xFF, sizeof(unsigned long long), st));
+  {
+    PTimer t(e, PK_OTHER, st);
+    k_validate<<<(unsigned)((e->n + 255) / 256), 256, 0, st>>>(actions_dev, e->n, e->d.NA, e->bad);
+  }
+  unsigned long long bad = 0;
+  CK(cudaMemcpyAsync(&bad, e->bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (bad != ~0ull) {
+    int64_t a = 0;
+    CK(cudaMemcpy(&a, actions_dev + bad, sizeof(a), cudaMemcpyDeviceToHost));
+    e->last_bad_env = (int64_t)bad;
+    e->last_bad_action = a;
+    return fail(GR_E_BAD_ACTION, "invalid action %lld for env %lld", (long long)a, (long long)bad);
+  }
+  return GR_OK;
+}
+
 // the env update; its last CTA also runs the done-count scan and, for a
 // one-shard step (fuse_info), the StepInfo combine
 static int step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, uint8_t* done_dev,
                       uint8_t* newly_dev, uint32_t* time_dev, uint8_t* floor_dev, int32_t* exchange_dev, void* stream,
-                      bool fuse_info) {
+                      bool fuse_info, bool validate = true) {
   if (!e) return fail(GR_E_INVALID, "null env");
   if (!e->have_reset) return fail(GR_E_STATE, "call reset() before step()");
   if (!actions_dev || !reward_dev || !done_dev) return fail(GR_E_INVALID, "actions/reward/done are required");
   cudaStream_t st = (cudaStream_t)stream;
-  if (e->validate) {
-    CK(cudaMemsetAsync(e->bad, 0xFF, sizeof(unsigned long long), st));
-    {
-      PTimer t(e, PK_OTHER, st);
-      k_validate<<<(unsigned)((e->n + 255) / 256), 256, 0, st>>>(actions_dev, e->n, e->d.NA, e->bad);
-    }
-    unsigned long long bad = 0;
-    CK(cudaMemcpyAsync(&bad, e->bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (bad != ~0ull) {
-      int64_t a = 0;
-      CK(cudaMemcpy(&a, actions_dev + bad, sizeof(a), cudaMemcpyDeviceToHost));
-      e->last_bad_env = (int64_t)bad;
-      e->last_bad_action = a;
-      return fail(GR_E_BAD_ACTION, "invalid action %lld for env %lld", (long long)a, (long long)bad);
-    }
+  if (e->validate && validate) {
+    const int rc = validate_actions(e, actions_dev, st);
+    if (rc) return rc;
   }
   CK(cudaMemsetAsync(e->cur_flags, 0, sizeof(uint32_t), st));
   StepArgs a{};
@@ -452,9 +476,9 @@ static int step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, 
   a.nb = (int)e->nb;
   a.exchange = exchange_dev ? exchange_dev : e->exchange;
   if (fuse_info) {
-    // WorldPool(pool_key, step_index + 1, M) (batch.py:217)
     a.info = e->info;
-    a.step_key = hash2(e->pool_key, (uint64_t)(e->step_index + 1));
+    a.pool_key = e->pool_key;
+    a.dstep = e->dstep;
     a.M = e->M;
     a.flags_out = e->prev_flags;
   }
@@ -478,11 +502,9 @@ static int step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank,
   if (world < 1 || rank < 0 || rank >= world) return fail(GR_E_INVALID, "bad rank %d / world %d", rank, world);
   cudaStream_t st = (cudaStream_t)stream;
   if (!info_done) {
-    // WorldPool(pool_key, step_index + 1, M) (batch.py:217)
-    const uint64_t step_key = hash2(e->pool_key, (uint64_t)(e->step_index + 1));
     PTimer t(e, PK_INFO, st);
-    launch_finish_info(exchange_all_dev ? exchange_all_dev : e->exchange, rank, world, e->M, step_key, e->info,
-                       e->prev_flags, st);
+    launch_finish_info(exchange_all_dev ? exchange_all_dev : e->exchange, rank, world, e->M, e->pool_key, e->dstep,
+                       e->info, e->prev_flags, st);
   }
   // reset work on the side stream, overlapping the obs of the other envs
   const bool split = e->overlap && obs_dev && e->cfg.obs_mode != GR_OBS_NONE && e->last_done;
@@ -544,11 +566,64 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
   return step_finish(e, exchange_all_dev, rank, world, obs_dev, stream, false);
 }
 
+// One-shard steps replay a CUDA graph of the whole launch sequence (step,
+// scan tail, compaction, worldgen, install, observation writers on two
+// streams), captured once per set of output buffers on the handle's own
+// capture stream and launched into the caller's stream: the per-step
+// inputs that change (the step counter and pool key) live on the device.
 int gr_step(gr_env* e, const int64_t* actions_dev, void* obs_dev, float* reward_dev, uint8_t* done_dev,
             uint8_t* newly_dev, uint32_t* time_dev, uint8_t* floor_dev, void* stream) {
-  int rc = step_local(e, actions_dev, reward_dev, done_dev, newly_dev, time_dev, floor_dev, nullptr, stream, true);
-  if (rc) return rc;
-  return step_finish(e, nullptr, 0, 1, obs_dev, stream, true);
+  if (!e) return fail(GR_E_INVALID, "null env");
+  if (!e->graphs || e->prof.on) {
+    int rc = step_local(e, actions_dev, reward_dev, done_dev, newly_dev, time_dev, floor_dev, nullptr, stream, true);
+    if (rc) return rc;
+    return step_finish(e, nullptr, 0, 1, obs_dev, stream, true);
+  }
+  if (!e->have_reset) return fail(GR_E_STATE, "call reset() before step()");
+  if (!actions_dev || !reward_dev || !done_dev) return fail(GR_E_INVALID, "actions/reward/done are required");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (e->validate) {
+    const int rc = validate_actions(e, actions_dev, st);
+    if (rc) return rc;
+  }
+  const void* key[7] = {actions_dev, obs_dev, reward_dev, done_dev, newly_dev, time_dev, floor_dev};
+  StepGraph* g = nullptr;
+  for (auto& x : e->step_graphs)
+    if (!memcmp(x.key, key, sizeof(key))) g = &x;
+  if (!g) {
+    if (e->step_graphs.size() >= 4) {   // a small cache: buffers rarely change
+      cudaGraphExecDestroy(e->step_graphs.front().exec);
+      e->step_graphs.erase(e->step_graphs.begin());
+    }
+    if (!e->cap_stream) CK(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+    const int64_t l0 = e->launches, s0 = e->step_index;
+    CK(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = step_local(e, actions_dev, reward_dev, done_dev, newly_dev, time_dev, floor_dev, nullptr, e->cap_stream,
+                        true, false);
+    if (!rc) rc = step_finish(e, nullptr, 0, 1, obs_dev, e->cap_stream, true);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (ce != cudaSuccess) return fail(GR_E_CUDA, "step graph capture: %s", cudaGetErrorString(ce));
+    StepGraph ng{};
+    memcpy(ng.key, key, sizeof(key));
+    const cudaError_t ie = cudaGraphInstantiate(&ng.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) return fail(GR_E_CUDA, "step graph instantiate: %s", cudaGetErrorString(ie));
+    ng.launches = e->launches - l0;
+    e->launches = l0;        // nothing ran during the capture
+    e->step_index = s0;
+    e->step_graphs.push_back(ng);
+    g = &e->step_graphs.back();
+  }
+  CK(cudaGraphLaunch(g->exec, st));
+  e->launches += g->launches;
+  e->step_index += 1;
+  e->last_done = done_dev;
+  return GR_OK;
 }
 
 static int ensure_host_scratch(gr_env* e) {
@@ -715,6 +790,52 @@ int gr_stats_get(gr_env* e, gr_stats* out) {
   out->total_steps = (int64_t)steps;
   out->total_return = ret;
   for (int a = 0; a < 67; ++a) out->ach_episodes[a] = (int64_t)ach[a];
+  return GR_OK;
+}
+
+int gr_export_episode(gr_env* e, double* ep_return_host, int64_t* ep_length_host) {
+  if (!e) return fail(GR_E_INVALID, "null env");
+  CK(cudaSetDevice(e->cfg.device));
+  CK(cudaDeviceSynchronize());
+  if (ep_return_host) CK(cudaMemcpy(ep_return_host, e->S.ep_return, e->n * sizeof(double), cudaMemcpyDeviceToHost));
+  if (ep_length_host) {
+    std::vector<int32_t> tmp(e->n);
+    CK(cudaMemcpy(tmp.data(), e->S.ep_length, e->n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < e->n; ++i) ep_length_host[i] = tmp[i];
+  }
+  return GR_OK;
+}
+
+int gr_import_episode(gr_env* e, const double* ep_return_host, const int64_t* ep_length_host) {
+  if (!e) return fail(GR_E_INVALID, "null env");
+  CK(cudaSetDevice(e->cfg.device));
+  CK(cudaDeviceSynchronize());
+  if (ep_return_host) CK(cudaMemcpy(e->S.ep_return, ep_return_host, e->n * sizeof(double), cudaMemcpyHostToDevice));
+  if (ep_length_host) {
+    std::vector<int32_t> tmp(e->n);
+    for (int64_t i = 0; i < e->n; ++i) {
+      if (ep_length_host[i] < 0 || ep_length_host[i] > INT32_MAX)
+        return fail(GR_E_INVALID, "ep_length[%lld] out of range", (long long)i);
+      tmp[i] = (int32_t)ep_length_host[i];
+    }
+    CK(cudaMemcpy(e->S.ep_length, tmp.data(), e->n * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  return GR_OK;
+}
+
+int gr_get_step_index(gr_env* e, int64_t* out) {
+  if (!e || !out) return fail(GR_E_INVALID, "null argument");
+  *out = e->step_index;
+  return GR_OK;
+}
+
+int gr_set_step_index(gr_env* e, int64_t step_index) {
+  if (!e || step_index < 0) return fail(GR_E_INVALID, "bad step index");
+  CK(cudaSetDevice(e->cfg.device));
+  CK(cudaDeviceSynchronize());
+  const unsigned long long v = (unsigned long long)step_index;
+  CK(cudaMemcpy(e->dstep, &v, sizeof(v), cudaMemcpyHostToDevice));
+  e->step_index = step_index;
   return GR_OK;
 }
 

@@ -29,7 +29,8 @@ struct StepArgs {
   int nb;
   int32_t* exchange;
   StepInfo* info;
-  uint64_t step_key;
+  uint64_t pool_key;
+  unsigned long long* dstep;   // device step counter (combine_info)
   int64_t M;
   uint32_t* flags_out;
 };

@@ -18,9 +18,9 @@
 namespace gr {
 
 // combine the all-gathered exchange records of every rank
-__global__ void k_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t step_key,
-                              StepInfo* info, uint32_t* flags_out) {
-  combine_info(ex_all, rank, world, M, step_key, info, flags_out);
+__global__ void k_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t pool_key,
+                              unsigned long long* dstep, StepInfo* info, uint32_t* flags_out) {
+  combine_info(ex_all, rank, world, M, pool_key, dstep, info, flags_out);
 }
 
 // install_worlds for one env (state.py:198-249); all threads of the CTA
@@ -191,9 +191,9 @@ __global__ void __launch_bounds__(128) k_install_pool(DS S, InstallArgs a) {
   }
 }
 
-void launch_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t step_key, StepInfo* info,
-                        uint32_t* flags_out, cudaStream_t st) {
-  k_finish_info<<<1, 1, 0, st>>>(ex_all, rank, world, M, step_key, info, flags_out);
+void launch_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t pool_key,
+                        unsigned long long* dstep, StepInfo* info, uint32_t* flags_out, cudaStream_t st) {
+  k_finish_info<<<1, 1, 0, st>>>(ex_all, rank, world, M, pool_key, dstep, info, flags_out);
 }
 
 void launch_install_initial(bool ext, const DS& S, const WBuf& wb, int64_t n, cudaStream_t st) {

@@ -193,6 +193,35 @@ class GridrogueBatch:
         return {"episodes": s.episodes, "total_return": s.total_return, "total_steps": s.total_steps,
                 "ach_episodes": np.array(s.ach_episodes[:self.n_achievements], np.int64)}
 
+    def episode_progress(self) -> tuple:
+        """BatchState.ep_return (f64[N]) and ep_length (i64[N]) of the running episodes."""
+        self.torch.cuda.synchronize(self.device)
+        ret = np.zeros(self.n, np.float64)
+        length = np.zeros(self.n, np.int64)
+        check(lib().gr_export_episode(self.h, ret.ctypes.data_as(ctypes.c_void_p),
+                                      length.ctypes.data_as(ctypes.c_void_p)))
+        return ret, length
+
+    def set_episode_progress(self, ep_return: np.ndarray, ep_length: np.ndarray) -> None:
+        ret = np.ascontiguousarray(ep_return, np.float64)
+        length = np.ascontiguousarray(ep_length, np.int64)
+        if ret.shape != (self.n,) or length.shape != (self.n,):
+            raise ValueError(f"episode arrays must have shape ({self.n},)")
+        self.torch.cuda.synchronize(self.device)
+        check(lib().gr_import_episode(self.h, ret.ctypes.data_as(ctypes.c_void_p),
+                                      length.ctypes.data_as(ctypes.c_void_p)))
+
+    @property
+    def step_index(self) -> int:
+        v = ctypes.c_int64()
+        check(lib().gr_get_step_index(self.h, ctypes.byref(v)))
+        return v.value
+
+    @step_index.setter
+    def step_index(self, value: int) -> None:
+        self.torch.cuda.synchronize(self.device)
+        check(lib().gr_set_step_index(self.h, int(value)))
+
     def episodes_completed(self) -> int:
         v = ctypes.c_int64()
         check(lib().gr_episodes_completed(self.h, ctypes.byref(v)))

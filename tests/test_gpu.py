@@ -8,6 +8,7 @@ auto-reset pool, reset-stress runs and scrambled states that reach the
 rare branches (enchanting, potions, ladders, boss waves, projectiles).
 """
 
+import json
 import os
 
 import numpy as np
@@ -247,3 +248,55 @@ def test_sharded_batch_world_one(torch_cuda, oracle_lib):
         assert sb.stats()["episodes"] == ob.stats()["episodes"]
     finally:
         dist.destroy_process_group()
+
+
+def _golden_rollouts():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "bench_rollout_report.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_rollout_report_matches_reference(torch_cuda, case):
+    """bench_report.run_rollout_report == the reference's run_rollout_report (bench.py:67-107)."""
+    from paper_2402_16801_b200.bench_report import run_rollout_report
+    g = _golden_rollouts()[case]
+    tier, n, total, seed = g["args"]
+    ref = g["report"]
+    rep = run_rollout_report(tier, n, total, policy="random", seed=seed)
+    for k in ("tier", "policy", "seed", "n_envs", "total_steps", "episodes_completed", "episodes_counted",
+              "max_return", "achievement_rates"):
+        assert rep[k] == ref[k], k
+    # EpisodeStats.total_return is summed in a different order on the device
+    assert rep["mean_return"] == pytest.approx(ref["mean_return"], abs=2e-6)
+    assert rep["return_pct_of_max"] == pytest.approx(ref["return_pct_of_max"], abs=2e-4)
+
+
+def test_speed_sweep_rows(torch_cuda):
+    from paper_2402_16801_b200.bench_report import run_speed_sweep
+    rows = run_speed_sweep("classic", [1, 64], 640)
+    assert [r["workers"] for r in rows] == [1, 64]
+    assert sum(r["best"] for r in rows) == 1
+    assert all(r["sps"] > 0 for r in rows)
+    assert rows[1]["steps"] == 640
+
+
+def test_episode_progress_roundtrip(torch_cuda, oracle_lib):
+    """BatchState.ep_return / ep_length / step_index export == the oracle's, and import restores them."""
+    from paper_2402_16801_b200 import GridrogueBatch
+    O = oracle_lib
+    n = 48
+    gb = GridrogueBatch(n, "classic", 3, "none", 25)
+    gb.reset()
+    ob = O.OracleBatch("classic", n, 3, max_episode_length=25)
+    for k in range(40):
+        a = O.random_actions(3, k, n, O.TIERS["classic"]["NA"])
+        gb.step(torch_cuda.from_numpy(a).cuda())
+        ob.step(a)
+    ret, length = gb.episode_progress()
+    oret, olen = ob.episode_progress()
+    assert np.array_equal(length, olen)
+    assert np.array_equal(ret, oret)
+    assert gb.step_index == 40
+    gb.set_episode_progress(ret * 0 + 1.5, length + 1)
+    r2, l2 = gb.episode_progress()
+    assert np.all(r2 == 1.5) and np.array_equal(l2, length + 1)
