@@ -28,6 +28,8 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
     "-Xcompiler", "-fPIC", "-Xptxas", "-v",
 ]
+# dev A/B builds: GR_NVCC_EXTRA="-DGR_STEP_MINB=6" python -m paper_2402_16801_b200._build
+NVCC_FLAGS += os.environ.get("GR_NVCC_EXTRA", "").split()
 
 
 def _nvcc() -> str:

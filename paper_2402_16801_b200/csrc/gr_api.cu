@@ -27,6 +27,7 @@
 #include "gr_device.cuh"
 #include "gr_state.cuh"
 #include "gr_kernels.cuh"
+#include "gr_desc.cuh"
 
 namespace gr {
 void launch_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t pool_key,
@@ -291,6 +292,15 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.ep_length, e->n * sizeof(int32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.desc, e->n * 256);
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->S.torch_bits, e->n * sizeof(uint16_t));
+  if (rc == GR_OK) {
+    float* lut = nullptr;
+    rc = dev_alloc(e, (void**)&lut, LUT_N * sizeof(float));
+    if (rc == GR_OK) {
+      launch_init_lut(lut, 0);
+      if (cudaDeviceSynchronize() != cudaSuccess) rc = fail(GR_E_CUDA, "lut init failed");
+    }
+    e->S.lut = lut;
+  }
   const int64_t cap = std::min(e->n, e->M);
   const size_t wbytes = (size_t)cap * e->d.F * e->d.H * e->d.W;
   e->pool.cap = cap;

@@ -45,15 +45,40 @@ struct InvSrc {
 
 __device__ __forceinline__ float sq10(uint8_t n) { return __fdiv_rn(__fsqrt_rn((float)n), 10.0f); }
 
-// obs._scaled_inventory in inventory_fields order (obs.py:87-122)
+// The observation values of small integer arguments come from one table,
+// computed once per handle on the device by the exact expressions below
+// (k_init_lut), so every entry is bit-identical to evaluating them: the
+// descriptor writers then spend a load instead of an IEEE div / sqrt (20-40
+// instructions each, ~1,000 per env in the step kernel) or numpy's sin.
+constexpr int LUT_SQ10 = 0;          // sqrt(n) / 10, n < 256          (obs.py:98)
+constexpr int LUT_DIV10 = 256;       // n / 10, n < 256                (obs.py:105-121)
+constexpr int LUT_DAY = 512;         // (t % 300) / 300, t < 300       (obs.py:113)
+constexpr int LUT_DAYLIGHT = 812;    // daylight(t), t < 300           (obs.py:191-195)
+constexpr int LUT_N = 1112;
+
+__device__ __forceinline__ float lut_value_exact(int k) {
+  if (k < LUT_DIV10) return sq10((uint8_t)k);
+  if (k < LUT_DAY) return __fdiv_rn((float)(k - LUT_DIV10), 10.0f);
+  if (k < LUT_DAYLIGHT) return __fdiv_rn((float)(k - LUT_DAY), 300.0f);
+  return daylight((uint32_t)(k - LUT_DAYLIGHT));
+}
+
+__device__ __forceinline__ float lut_daylight(const float* lut, uint32_t time) {
+  return __ldg(lut + LUT_DAYLIGHT + time % 300u);
+}
+
+// obs._scaled_inventory in inventory_fields order (obs.py:87-122); the
+// divisions by 2 and 4 are exact scalings
 template <bool EXT>
-__device__ __forceinline__ void inv_section(const InvSrc& s, float* v) {
-  const float day = __fdiv_rn((float)(s.time % 300u), 300.0f);
+__device__ __forceinline__ void inv_section(const InvSrc& s, float* v, const float* lut) {
+  auto q = [&](uint8_t n) { return __ldg(lut + LUT_SQ10 + n); };
+  auto d10 = [&](uint8_t n) { return __ldg(lut + LUT_DIV10 + n); };
+  const float day = __ldg(lut + LUT_DAY + s.time % 300u);
   int k = 0;
   if (!EXT) {
-    v[k++] = sq10(s.wood); v[k++] = sq10(s.stone); v[k++] = sq10(s.coal);
-    v[k++] = sq10(s.iron); v[k++] = sq10(s.diamond); v[k++] = sq10(s.sapling);
-    v[k++] = __fdiv_rn((float)s.pick, 4.0f); v[k++] = __fdiv_rn((float)s.sword, 4.0f);
+    v[k++] = q(s.wood); v[k++] = q(s.stone); v[k++] = q(s.coal);
+    v[k++] = q(s.iron); v[k++] = q(s.diamond); v[k++] = q(s.sapling);
+    v[k++] = __fmul_rn((float)s.pick, 0.25f); v[k++] = __fmul_rn((float)s.sword, 0.25f);
     v[k++] = __fdiv_rn(s.health, 10.0f); v[k++] = __fdiv_rn(s.food, 10.0f);
     v[k++] = __fdiv_rn(s.drink, 10.0f); v[k++] = __fdiv_rn(s.energy, 10.0f);
     for (int d = 0; d < 4; ++d) v[k++] = s.facing == d ? 1.0f : 0.0f;
@@ -61,27 +86,27 @@ __device__ __forceinline__ void inv_section(const InvSrc& s, float* v) {
     v[k++] = s.sleeping ? 1.0f : 0.0f;
     return;
   }
-  v[k++] = sq10(s.wood); v[k++] = sq10(s.stone); v[k++] = sq10(s.coal); v[k++] = sq10(s.iron);
-  v[k++] = sq10(s.diamond); v[k++] = sq10(s.sapphire); v[k++] = sq10(s.ruby); v[k++] = sq10(s.sapling);
-  v[k++] = sq10(s.torch); v[k++] = sq10(s.arrow);
-  for (int p = 0; p < 6; ++p) v[k++] = sq10(s.potion[p]);
-  v[k++] = __fdiv_rn((float)s.book, 2.0f);
-  v[k++] = __fdiv_rn((float)s.pick, 4.0f);
-  v[k++] = __fdiv_rn((float)s.sword, 4.0f);
+  v[k++] = q(s.wood); v[k++] = q(s.stone); v[k++] = q(s.coal); v[k++] = q(s.iron);
+  v[k++] = q(s.diamond); v[k++] = q(s.sapphire); v[k++] = q(s.ruby); v[k++] = q(s.sapling);
+  v[k++] = q(s.torch); v[k++] = q(s.arrow);
+  for (int p = 0; p < 6; ++p) v[k++] = q(s.potion[p]);
+  v[k++] = __fmul_rn((float)s.book, 0.5f);
+  v[k++] = __fmul_rn((float)s.pick, 0.25f);
+  v[k++] = __fmul_rn((float)s.sword, 0.25f);
   v[k++] = (float)s.sword_ench;
   v[k++] = (float)s.has_bow;
-  for (int p = 0; p < 4; ++p) v[k++] = __fdiv_rn((float)s.armour[p], 2.0f);
+  for (int p = 0; p < 4; ++p) v[k++] = __fmul_rn((float)s.armour[p], 0.5f);
   for (int p = 0; p < 4; ++p) v[k++] = (float)s.armour_ench[p];
   v[k++] = __fdiv_rn(s.health, 10.0f); v[k++] = __fdiv_rn(s.food, 10.0f);
   v[k++] = __fdiv_rn(s.drink, 10.0f); v[k++] = __fdiv_rn(s.energy, 10.0f);
-  v[k++] = __fdiv_rn(s.mana, 10.0f); v[k++] = __fdiv_rn((float)s.xp, 10.0f);
-  v[k++] = __fdiv_rn((float)s.dex, 10.0f); v[k++] = __fdiv_rn((float)s.str_, 10.0f);
-  v[k++] = __fdiv_rn((float)s.intel, 10.0f);
+  v[k++] = __fdiv_rn(s.mana, 10.0f); v[k++] = d10(s.xp);
+  v[k++] = d10(s.dex); v[k++] = d10(s.str_);
+  v[k++] = d10(s.intel);
   for (int d = 0; d < 4; ++d) v[k++] = s.facing == d ? 1.0f : 0.0f;
   v[k++] = day;
   v[k++] = (float)s.sleeping; v[k++] = (float)s.resting;
   v[k++] = (float)s.learned_fire; v[k++] = (float)s.learned_ice;
-  v[k++] = __fdiv_rn((float)s.pf, 10.0f);
+  v[k++] = d10(s.pf);
   v[k++] = (float)s.cleared;
   v[k++] = (float)s.boss_vuln;
 }

@@ -91,6 +91,7 @@ struct ObsArgs {
 __host__ __device__ constexpr int pix_scratch_words(bool ext) { return ext ? 212 : 140; }
 
 void launch_step(bool ext, const DS& S, const StepArgs& a, cudaStream_t st);
+void launch_init_lut(float* lut, cudaStream_t st);
 void launch_make_desc(bool ext, const DS& S, int64_t n, cudaStream_t st);
 void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st);
 void launch_install(bool ext, const DS& S, const InstallArgs& a, int64_t grid_envs, cudaStream_t st);

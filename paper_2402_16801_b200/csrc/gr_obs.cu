@@ -1,13 +1,11 @@
 // gr_obs.cu -- observation rendering: the symbolic one-hot vector
 // (obs.encode_symbolic_batch, obs.py:191-386) and the RGB tile frame
-// (tiles.render_tiles, tiles.py:85-186), one warp per environment.
+// (tiles.render_tiles, tiles.py:85-186).
 //
-// Per env the warp first builds the egocentric view in shared memory
-// (block / item / creature channel and light per tile: obs.view_window,
-// light_window, _creature_channel_grid) and the scaled inventory, then
-// streams the row out: each lane writes consecutive 16-byte vectors, so a
-// warp instruction covers 512 contiguous bytes and every obs byte is
-// written exactly once (write-only, no read-for-ownership of the output).
+// Both writers start from the env's 256-byte observation descriptor
+// (gr_desc.cuh, written by the step / install kernels) plus the egocentric
+// window of its block / item maps, and write every output byte exactly
+// once with full-line stores (write-only, no read-for-ownership).
 #include <cstdint>
 #include <algorithm>
 #include "gr_device.cuh"
@@ -28,178 +26,8 @@ struct OT {
 };
 
 
-template <bool EXT>
-struct ViewSmem {
-  uint8_t blk[OT<EXT>::T];     // block id (global)
-  uint8_t itm[OT<EXT>::T];
-  uint8_t cre[OT<EXT>::T];
-  float light[OT<EXT>::T];
-  float inv[OT<EXT>::NINV];
-};
-
-
 __constant__ int8_t C_CLASSIC_LOCAL[37] = {0, 0, 1, 2, 3, 4, 0, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 0, 0,
                                            0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-
-// build the view of env i into v (whole warp); glow: batch-wide torch flag
-template <bool EXT>
-__device__ void build_view(const DS& S, int64_t i, bool glow, ViewSmem<EXT>& v) {
-  using O = OT<EXT>;
-  const int lane = threadIdx.x & 31;
-  const int pf = EXT ? GR_AT(S, GR_F_PFLOOR, uint8_t, 0, i) : 0;
-  const int pr = GR_AT(S, GR_F_PROW, int16_t, 0, i), pc = GR_AT(S, GR_F_PCOL, int16_t, 0, i);
-  const uint32_t time = GR_AT(S, GR_F_TIME, uint32_t, 0, i);
-  const bool sleeping = GR_AT(S, GR_F_SLEEPING, uint8_t, 0, i);
-  const uint8_t* blk = (const uint8_t*)S.f[GR_F_BLOCKS] + ((size_t)i * O::F + pf) * O::HW;
-  const uint8_t* itm = (const uint8_t*)S.f[GR_F_ITEMS] + ((size_t)i * O::F + pf) * O::HW;
-  const float base = pf == 0 ? daylight(time) : C_FLOOR_AMB[pf];
-  const int r0 = pr - O::VR / 2, c0 = pc - O::VC / 2;
-  for (int t = lane; t < O::T; t += 32) {
-    const int r = r0 + t / O::VC, c = c0 + t % O::VC;
-    const bool inb = r >= 0 && r < O::H && c >= 0 && c < O::W;
-    const uint8_t b = inb ? blk[r * O::W + c] : B_OOB;
-    v.blk[t] = b;
-    v.itm[t] = inb && EXT ? itm[r * O::W + c] : 0;
-    v.cre[t] = 0;
-    v.light[t] = base;
-  }
-  __syncwarp();
-  if (EXT && glow) {
-    // obs._torch_light over the (VR+6)x(VC+6) item window: each torch lights
-    // view tiles within Chebyshev 3 at 1 - d/4
-    constexpr int WR = O::VR + 6, WC = O::VC + 6;
-    for (int t = lane; t < WR * WC; t += 32) {
-      const int wr = t / WC - 3, wc = t % WC - 3;   // view coordinates
-      const int r = r0 + wr, c = c0 + wc;
-      if (r < 0 || r >= O::H || c < 0 || c >= O::W || itm[r * O::W + c] != I_TORCH) continue;
-      for (int a = max(wr - 3, 0); a <= min(wr + 3, O::VR - 1); ++a)
-        for (int b = max(wc - 3, 0); b <= min(wc + 3, O::VC - 1); ++b) {
-          const int d = max(abs(a - wr), abs(b - wc));
-          const float g = 1.0f - 0.25f * (float)d;   // exact: 1, .75, .5, .25
-          atomicMax(reinterpret_cast<int*>(&v.light[a * O::VC + b]), __float_as_int(g));
-        }
-    }
-    __syncwarp();
-  }
-  if (sleeping)
-    for (int t = lane; t < O::T; t += 32) v.light[t] = 0.0f;
-  // creature channels (obs.py:263-296): lane s loads slot s in parallel
-  // (melee 0-2, ranged 3-4, passive 5-7, enemy proj 8-10, player proj 11-13);
-  // the paint order -- later slots overwrite earlier ones -- is kept by
-  // letting the highest slot index win each cell
-  {
-    constexpr int NSLOT = EXT ? 14 : 11;
-    int cell = -1, ch = 0;
-    if (lane < NSLOT) {
-      int r = 0, c = 0, alive = 0;
-      if (lane < 8) {
-        const int cls = lane < 3 ? 0 : lane < 5 ? 1 : 2;
-        const int l = lane - (cls == 0 ? 0 : cls == 1 ? 3 : 5), cap = cls == 1 ? 2 : 3;
-        const int fp = cls == 0 ? GR_F_MEL_POS : cls == 1 ? GR_F_RAN_POS : GR_F_PAS_POS;
-        const int fa = cls < 2 ? fp + 3 : fp + 2, ft = cls < 2 ? fp + 4 : fp + 3;
-        const int li = pf * cap + l;
-        r = GR_AT(S, fp, int16_t, 2 * li, i);
-        c = GR_AT(S, fp, int16_t, 2 * li + 1, i);
-        alive = GR_AT(S, fa, uint8_t, li, i);
-        const int ty = GR_AT(S, ft, uint8_t, li, i);
-        ch = EXT ? ty + 1 : (ty == 0 ? 1 : ty == 2 ? 2 : ty == 1 ? 3 : 0);
-      } else {
-        const bool ep = lane < 11;
-        const int l = ep ? lane - 8 : lane - 11;
-        const int fp = ep ? GR_F_EPROJ_POS : GR_F_PPROJ_POS;
-        r = GR_AT(S, fp, int16_t, 2 * l, i);
-        c = GR_AT(S, fp, int16_t, 2 * l + 1, i);
-        alive = GR_AT(S, ep ? GR_F_EPROJ_ALIVE : GR_F_PPROJ_ALIVE, uint8_t, l, i);
-        ch = EXT ? GR_AT(S, ep ? GR_F_EPROJ_TYPE : GR_F_PPROJ_TYPE, uint8_t, l, i) + 20 : 4;
-      }
-      const int wr = r - r0, wc = c - c0;
-      if (alive && wr >= 0 && wr < O::VR && wc >= 0 && wc < O::VC) cell = wr * O::VC + wc;
-    }
-    // later slots win: a slot paints unless a higher slot targets the same cell
-    bool win = cell >= 0;
-    for (int s = 1; s < NSLOT; ++s) {
-      const int oc = __shfl_down_sync(0xffffffffu, cell, s);
-      if (lane + s < NSLOT && oc == cell) win = false;
-    }
-    if (win) v.cre[cell] = (uint8_t)ch;
-  }
-  // inventory section (obs._scaled_inventory, obs.py:300-340)
-  for (int k = lane; k < O::NINV; k += 32) {
-    auto sq = [](uint8_t n) { return __fdiv_rn(__fsqrt_rn((float)n), 10.0f); };
-    auto u8 = [&](int fid, int c) { return GR_AT(S, fid, uint8_t, c, i); };
-    auto f32 = [&](int fid) { return GR_AT(S, fid, float, 0, i); };
-    const uint8_t facing = u8(GR_F_FACING, 0);
-    const float day = __fdiv_rn((float)(time % 300u), 300.0f);
-    float x = 0.0f;
-    if (!EXT) {
-      switch (k) {
-        case 0: x = sq(u8(GR_F_INV_WOOD, 0)); break;
-        case 1: x = sq(u8(GR_F_INV_STONE, 0)); break;
-        case 2: x = sq(u8(GR_F_INV_COAL, 0)); break;
-        case 3: x = sq(u8(GR_F_INV_IRON, 0)); break;
-        case 4: x = sq(u8(GR_F_INV_DIAMOND, 0)); break;
-        case 5: x = sq(u8(GR_F_INV_SAPLING, 0)); break;
-        case 6: x = __fdiv_rn((float)u8(GR_F_PICK_TIER, 0), 4.0f); break;
-        case 7: x = __fdiv_rn((float)u8(GR_F_SWORD_TIER, 0), 4.0f); break;
-        case 8: x = __fdiv_rn(f32(GR_F_HEALTH), 10.0f); break;
-        case 9: x = __fdiv_rn(f32(GR_F_FOOD), 10.0f); break;
-        case 10: x = __fdiv_rn(f32(GR_F_DRINK), 10.0f); break;
-        case 11: x = __fdiv_rn(f32(GR_F_ENERGY), 10.0f); break;
-        case 12: case 13: case 14: case 15: x = facing == k - 12 ? 1.0f : 0.0f; break;
-        case 16: x = day; break;
-        default: x = sleeping ? 1.0f : 0.0f; break;
-      }
-    } else {
-      if (k < 10) {
-        const int fids[10] = {GR_F_INV_WOOD, GR_F_INV_STONE, GR_F_INV_COAL, GR_F_INV_IRON, GR_F_INV_DIAMOND,
-                              GR_F_INV_SAPPHIRE, GR_F_INV_RUBY, GR_F_INV_SAPLING, GR_F_INV_TORCH, GR_F_INV_ARROW};
-        x = sq(u8(fids[k], 0));
-      } else if (k < 16) {
-        x = sq(u8(GR_F_INV_POTION, k - 10));
-      } else if (k == 16) {
-        x = __fdiv_rn((float)u8(GR_F_INV_BOOK, 0), 2.0f);
-      } else if (k == 17) {
-        x = __fdiv_rn((float)u8(GR_F_PICK_TIER, 0), 4.0f);
-      } else if (k == 18) {
-        x = __fdiv_rn((float)u8(GR_F_SWORD_TIER, 0), 4.0f);
-      } else if (k == 19) {
-        x = (float)u8(GR_F_SWORD_ENCH, 0);
-      } else if (k == 20) {
-        x = (float)u8(GR_F_HAS_BOW, 0);
-      } else if (k < 25) {
-        x = __fdiv_rn((float)u8(GR_F_ARMOUR, k - 21), 2.0f);
-      } else if (k < 29) {
-        x = (float)u8(GR_F_ARMOUR_ENCH, k - 25);
-      } else if (k < 34) {
-        const int fids[5] = {GR_F_HEALTH, GR_F_FOOD, GR_F_DRINK, GR_F_ENERGY, GR_F_MANA};
-        x = __fdiv_rn(f32(fids[k - 29]), 10.0f);
-      } else if (k < 38) {
-        const int fids[4] = {GR_F_XP, GR_F_DEX, GR_F_STR, GR_F_INTEL};
-        x = __fdiv_rn((float)u8(fids[k - 34], 0), 10.0f);
-      } else if (k < 42) {
-        x = facing == k - 38 ? 1.0f : 0.0f;
-      } else if (k == 42) {
-        x = day;
-      } else if (k == 43) {
-        x = sleeping ? 1.0f : 0.0f;
-      } else if (k == 44) {
-        x = (float)u8(GR_F_RESTING, 0);
-      } else if (k == 45) {
-        x = (float)u8(GR_F_LEARNED_FIRE, 0);
-      } else if (k == 46) {
-        x = (float)u8(GR_F_LEARNED_ICE, 0);
-      } else if (k == 47) {
-        x = __fdiv_rn((float)pf, 10.0f);
-      } else if (k == 48) {
-        x = (float)u8(GR_F_FLOOR_CLEARED, pf);
-      } else {
-        x = (float)u8(GR_F_BOSS_VULN, 0);
-      }
-    }
-    v.inv[k] = x;
-  }
-  __syncwarp();
-}
 
 // the window of env i's current floor: lane t (+32q) holds tile t's block and item
 template <bool EXT>

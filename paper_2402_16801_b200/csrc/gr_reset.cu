@@ -133,13 +133,13 @@ __device__ void install_one(const DS& S, int64_t i, const WMeta& m, const uint8_
       s.dex = s.str_ = s.intel = 1;
       s.facing = 3;
       s.health = 10.0f; s.food = 13.0f; s.drink = 13.0f; s.energy = 13.0f; s.mana = 17.0f;
-      inv_section<EXT>(s, inv_s);
+      inv_section<EXT>(s, inv_s, S.lut);
     }
     __syncwarp();
     for (int k = lane; k < DESC_WORDS; k += 32) {
       uint32_t w = 0;
       if (k < NINV) w = __float_as_uint(inv_s[k]);
-      else if (k == D_BASE) w = __float_as_uint(daylight(0));
+      else if (k == D_BASE) w = __float_as_uint(lut_daylight(S.lut, 0));
       else if (k == D_POS) w = (uint32_t)(uint16_t)m.spawn[0] | ((uint32_t)(uint16_t)m.spawn[1] << 16);
       else if (k >= D_CRE && k < D_CRE + 7) w = 0xFFFFFFFFu;
       d[k] = w;

@@ -74,6 +74,7 @@ struct DS {
   int32_t* ep_length;         // batch.BatchState.ep_length
   uint32_t* desc;             // [ns][64] observation descriptors (gr_desc.cuh)
   uint16_t* torch_bits;       // bit f: a torch may lie on floor f (torches are never removed)
+  const float* lut;           // exact small-argument tables of the observation values (gr_desc.cuh)
 };
 
 // one generated world (worldgen.World) in a world buffer

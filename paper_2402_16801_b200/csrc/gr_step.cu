@@ -1131,7 +1131,7 @@ __device__ void grow_plants(Ctx& e) {
 
 // the observation descriptor of this env (gr_desc.cuh) from registers
 template <bool EXT>
-__device__ void write_desc(const Ctx& e, uint32_t* d) {
+__device__ void write_desc(const Ctx& e, uint32_t* d, const float* lut) {
   InvSrc s;
   s.wood = e.inv_wood; s.stone = e.inv_stone; s.coal = e.inv_coal; s.iron = e.inv_iron;
   s.diamond = e.inv_diamond; s.sapphire = e.inv_sapphire; s.ruby = e.inv_ruby; s.sapling = e.inv_sapling;
@@ -1147,12 +1147,12 @@ __device__ void write_desc(const Ctx& e, uint32_t* d) {
   s.health = e.health; s.food = e.food; s.drink = e.drink; s.energy = e.energy; s.mana = e.mana;
   s.time = e.time;
   float inv[50];
-  inv_section<EXT>(s, inv);
+  inv_section<EXT>(s, inv, lut);
   uint32_t w[DESC_WORDS];
   constexpr int NINV = EXT ? 50 : 18;
 #pragma unroll
   for (int k = 0; k < 50; ++k) w[k] = k < NINV ? __float_as_uint(inv[k]) : 0u;
-  w[D_BASE] = __float_as_uint(e.pfloor == 0 ? daylight(e.time) : C_FLOOR_AMB[e.pfloor]);
+  w[D_BASE] = __float_as_uint(e.pfloor == 0 ? lut_daylight(lut, e.time) : C_FLOOR_AMB[e.pfloor]);
   w[D_POS] = (uint32_t)(uint16_t)e.prow | ((uint32_t)(uint16_t)e.pcol << 16);
   w[D_FLAGS] = (uint32_t)e.pfloor | ((uint32_t)e.sleeping << 8) | ((uint32_t)((e.torch >> e.pfloor) & 1u) << 9);
   uint32_t slot[14];
@@ -1187,7 +1187,7 @@ __global__ void __launch_bounds__(128) k_make_desc(DS S, int64_t n) {
   e.itm = (uint8_t*)S.f[GR_F_ITEMS] + (size_t)i * T::F * T::HW;
   load_env<EXT>(e, S);
   load_lanes<EXT>(e, S, e.pfloor);
-  write_desc<EXT>(e, S.desc + (size_t)i * DESC_WORDS);
+  write_desc<EXT>(e, S.desc + (size_t)i * DESC_WORDS, S.lut);
 }
 
 void launch_make_desc(bool ext, const DS& S, int64_t n, cudaStream_t st) {
@@ -1211,7 +1211,10 @@ __device__ __forceinline__ void apply_pending(Ctx& e, uint8_t pend, uint32_t pre
 }
 
 template <bool EXT>
-__global__ void __launch_bounds__(128, 4) k_step(DS S, StepArgs a) {
+#ifndef GR_STEP_MINB
+#define GR_STEP_MINB 4   // resident CTAs per SM the register budget is fitted to (128 regs/thread)
+#endif
+__global__ void __launch_bounds__(128, GR_STEP_MINB) k_step(DS S, StepArgs a) {
   using T = TD<EXT>;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < a.n && !(a.bad && a.bad[0] >= 0);
@@ -1287,7 +1290,7 @@ __global__ void __launch_bounds__(128, 4) k_step(DS S, StepArgs a) {
       for (int k = 0; k < T::A; ++k) nw[k] = (newly[k >> 5] >> (k & 31)) & 1u;
     }
     if (a.reward64) a.reward64[i] = reward;
-    if (!done) write_desc<EXT>(e, S.desc + (size_t)i * DESC_WORDS);   // reset envs: install writes it
+    if (!done) write_desc<EXT>(e, S.desc + (size_t)i * DESC_WORDS, S.lut);   // reset envs: install writes it
     my_done = done;
     if (EXT && !done && C_FLOOR_AMB[e.pfloor] < 1.0f) my_flags |= 4u;
   }
@@ -1321,6 +1324,14 @@ __global__ void __launch_bounds__(128, 4) k_step(DS S, StepArgs a) {
     *a.arrive = 0u;
   }
 }
+
+// the observation value tables (gr_desc.cuh), evaluated by the exact expressions
+__global__ void k_init_lut(float* lut) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < LUT_N) lut[k] = lut_value_exact(k);
+}
+
+void launch_init_lut(float* lut, cudaStream_t st) { k_init_lut<<<(LUT_N + 127) / 128, 128, 0, st>>>(lut); }
 
 void launch_step(bool ext, const DS& S, const StepArgs& a, cudaStream_t st) {
   const int bs = 128;
