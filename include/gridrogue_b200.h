@@ -174,6 +174,7 @@ int gr_observe(gr_env *env, void *obs_dev, void *stream);
 
 /* ---- metrics ------------------------------------------------------------- */
 int gr_stats_get(gr_env *env, gr_stats *out);                 /* EpisodeStats */
+int gr_stats_set(gr_env *env, const gr_stats *in);            /* restore (checkpoint / resume) */
 int gr_level_seeds(gr_env *env, uint64_t *host_dst);          /* BatchState.level_seeds */
 int gr_episodes_completed(gr_env *env, int64_t *out);         /* info["episodes_completed"] */
 /* count of kernels this library launched since creation (bench evidence) */

@@ -101,6 +101,7 @@ def lib() -> ctypes.CDLL:
         "gr_import_field": (I32, [P, I32, P]),
         "gr_observe": (I32, [P, P, P]),
         "gr_stats_get": (I32, [P, ctypes.POINTER(GrStats)]),
+        "gr_stats_set": (I32, [P, ctypes.POINTER(GrStats)]),
         "gr_level_seeds": (I32, [P, P]),
         "gr_episodes_completed": (I32, [P, ctypes.POINTER(I64)]),
         "gr_export_episode": (I32, [P, P, P]),

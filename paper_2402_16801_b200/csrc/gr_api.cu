@@ -803,6 +803,21 @@ int gr_stats_get(gr_env* e, gr_stats* out) {
   return GR_OK;
 }
 
+int gr_stats_set(gr_env* e, const gr_stats* in) {
+  if (!e || !in) return fail(GR_E_INVALID, "null argument");
+  if (in->episodes < 0 || in->total_steps < 0) return fail(GR_E_INVALID, "negative episode statistics");
+  CK(cudaSetDevice(e->cfg.device));
+  CK(cudaDeviceSynchronize());
+  const unsigned long long ep = (unsigned long long)in->episodes, steps = (unsigned long long)in->total_steps;
+  unsigned long long ach[67];
+  for (int a = 0; a < 67; ++a) ach[a] = (unsigned long long)in->ach_episodes[a];
+  CK(cudaMemcpy(e->st_episodes, &ep, sizeof(ep), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e->st_steps, &steps, sizeof(steps), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e->st_return, &in->total_return, sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e->st_ach, ach, sizeof(ach), cudaMemcpyHostToDevice));
+  return GR_OK;
+}
+
 int gr_export_episode(gr_env* e, double* ep_return_host, int64_t* ep_length_host) {
   if (!e) return fail(GR_E_INVALID, "null env");
   CK(cudaSetDevice(e->cfg.device));

@@ -174,8 +174,11 @@ class GridrogueBatch:
             raise ValueError(f"field {name}: expected {self.n * n_el * esz} bytes, got {a.nbytes}")
         check(lib().gr_import_field(self.h, _lib.FIELD_ID[name], a.ctypes.data_as(ctypes.c_void_p)))
 
-    def export_state(self, shapes: dict) -> dict:
-        """Every SimState field as numpy, given {name: (dtype, shape)}."""
+    def export_state(self, shapes: dict | None = None) -> dict:
+        """Every SimState field as numpy in the reference layout (layout.field_shapes)."""
+        if shapes is None:
+            from .layout import field_shapes
+            shapes = field_shapes(self.tier, self.n)
         out = {}
         for name in _lib.FIELD_NAMES:
             dt, shape = shapes[name]
@@ -221,6 +224,17 @@ class GridrogueBatch:
     def step_index(self, value: int) -> None:
         self.torch.cuda.synchronize(self.device)
         check(lib().gr_set_step_index(self.h, int(value)))
+
+    def set_stats(self, stats: dict) -> None:
+        """Restore EpisodeStats (checkpoint / resume)."""
+        s = _lib.GrStats()
+        s.episodes = int(stats["episodes"])
+        s.total_steps = int(stats["total_steps"])
+        s.total_return = float(stats["total_return"])
+        ach = np.asarray(stats["ach_episodes"], np.int64)
+        for k in range(min(len(ach), 67)):
+            s.ach_episodes[k] = int(ach[k])
+        check(lib().gr_stats_set(self.h, ctypes.byref(s)))
 
     def episodes_completed(self) -> int:
         v = ctypes.c_int64()
