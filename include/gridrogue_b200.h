@@ -172,6 +172,37 @@ int gr_set_step_index(gr_env *env, int64_t step_index);
 /* encode the current state (no step): symbolic or pixels per obs_mode */
 int gr_observe(gr_env *env, void *obs_dev, void *stream);
 
+/* ---- level buffers (UED curricula; mutate.py, worldgen.py, state.py) ------ *
+ * A device buffer of `capacity` levels: LevelParams (seed, 252 overworld
+ * angles, 9 floor seeds) and the World generated from them.  All calls are
+ * synchronous; index / key arrays are host memory. */
+typedef struct gr_levels gr_levels;
+enum { GR_MUT_NOISE = 0, GR_MUT_SWAP = 1, GR_MUT_RSWAP = 2 };
+int gr_levels_create(gr_env *env, int64_t capacity, gr_levels **out);
+void gr_levels_destroy(gr_levels *lv);
+/* params of levels [first, first+count): angles / floor_seeds NULL =
+ * worldgen.make_level_params(seed) (worldgen.py:75-87) */
+int gr_levels_set_params(gr_levels *lv, int64_t first, int64_t count, const uint64_t *seeds,
+                         const float *angles, const uint64_t *floor_seeds);
+int gr_levels_get_params(gr_levels *lv, int64_t first, int64_t count, uint64_t *seeds, float *angles,
+                         uint64_t *floor_seeds);
+/* worldgen.generate_world(params) for levels [first, first+count) (worldgen.py:636-651) */
+int gr_levels_generate(gr_levels *lv, int64_t first, int64_t count);
+/* mutate.mutate_noise (params; regenerate after) / mutate_swap / mutate_rswap
+ * (worlds, in place) of level_idx[k] with the RngStream (stream_key[k],
+ * stream_counter[k]); scale: mutate_noise's range (mutate.NOISE_RANGE = 0.5) */
+int gr_levels_mutate(gr_levels *lv, int32_t op, int64_t count, const int64_t *level_idx,
+                     const uint64_t *stream_key, const uint64_t *stream_counter, double scale);
+/* state.install_world(sim, env_idx[k], level level_idx[k], keys[k]) (state.py:169-249);
+ * also clears the env's running episode return / length */
+int gr_levels_install(gr_levels *lv, int64_t count, const int64_t *env_idx, const int64_t *level_idx,
+                      const uint64_t *keys);
+/* one World in the reference's layout: blocks / items [F][H][W], spawn[2],
+ * ladders [F][4] (down r, c, up r, c; -1 none), chests [F][6][4] (r, c,
+ * loot, qty; -1 rows pad), potion permutation [6] */
+int gr_levels_export_world(gr_levels *lv, int64_t level, uint8_t *blocks, uint8_t *items, int16_t *spawn,
+                           int16_t *ladders, int64_t *chests, uint8_t *potion);
+
 /* ---- metrics ------------------------------------------------------------- */
 int gr_stats_get(gr_env *env, gr_stats *out);                 /* EpisodeStats */
 int gr_stats_set(gr_env *env, const gr_stats *in);            /* restore (checkpoint / resume) */

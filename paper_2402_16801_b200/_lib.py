@@ -105,6 +105,14 @@ def lib() -> ctypes.CDLL:
         "gr_level_seeds": (I32, [P, P]),
         "gr_episodes_completed": (I32, [P, ctypes.POINTER(I64)]),
         "gr_export_episode": (I32, [P, P, P]),
+        "gr_levels_create": (I32, [P, I64, ctypes.POINTER(P)]),
+        "gr_levels_destroy": (None, [P]),
+        "gr_levels_set_params": (I32, [P, I64, I64, P, P, P]),
+        "gr_levels_get_params": (I32, [P, I64, I64, P, P, P]),
+        "gr_levels_generate": (I32, [P, I64, I64]),
+        "gr_levels_mutate": (I32, [P, I32, I64, P, P, P, ctypes.c_double]),
+        "gr_levels_install": (I32, [P, I64, P, P, P]),
+        "gr_levels_export_world": (I32, [P, I64, P, P, P, P, P, P]),
         "gr_import_episode": (I32, [P, P, P]),
         "gr_get_step_index": (I32, [P, ctypes.POINTER(I64)]),
         "gr_set_step_index": (I32, [P, I64]),

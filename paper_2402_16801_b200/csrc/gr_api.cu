@@ -28,6 +28,7 @@
 #include "gr_state.cuh"
 #include "gr_kernels.cuh"
 #include "gr_desc.cuh"
+#include "gr_levels.cuh"
 
 namespace gr {
 void launch_finish_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t pool_key,
@@ -217,6 +218,31 @@ static int dev_alloc(gr_env* e, void** p, size_t bytes) {
   if (err != cudaSuccess) return fail(GR_E_CUDA, "cudaMemset: %s", cudaGetErrorString(err));
   return GR_OK;
 }
+
+// ---------------------------------------------------------- level buffers
+struct gr_levels {
+  gr_env* e;
+  int64_t cap;
+  WBuf w;
+  LevelParamsBuf p;
+  std::vector<void*> allocs;
+};
+
+// host index / key arrays -> device scratch (freed on return)
+struct DevArrays {
+  std::vector<void*> p;
+  ~DevArrays() {
+    for (void* q : p) cudaFree(q);
+  }
+  template <class T>
+  T* put(const T* host, int64_t n) {
+    void* d = nullptr;
+    if (cudaMalloc(&d, std::max<int64_t>(n, 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    p.push_back(d);
+    if (n && cudaMemcpy(d, host, n * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    return (T*)d;
+  }
+};
 
 extern "C" {
 
@@ -861,6 +887,173 @@ int gr_set_step_index(gr_env* e, int64_t step_index) {
   const unsigned long long v = (unsigned long long)step_index;
   CK(cudaMemcpy(e->dstep, &v, sizeof(v), cudaMemcpyHostToDevice));
   e->step_index = step_index;
+  return GR_OK;
+}
+
+void gr_levels_destroy(gr_levels* lv) {
+  if (!lv) return;
+  cudaSetDevice(lv->e->cfg.device);
+  cudaDeviceSynchronize();
+  for (void* q : lv->allocs) cudaFree(q);
+  delete lv;
+}
+
+int gr_levels_create(gr_env* e, int64_t capacity, gr_levels** out) {
+  if (!e || !out || capacity <= 0) return fail(GR_E_INVALID, "bad level buffer arguments");
+  CK(cudaSetDevice(e->cfg.device));
+  gr_levels* lv = new gr_levels();
+  lv->e = e;
+  lv->cap = capacity;
+  const size_t mb = (size_t)capacity * e->d.F * e->d.H * e->d.W;
+  auto al = [&](void** q, size_t bytes) -> bool {
+    if (cudaMalloc(q, bytes) != cudaSuccess) return false;
+    lv->allocs.push_back(*q);
+    return cudaMemset(*q, 0, bytes) == cudaSuccess;
+  };
+  const bool ok = al((void**)&lv->w.blocks, mb) && al((void**)&lv->w.items, mb) &&
+                  al((void**)&lv->w.meta, capacity * sizeof(WMeta)) &&
+                  al((void**)&lv->p.seed, capacity * sizeof(uint64_t)) &&
+                  al((void**)&lv->p.angles, capacity * 252 * sizeof(float)) &&
+                  al((void**)&lv->p.floor_seed, capacity * 9 * sizeof(uint64_t));
+  lv->w.cap = capacity;
+  if (!ok) {
+    gr_levels_destroy(lv);
+    return fail(GR_E_OOM, "level buffer of %lld levels: out of device memory", (long long)capacity);
+  }
+  *out = lv;
+  return GR_OK;
+}
+
+static int lv_range(gr_levels* lv, int64_t first, int64_t count) {
+  if (!lv) return fail(GR_E_INVALID, "null level buffer");
+  if (first < 0 || count < 0 || first + count > lv->cap)
+    return fail(GR_E_INVALID, "levels [%lld, %lld) outside the buffer of %lld", (long long)first,
+                (long long)(first + count), (long long)lv->cap);
+  return GR_OK;
+}
+
+int gr_levels_set_params(gr_levels* lv, int64_t first, int64_t count, const uint64_t* seeds, const float* angles,
+                         const uint64_t* floor_seeds) {
+  int rc = lv_range(lv, first, count);
+  if (rc) return rc;
+  if (!seeds || (!angles) != (!floor_seeds)) return fail(GR_E_INVALID, "seeds required; angles and floor seeds together");
+  CK(cudaSetDevice(lv->e->cfg.device));
+  CK(cudaMemcpy(lv->p.seed + first, seeds, count * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  if (angles) {
+    CK(cudaMemcpy(lv->p.angles + first * 252, angles, count * 252 * sizeof(float), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(lv->p.floor_seed + first * 9, floor_seeds, count * 9 * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  } else {
+    launch_level_params(lv->p, first, count, 0);
+    CK(cudaGetLastError());
+  }
+  CK(cudaDeviceSynchronize());
+  return GR_OK;
+}
+
+int gr_levels_get_params(gr_levels* lv, int64_t first, int64_t count, uint64_t* seeds, float* angles,
+                         uint64_t* floor_seeds) {
+  int rc = lv_range(lv, first, count);
+  if (rc) return rc;
+  CK(cudaSetDevice(lv->e->cfg.device));
+  CK(cudaDeviceSynchronize());
+  if (seeds) CK(cudaMemcpy(seeds, lv->p.seed + first, count * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (angles) CK(cudaMemcpy(angles, lv->p.angles + first * 252, count * 252 * sizeof(float), cudaMemcpyDeviceToHost));
+  if (floor_seeds)
+    CK(cudaMemcpy(floor_seeds, lv->p.floor_seed + first * 9, count * 9 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return GR_OK;
+}
+
+int gr_levels_generate(gr_levels* lv, int64_t first, int64_t count) {
+  int rc = lv_range(lv, first, count);
+  if (rc) return rc;
+  if (!count) return GR_OK;
+  gr_env* e = lv->e;
+  CK(cudaSetDevice(e->cfg.device));
+  CK(cudaMemset(lv->w.meta + first, 0, count * sizeof(WMeta)));
+  WorldJob j{};
+  j.mode = 2;
+  j.count = count;
+  j.first = first;
+  j.out = lv->w;
+  j.params = lv->p;
+  j.counters = e->counters;
+  launch_worldgen(e->ext, j, 0);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return GR_OK;
+}
+
+int gr_levels_mutate(gr_levels* lv, int32_t op, int64_t count, const int64_t* level_idx, const uint64_t* stream_key,
+                     const uint64_t* stream_counter, double scale) {
+  if (!lv || count < 0 || (count && (!level_idx || !stream_key || !stream_counter)))
+    return fail(GR_E_INVALID, "bad mutation arguments");
+  if (op != GR_MUT_NOISE && op != GR_MUT_SWAP && op != GR_MUT_RSWAP) return fail(GR_E_INVALID, "unknown mutation %d", op);
+  for (int64_t k = 0; k < count; ++k)
+    if (level_idx[k] < 0 || level_idx[k] >= lv->cap) return fail(GR_E_INVALID, "level %lld out of range", (long long)level_idx[k]);
+  if (!count) return GR_OK;
+  CK(cudaSetDevice(lv->e->cfg.device));
+  DevArrays d;
+  const int64_t* di = d.put(level_idx, count);
+  const uint64_t* dk = d.put(stream_key, count);
+  const uint64_t* dc = d.put(stream_counter, count);
+  if (!di || !dk || !dc) return fail(GR_E_OOM, "mutation scratch");
+  launch_mutate(lv->e->ext, op, lv->p, lv->w, di, dk, dc, count, scale, 0);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return GR_OK;
+}
+
+int gr_levels_install(gr_levels* lv, int64_t count, const int64_t* env_idx, const int64_t* level_idx,
+                      const uint64_t* keys) {
+  if (!lv || count < 0 || (count && (!env_idx || !level_idx || !keys))) return fail(GR_E_INVALID, "bad install arguments");
+  gr_env* e = lv->e;
+  for (int64_t k = 0; k < count; ++k) {
+    if (env_idx[k] < 0 || env_idx[k] >= e->n) return fail(GR_E_INVALID, "env %lld out of range", (long long)env_idx[k]);
+    if (level_idx[k] < 0 || level_idx[k] >= lv->cap)
+      return fail(GR_E_INVALID, "level %lld out of range", (long long)level_idx[k]);
+  }
+  if (!count) return GR_OK;
+  CK(cudaSetDevice(e->cfg.device));
+  int rc = materialize(e);   // deferred cooldowns of the envs being replaced
+  if (rc) return rc;
+  DevArrays d;
+  const int64_t* de = d.put(env_idx, count);
+  const int64_t* dl = d.put(level_idx, count);
+  const uint64_t* dk = d.put(keys, count);
+  if (!de || !dl || !dk) return fail(GR_E_OOM, "install scratch");
+  launch_install_levels(e->ext, e->S, lv->w, de, dl, dk, count, 0);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  e->have_reset = true;
+  return GR_OK;
+}
+
+int gr_levels_export_world(gr_levels* lv, int64_t level, uint8_t* blocks, uint8_t* items, int16_t* spawn,
+                           int16_t* ladders, int64_t* chests, uint8_t* potion) {
+  int rc = lv_range(lv, level, 1);
+  if (rc) return rc;
+  gr_env* e = lv->e;
+  CK(cudaSetDevice(e->cfg.device));
+  CK(cudaDeviceSynchronize());
+  const size_t mb = (size_t)e->d.F * e->d.H * e->d.W;
+  if (blocks) CK(cudaMemcpy(blocks, lv->w.blocks + level * mb, mb, cudaMemcpyDeviceToHost));
+  if (items) CK(cudaMemcpy(items, lv->w.items + level * mb, mb, cudaMemcpyDeviceToHost));
+  WMeta m;
+  CK(cudaMemcpy(&m, lv->w.meta + level, sizeof(m), cudaMemcpyDeviceToHost));
+  const int F = e->d.F;
+  if (spawn) { spawn[0] = m.spawn[0]; spawn[1] = m.spawn[1]; }
+  if (ladders)
+    for (int f = 0; f < F; ++f) {
+      ladders[4 * f] = m.ld[f][0]; ladders[4 * f + 1] = m.ld[f][1];
+      ladders[4 * f + 2] = m.lu[f][0]; ladders[4 * f + 3] = m.lu[f][1];
+    }
+  if (chests)
+    for (int f = 0; f < F; ++f)
+      for (int jj = 0; jj < 6; ++jj)
+        for (int q = 0; q < 4; ++q)
+          chests[(f * 6 + jj) * 4 + q] = (e->ext && jj < m.nch[f]) ? (int64_t)m.chest[f][jj][q] : -1;
+  if (potion)
+    for (int k = 0; k < 6; ++k) potion[k] = m.potion[k];
   return GR_OK;
 }
 

@@ -46,8 +46,15 @@ struct StepInfo {
   uint64_t step_key;    // WorldPool._step_key of the pool serving this step
 };
 
+// explicit LevelParams (worldgen.LevelParams) of a level buffer
+struct LevelParamsBuf {
+  uint64_t* seed;         // [cap]
+  float* angles;          // [cap][252]: the overworld octave grids, flattened in order
+  uint64_t* floor_seed;   // [cap][9]
+};
+
 struct WorldJob {
-  int mode;               // 0: initial reset (env-indexed seeds), 1: pool
+  int mode;               // 0: initial reset (env-indexed seeds), 1: pool, 2: explicit params
   int64_t count;          // worlds (mode 0: n envs; mode 1: read from info->n_pool)
   const StepInfo* info;   // mode 1
   uint64_t env_key;       // mode 0: split(make_stream(seed), 0).key
@@ -56,6 +63,8 @@ struct WorldJob {
   WBuf out;
   unsigned long long* counters;  // [5] diagnostics
   int ctas_per_sm;               // resident CTAs per SM (0 = default)
+  LevelParamsBuf params;         // mode 2: world w of the job <- params / out slot first + w
+  int64_t first;
 };
 
 struct InstallArgs {
@@ -94,6 +103,8 @@ void launch_step(bool ext, const DS& S, const StepArgs& a, cudaStream_t st);
 void launch_init_lut(float* lut, cudaStream_t st);
 void launch_make_desc(bool ext, const DS& S, int64_t n, cudaStream_t st);
 void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st);
+// make_level_params(seed) for params slots [first, first + count) (seeds already set)
+void launch_level_params(const LevelParamsBuf& p, int64_t first, int64_t count, cudaStream_t st);
 void launch_install(bool ext, const DS& S, const InstallArgs& a, int64_t grid_envs, cudaStream_t st);
 void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st);
 void launch_pixels(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st);

@@ -14,6 +14,7 @@
 #include "gr_kernels.cuh"
 #include "gr_desc.cuh"
 #include "gr_tail.cuh"
+#include "gr_levels.cuh"
 
 namespace gr {
 
@@ -146,6 +147,33 @@ __device__ void install_one(const DS& S, int64_t i, const WMeta& m, const uint8_
     }
   }
 #undef Z
+}
+
+// level buffer -> chosen envs (UED): level_idx[k] installed into env_idx[k]
+// with install key keys[k] (state.install_world, state.py:169-171)
+template <bool EXT>
+__global__ void __launch_bounds__(128) k_install_levels(DS S, WBuf w, const int64_t* env_idx, const int64_t* level_idx,
+                                                        const uint64_t* keys, int64_t count) {
+  constexpr int F = EXT ? 9 : 1, HW = EXT ? 48 * 48 : 64 * 64;
+  __shared__ WMeta m;
+  for (int64_t k = blockIdx.x; k < count; k += gridDim.x) {
+    const int64_t l = level_idx[k];
+    if (threadIdx.x == 0) {
+      m = w.meta[l];
+      m.key = keys[k];
+    }
+    __syncthreads();
+    install_one<EXT>(S, env_idx[k], m, w.blocks + (size_t)l * F * HW, w.items + (size_t)l * F * HW);
+    __syncthreads();
+  }
+}
+
+void launch_install_levels(bool ext, const DS& S, const WBuf& w, const int64_t* env_idx, const int64_t* level_idx,
+                           const uint64_t* keys, int64_t count, cudaStream_t st) {
+  if (count <= 0) return;
+  const int grid = (int)std::min<int64_t>(count, 148 * 8);
+  if (ext) k_install_levels<true><<<grid, 128, 0, st>>>(S, w, env_idx, level_idx, keys, count);
+  else k_install_levels<false><<<grid, 128, 0, st>>>(S, w, env_idx, level_idx, keys, count);
 }
 
 // initial reset: world w was generated straight into env w's maps

@@ -796,28 +796,32 @@ __global__ void __launch_bounds__(WG_THREADS, 8) k_worldgen(WorldJob job) {
     // floor-major order: CTAs resident at the same time run the same floor
     // generator, which keeps the instruction cache warm (no_instructions
     // stalls dominated a world-major order)
-    const int64_t w = it % nworlds;
     const int f = (int)(it / nworlds);
+    const int64_t w = (it % nworlds) + (job.mode == 2 ? job.first : 0);   // output slot
     uint64_t seed, key;
     if (job.mode == 0) {
       seed = hash2(job.env_key, hash2((uint64_t)(job.env_offset + w), 0));
       key = hash2(seed, hash2(1, 0));
-    } else {
+    } else if (job.mode == 1) {
       const int64_t slot = ((int64_t)job.info->offset + w) % job.M;
       seed = hash2(job.info->step_key, (uint64_t)slot);
       key = hash2(job.info->step_key, (1ull << 32) + (uint64_t)slot);
+    } else {
+      seed = job.params.seed[w];
+      key = 0;   // levels get their install key when installed
     }
     WMeta* meta = job.out.meta + w;
-    // make_level_params (worldgen.py:75-87)
+    // make_level_params (worldgen.py:75-87), or the explicit params
     const uint64_t base = mix64(seed);
-    const uint64_t fseed = hash2(base, hash2(100 + (uint64_t)f, 0));
+    const uint64_t fseed = job.mode == 2 ? job.params.floor_seed[w * 9 + f] : hash2(base, hash2(100 + (uint64_t)f, 0));
     bool fragile = false;
     FloorOut fo{-1, -1, -1};
     int attempt = 0;
     bool ok = false;
     if (f == 0) {
       const uint64_t k1 = hash2(base, hash2(1, 0));
-      for (int k = threadIdx.x; k < 252; k += WG_THREADS) sm.ang[k] = angle_of(u64d(k1, (uint64_t)k));
+      for (int k = threadIdx.x; k < 252; k += WG_THREADS)
+        sm.ang[k] = job.mode == 2 ? job.params.angles[w * 252 + k] : angle_of(u64d(k1, (uint64_t)k));
       __syncthreads();
       overworld_gradients<EXT>(sm);
       for (attempt = 0; attempt < 16 && !ok; ++attempt) {
@@ -891,12 +895,27 @@ __global__ void __launch_bounds__(WG_THREADS, 8) k_worldgen(WorldJob job) {
   }
 }
 
+// make_level_params (worldgen.py:75-87): 252 angles f32(u * 2 pi) from
+// split(make_stream(seed), 1) and the floor seeds split(base, 100 + f).key
+__global__ void k_level_params(LevelParamsBuf p, int64_t first, int64_t count) {
+  const int64_t l = first + blockIdx.x;
+  if (blockIdx.x >= count) return;
+  const uint64_t base = mix64(p.seed[l]);
+  const uint64_t k1 = hash2(base, hash2(1, 0));
+  for (int k = threadIdx.x; k < 252; k += blockDim.x) p.angles[l * 252 + k] = angle_of(u64d(k1, (uint64_t)k));
+  for (int f = threadIdx.x; f < 9; f += blockDim.x) p.floor_seed[l * 9 + f] = hash2(base, hash2(100 + (uint64_t)f, 0));
+}
+
+void launch_level_params(const LevelParamsBuf& p, int64_t first, int64_t count, cudaStream_t st) {
+  if (count > 0) k_level_params<<<(unsigned)count, 128, 0, st>>>(p, first, count);
+}
+
 void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st) {
   // persistent grid: CTAs walk the (world, floor) items
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t max_items = (j.mode == 0 ? j.count : j.out.cap) * (ext ? 9 : 1);
+  int64_t max_items = (j.mode == 1 ? j.out.cap : j.count) * (ext ? 9 : 1);
   int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * (j.ctas_per_sm > 0 ? j.ctas_per_sm : 8));
   if (grid <= 0) return;
   if (ext) k_worldgen<true><<<grid, WG_THREADS, 0, st>>>(j);

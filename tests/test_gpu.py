@@ -362,3 +362,55 @@ def test_batch_checkpoint_resume_is_exact(torch_cuda, tier):
     ra, la = a.episode_progress()
     rb, lb = b.episode_progress()
     assert np.array_equal(la, lb) and np.array_equal(ra, rb)
+
+
+def _ued():
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "ued_levels.npz"))
+
+
+@pytest.mark.parametrize("tag", ["classic_3", "classic_1001", "extended_5", "extended_77", "extended_2024"])
+def test_ued_levels_match_reference(torch_cuda, tag):
+    """make_level_params -> mutate_noise -> generate_world -> mutate_swap / mutate_rswap
+    -> install_world on the device equal the reference (tests/golden/make_mutate_golden.py)."""
+    from paper_2402_16801_b200 import GridrogueBatch, rng
+    from paper_2402_16801_b200.levels import LevelBuffer
+    from paper_2402_16801_b200.layout import field_shapes
+    g = _ued()
+    tier, seed = tag.split("_")[0], int(tag.split("_")[1])
+    gb = GridrogueBatch(4, tier, 0, "symbolic")
+    gb.reset()
+    lv = LevelBuffer(gb, 3)
+    lv.set_params(0, [seed, seed, seed])
+    s, a, f = lv.params(0, 3)
+    assert np.array_equal(a[0].view(np.uint32), g[f"{tag}_params_angles"].view(np.uint32))
+    assert np.array_equal(f[0], g[f"{tag}_params_floor_seeds"])
+    lv.mutate("noise", [0, 1, 2], [rng.make_stream(seed + 1)] * 3)
+    s, a, f = lv.params(0, 3)
+    for k in range(3):
+        assert np.array_equal(a[k].view(np.uint32), g[f"{tag}_noisy_angles"].view(np.uint32))
+        assert np.array_equal(f[k], g[f"{tag}_noisy_floor_seeds"]) and s[k] == g[f"{tag}_noisy_seed"]
+    lv.generate(0, 3)
+
+    def same_world(w, pre):
+        assert np.array_equal(w["blocks"], g[f"{pre}_blocks"])
+        assert np.array_equal(w["items"], g[f"{pre}_items"])
+        assert np.array_equal(w["spawn"], g[f"{pre}_spawn"])
+        assert np.array_equal(w["ladders"], g[f"{pre}_ladders"])
+        assert np.array_equal(w["chests"], g[f"{pre}_chests"])
+        assert np.array_equal(w["potion"], g[f"{pre}_potion"])
+
+    same_world(lv.world(0), f"{tag}_world")
+    lv.mutate("swap", [1], [rng.make_stream(seed + 2)])
+    same_world(lv.world(1), f"{tag}_swap")
+    lv.mutate("rswap", [2], [rng.make_stream(seed + 3)])
+    same_world(lv.world(2), f"{tag}_rswap")
+    key = int(g[f"{tag}_install_key"])
+    assert key == rng.split(rng.make_stream(seed + 4), 0).key
+    lv.install([2], [2], [key])
+    st = gb.export_state()
+    for name, (dt, shape) in field_shapes(tier, 1).items():
+        assert np.array_equal(st[name][2:3], g[f"{tag}_state_{name}"]), name
+    # the installed env steps and renders like any other
+    gb.set_validate(False)
+    gb.random_actions(0, 0)
+    gb.step(gb.actions)
