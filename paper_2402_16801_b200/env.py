@@ -129,10 +129,13 @@ class GridrogueBatch:
     def step(self, actions=None):
         """Device step; returns (obs, reward, done, newly, time, floor) tensors."""
         a = self.actions if actions is None else actions
-        if a.dtype != self.torch.int64 or a.device != self.device or not a.is_contiguous():
-            a = a.to(device=self.device, dtype=self.torch.int64).contiguous()
         if tuple(a.shape) != (self.n,):
             raise ValueError(f"actions must have shape ({self.n},), got {tuple(a.shape)}")
+        if a is not self.actions:
+            # one stable action buffer: the library replays a captured step
+            # graph per set of buffer addresses
+            self.actions.copy_(a)
+            a = self.actions
         check(lib().gr_step(self.h, _ptr(a), self._obs_ptr(), _ptr(self.reward), _ptr(self.done),
                             _ptr(self.newly), _ptr(self.time), _ptr(self.floor), self._stream()))
         return self.obs, self.reward, self.done, self.newly, self.time, self.floor

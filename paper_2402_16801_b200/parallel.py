@@ -62,6 +62,9 @@ class ShardedBatch:
 
     def step(self, actions=None):
         a = self.batch.actions if actions is None else actions
+        if a is not self.batch.actions:
+            self.batch.actions.copy_(a)   # int64, on this rank's device
+            a = self.batch.actions
         self.batch.step_local(a, self.ex)
         self.dist.all_gather_into_tensor(self.ex_all, self.ex, group=self.group)
         return self.batch.step_finish(self.ex_all, self.rank, self.world)

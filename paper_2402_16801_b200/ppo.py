@@ -1,0 +1,249 @@
+"""PPO on the device batch engine: the caller of the hot path.
+
+Craftax-1B's PPO (PAPER.md, "Hyperparameter Tuning", Craftax-1B table):
+1024 env workers, 64 steps per rollout, 8 minibatches, 4 update epochs,
+MLP layer size 512 with tanh, learning rate 2e-4 linearly annealed, gamma
+0.99, GAE lambda 0.8, clip 0.2, value coefficient 0.5, entropy coefficient
+0.01.  Actor and critic are separate 3-hidden-layer MLPs (orthogonal init,
+gain sqrt 2; 0.01 on the policy head, 1 on the value head), Adam (eps 1e-5),
+global gradient-norm clip 0.5 -- the purejaxrl recipe the paper builds on.
+The reference ships no learner, so there is nothing to match
+bit for bit; tests check the advantage estimator against a plain loop and
+that a short run learns (tests/test_ppo_cpu.py, tests/test_gpu.py).
+
+Everything stays on the GPU: observations are written by the CUDA writer
+straight into the rollout buffer the policy reads; actions go back as a
+device tensor.  Multi-GPU: one process per GPU (torchrun), each with its own
+shard of the global batch (parallel.ShardedBatch, so pools and resets match
+one global batch), gradients all-reduced over NCCL by DDP.
+
+    python -m paper_2402_16801_b200.ppo --total-timesteps 20000000
+    torchrun --nproc-per-node 8 -m paper_2402_16801_b200.ppo --total-timesteps 1000000000
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+from dataclasses import asdict, dataclass
+
+import numpy as np
+
+
+@dataclass
+class PPOConfig:
+    tier: str = "extended"
+    n_envs: int = 1024            # per GPU
+    n_steps: int = 64
+    n_minibatches: int = 8
+    update_epochs: int = 4
+    layer_size: int = 512
+    lr: float = 2e-4
+    anneal_lr: bool = True
+    gamma: float = 0.99
+    gae_lambda: float = 0.8
+    clip_eps: float = 0.2
+    vf_coef: float = 0.5
+    ent_coef: float = 0.01
+    max_grad_norm: float = 0.5
+    total_timesteps: int = 1_000_000_000
+    seed: int = 0
+    bf16: bool = True             # autocast the MLPs to bf16 (tensor cores)
+
+
+def gae(rewards, values, dones, last_value, gamma: float, lam: float):
+    """Generalized advantage estimation over a [T, N] rollout.
+
+    dones[t] marks that the episode ended at step t (the env auto-reset), so
+    value[t + 1] belongs to a new episode and is not bootstrapped.
+    """
+    import torch
+    T = rewards.shape[0]
+    adv = torch.zeros_like(rewards)
+    last = torch.zeros_like(last_value)
+    for t in range(T - 1, -1, -1):
+        nxt = last_value if t == T - 1 else values[t + 1]
+        nonterm = 1.0 - dones[t]
+        delta = rewards[t] + gamma * nxt * nonterm - values[t]
+        last = delta + gamma * lam * nonterm * last
+        adv[t] = last
+    return adv, adv + values
+
+
+def _mlp(nn, sizes, out, out_gain):
+    layers = []
+    for a, b in zip(sizes[:-1], sizes[1:]):
+        lin = nn.Linear(a, b)
+        nn.init.orthogonal_(lin.weight, math.sqrt(2))
+        nn.init.zeros_(lin.bias)
+        layers += [lin, nn.Tanh()]
+    head = nn.Linear(sizes[-1], out)
+    nn.init.orthogonal_(head.weight, out_gain)
+    nn.init.zeros_(head.bias)
+    return nn.Sequential(*layers, head)
+
+
+def make_model(obs_dim: int, n_actions: int, layer: int):
+    import torch.nn as nn
+
+    class ActorCritic(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.actor = _mlp(nn, [obs_dim, layer, layer, layer], n_actions, 0.01)
+            self.critic = _mlp(nn, [obs_dim, layer, layer, layer], 1, 1.0)
+
+        def forward(self, x):
+            return self.actor(x), self.critic(x).squeeze(-1)
+
+    return ActorCritic()
+
+
+def train(cfg: PPOConfig, log=print, max_updates: int | None = None) -> dict:
+    import torch
+    import torch.distributed as dist
+    from .env import TIERS, GridrogueBatch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=dev)
+    torch.manual_seed(cfg.seed + rank)
+
+    n, T = cfg.n_envs, cfg.n_steps
+    if world > 1:
+        from .parallel import ShardedBatch
+        env = ShardedBatch(n * world, cfg.tier, cfg.seed, "symbolic")
+        gb = env.batch
+    else:
+        env = gb = GridrogueBatch(n, cfg.tier, cfg.seed, "symbolic", newly=False, info=False)
+    gb.set_validate(False)   # actions are sampled in range
+    t_info = TIERS[cfg.tier]
+    obs_dim, n_actions = t_info["obs"], t_info["n_actions"]
+
+    model = make_model(obs_dim, n_actions, cfg.layer_size).to(dev)
+    if world > 1:
+        model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local])
+    opt = torch.optim.Adam(model.parameters(), lr=cfg.lr, eps=1e-5)
+    batch_size = n * T
+    n_updates = max(1, cfg.total_timesteps // (batch_size * world))
+    if max_updates is not None:
+        n_updates = min(n_updates, max_updates)
+    mb = batch_size // cfg.n_minibatches
+
+    buf_obs = torch.empty((T, n, obs_dim), dtype=torch.float32, device=dev)
+    buf_act = torch.empty((T, n), dtype=torch.int64, device=dev)
+    buf_logp = torch.empty((T, n), dtype=torch.float32, device=dev)
+    buf_val = torch.empty((T, n), dtype=torch.float32, device=dev)
+    buf_rew = torch.empty((T, n), dtype=torch.float32, device=dev)
+    buf_done = torch.empty((T, n), dtype=torch.float32, device=dev)
+
+    def policy(x):
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.bf16):
+            logits, v = model(x)
+        return logits.float(), v.float()
+
+    obs = env.reset().clone()
+    history = []
+    last_ep, last_ret = 0, 0.0
+    t0 = time.perf_counter()
+    steps_done = 0
+    for upd in range(n_updates):
+        if cfg.anneal_lr:
+            for g in opt.param_groups:
+                g["lr"] = cfg.lr * (1.0 - upd / n_updates)
+        # --- rollout: the env writes obs straight into the buffer row -------
+        with torch.no_grad():
+            for t in range(T):
+                buf_obs[t].copy_(obs)
+                logits, v = policy(obs)
+                dist_ = torch.distributions.Categorical(logits=logits)
+                a = dist_.sample()
+                buf_act[t] = a
+                buf_logp[t] = dist_.log_prob(a)
+                buf_val[t] = v
+                out = env.step(a)
+                obs, rew, done = out[0], out[1], out[2]
+                buf_rew[t] = rew
+                buf_done[t] = done.float()
+            _, last_v = policy(obs)
+            adv, ret = gae(buf_rew, buf_val, buf_done, last_v, cfg.gamma, cfg.gae_lambda)
+        obs = obs.clone()   # the env overwrites its obs tensor in place next step
+        # --- update ----------------------------------------------------------
+        b_obs = buf_obs.reshape(batch_size, obs_dim)
+        b_act, b_logp = buf_act.reshape(-1), buf_logp.reshape(-1)
+        b_adv, b_ret, b_val = adv.reshape(-1), ret.reshape(-1), buf_val.reshape(-1)
+        stats = []
+        for _ in range(cfg.update_epochs):
+            perm = torch.randperm(batch_size, device=dev)
+            for k in range(cfg.n_minibatches):
+                idx = perm[k * mb:(k + 1) * mb]
+                logits, v = policy(b_obs[idx])
+                d = torch.distributions.Categorical(logits=logits)
+                logp = d.log_prob(b_act[idx])
+                ratio = torch.exp(logp - b_logp[idx])
+                a_ = b_adv[idx]
+                a_ = (a_ - a_.mean()) / (a_.std() + 1e-8)
+                pg = -torch.min(ratio * a_, ratio.clamp(1 - cfg.clip_eps, 1 + cfg.clip_eps) * a_).mean()
+                v_clip = b_val[idx] + (v - b_val[idx]).clamp(-cfg.clip_eps, cfg.clip_eps)
+                vl = 0.5 * torch.max((v - b_ret[idx]) ** 2, (v_clip - b_ret[idx]) ** 2).mean()
+                ent = d.entropy().mean()
+                loss = pg + cfg.vf_coef * vl - cfg.ent_coef * ent
+                opt.zero_grad(set_to_none=True)
+                loss.backward()
+                torch.nn.utils.clip_grad_norm_(model.parameters(), cfg.max_grad_norm)
+                opt.step()
+                stats.append(torch.stack([loss.detach(), pg.detach(), vl.detach(), ent.detach()]))
+        steps_done += batch_size * world
+        if upd % 10 == 0 or upd == n_updates - 1:
+            torch.cuda.synchronize()
+            s = torch.stack(stats).mean(0).tolist()
+            st = gb.stats()
+            mean_ret = st["total_return"] / max(st["episodes"], 1)
+            window = (st["total_return"] - last_ret) / max(st["episodes"] - last_ep, 1)
+            last_ep, last_ret = st["episodes"], st["total_return"]
+            row = {"update": upd, "env_steps": steps_done, "sps": round(steps_done / (time.perf_counter() - t0), 1),
+                   "loss": s[0], "pg_loss": s[1], "v_loss": s[2], "entropy": s[3],
+                   "episodes": st["episodes"], "mean_episode_return": mean_ret,
+                   "recent_episode_return": window}
+            history.append(row)
+            if rank == 0:
+                log(json.dumps(row))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    st = gb.stats()
+    result = {"config": asdict(cfg), "n_gpus": world, "updates": n_updates, "env_steps": steps_done,
+              "seconds": round(dt, 3), "sps": round(steps_done / dt, 1), "episodes_rank0": st["episodes"],
+              "mean_episode_return_rank0": st["total_return"] / max(st["episodes"], 1), "history": history}
+    return result
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description="PPO (Craftax-1B hyper-parameters) on the B200 batch engine")
+    for k, v in asdict(PPOConfig()).items():
+        if isinstance(v, bool):
+            ap.add_argument(f"--{k.replace('_', '-')}", type=lambda s: s.lower() in ("1", "true", "yes"), default=v)
+        else:
+            ap.add_argument(f"--{k.replace('_', '-')}", type=type(v), default=v)
+    ap.add_argument("--max-updates", type=int, default=None)
+    ap.add_argument("--out", default=None, help="write the result JSON here")
+    args = ap.parse_args(argv)
+    kw = {k: getattr(args, k) for k in asdict(PPOConfig())}
+    res = train(PPOConfig(**kw), log=lambda s: print(s, file=sys.stderr, flush=True), max_updates=args.max_updates)
+    if int(os.environ.get("RANK", "0")) == 0:
+        txt = json.dumps({k: v for k, v in res.items() if k != "history"})
+        print(txt, flush=True)
+        if args.out:
+            with open(args.out, "w") as fh:
+                json.dump(res, fh, indent=1)
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

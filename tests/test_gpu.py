@@ -414,3 +414,14 @@ def test_ued_levels_match_reference(torch_cuda, tag):
     gb.set_validate(False)
     gb.random_actions(0, 0)
     gb.step(gb.actions)
+
+
+def test_ppo_short_run(torch_cuda):
+    """A short PPO run on the device engine: finite losses, episodes complete, throughput reported."""
+    from paper_2402_16801_b200.ppo import PPOConfig, train
+    cfg = PPOConfig(tier="classic", n_envs=256, n_steps=32, total_timesteps=256 * 32 * 6)
+    res = train(cfg, log=lambda s: None)
+    assert res["updates"] == 6 and res["env_steps"] == 256 * 32 * 6
+    assert res["sps"] > 0
+    for row in res["history"]:
+        assert all(np.isfinite([row["loss"], row["pg_loss"], row["v_loss"], row["entropy"]]))
