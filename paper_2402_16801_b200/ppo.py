@@ -11,9 +11,10 @@ The reference ships no learner, so there is nothing to match
 bit for bit; tests check the advantage estimator against a plain loop and
 that a short run learns (tests/test_ppo_cpu.py, tests/test_gpu.py).
 
-Everything stays on the GPU: observations are written by the CUDA writer
-straight into the rollout buffer the policy reads; actions go back as a
-device tensor.  Multi-GPU: one process per GPU (torchrun), each with its own
+Everything stays on the GPU: the CUDA writer renders observations into the
+batch's device buffer, copied on the device into the rollout buffer (one
+stable set of buffer addresses keeps every env step a replay of the
+library's captured step graph); actions go back as a device tensor.  Multi-GPU: one process per GPU (torchrun), each with its own
 shard of the global batch (parallel.ShardedBatch, so pools and resets match
 one global batch), gradients all-reduced over NCCL by DDP.
 
@@ -158,7 +159,7 @@ def train(cfg: PPOConfig, log=print, max_updates: int | None = None) -> dict:
         if cfg.anneal_lr:
             for g in opt.param_groups:
                 g["lr"] = cfg.lr * (1.0 - upd / n_updates)
-        # --- rollout: the env writes obs straight into the buffer row -------
+        # --- rollout ---------------------------------------------------------
         with torch.no_grad():
             for t in range(T):
                 buf_obs[t].copy_(obs)
