@@ -201,11 +201,19 @@ def main():
 
     import numpy as np
     import torch
+    # GR_BENCH_BACKEND=gloo lets a dev run put several ranks on one GPU to
+    # exercise the multi-rank path; the measured configuration is NCCL, one GPU per rank
+    backend = os.environ.get("GR_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2402_16801_b200 import GridrogueBatch, ShardedBatch
     from paper_2402_16801_b200.policies import RandomPolicy

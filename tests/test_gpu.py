@@ -425,3 +425,53 @@ def test_ppo_short_run(torch_cuda):
     assert res["sps"] > 0
     for row in res["history"]:
         assert all(np.isfinite([row["loss"], row["pg_loss"], row["v_loss"], row["entropy"]]))
+
+
+def _two_rank_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import oracle as O
+        from paper_2402_16801_b200 import ShardedBatch
+        n = 96
+        sb = ShardedBatch(n, "extended", 17, "symbolic", max_episode_length=15)
+        sb.reset()
+        ob = O.OracleBatch("extended", n, 17, max_episode_length=15)
+        lo, hi = sb.lo, sb.hi
+        for k in range(40):
+            a = O.random_actions(17, k, n, 43)
+            obs, rew, done, *_ = sb.step(torch.from_numpy(a[lo:hi]).cuda())
+            r2, d2, _, _ = ob.step(a)
+            assert np.array_equal(rew.cpu().numpy(), r2[lo:hi].astype(np.float32)), f"reward step {k}"
+            assert np.array_equal(done.cpu().numpy().astype(bool), d2[lo:hi]), f"done step {k}"
+            assert np.array_equal(obs.cpu().numpy(), ob.state.encode_symbolic()[lo:hi]), f"obs step {k}"
+        st = sb.stats()
+        assert st["episodes"] == ob.stats()["episodes"] > 0
+        seeds = sb.batch.export_state()["params_seed"]
+        assert np.array_equal(seeds, ob.state.export_fields()["params_seed"][lo:hi])
+        q.put((rank, "ok"))
+        dist.destroy_process_group()
+    except Exception as ex:   # reported to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+def test_sharded_batch_two_ranks_one_gpu(torch_cuda):
+    """Two ranks (two processes, gloo exchange) on one GPU: each shard equals the
+    matching slice of one global batch -- pool slots by global done rank, the
+    batch-wide flags, per-rank worldgen of the consumed slots."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + (os.getpid() % 200)
+    ps = [ctx.Process(target=_two_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, msg in res:
+        assert msg == "ok", f"rank {rank}: {msg}"
