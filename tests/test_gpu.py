@@ -475,3 +475,34 @@ def test_sharded_batch_two_ranks_one_gpu(torch_cuda):
         p.join(timeout=60)
     for rank, msg in res:
         assert msg == "ok", f"rank {rank}: {msg}"
+
+
+@pytest.mark.parametrize("tier,obs_mode,n", [("classic", "symbolic", 32), ("extended", "symbolic", 32),
+                                             ("classic", "pixels", 16), ("extended", "pixels", 12)])
+def test_long_rollout_parity_10k(torch_cuda, oracle_lib, tier, obs_mode, n):
+    """10^4-step rollouts, every step's reward / done / observation
+    equal to the oracle's, the full SimState every 2,500 steps (episodes capped at
+    700 steps, so every env lives through many resets)."""
+    from paper_2402_16801_b200 import GridrogueBatch
+    O = oracle_lib
+    torch = torch_cuda
+    steps, seed, max_len = 10_000, 31, 700
+    gb = GridrogueBatch(n, tier, seed, obs_mode, max_len, newly=False, info=False)
+    gb.reset()
+    gb.set_validate(False)
+    ob = O.OracleBatch(tier, n, seed, max_episode_length=max_len, threads=8)
+    na = O.TIERS[tier]["NA"]
+    px = gb.tile_px
+    for k in range(steps):
+        a = O.random_actions(seed, k, n, na)
+        obs, rew, done, *_ = gb.step(torch.from_numpy(a).cuda())
+        r2, d2, _, _ = ob.step(a)
+        ref_obs = ob.state.encode_symbolic() if obs_mode == "symbolic" else ob.state.render_pixels(px)
+        assert torch.equal(rew.cpu(), torch.from_numpy(r2.astype(np.float32))), f"reward step {k}"
+        assert np.array_equal(done.cpu().numpy().astype(bool), d2), f"done step {k}"
+        assert torch.equal(obs, torch.from_numpy(ref_obs).cuda()), f"obs step {k}"
+        if (k + 1) % 2500 == 0:
+            _cmp_state(O, gb, ob.state, tier, n)
+    s1, s2 = gb.stats(), ob.stats()
+    assert s1["episodes"] == s2["episodes"] >= n * (steps // max_len)
+    assert np.array_equal(s1["ach_episodes"], s2["ach_episodes"])

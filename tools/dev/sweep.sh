@@ -3,5 +3,5 @@
 for cfg in "$@"; do
   envs=$(echo "$cfg" | tr ',' ' ')
   env $envs timeout 300 python bench.py --steps 300 --warmup 300 --e2e-steps 0 --no-cpu-baseline > gpurun_out/sw.json 2>/dev/null
-  echo -n "$cfg: "; python tests/_kt.py gpurun_out/sw.json
+  echo -n "$cfg: "; python tools/dev/kt.py gpurun_out/sw.json
 done
