@@ -48,12 +48,14 @@ SEED = 0
 STEP_BYTES = {("extended", "symbolic"): 34579, ("classic", "symbolic"): 6281,
               ("extended", "pixels"): 44407, ("classic", "pixels"): 12808,
               ("extended", "none"): 1507, ("classic", "none"): 901}
-# dominant kernel (the observation writer): bytes per env per launch =
-# obs row written + block/item view window read + ~64 B of player scalars
+# dominant kernel (the observation writer): bytes per env per launch.
+# symbolic: row written + block/item view window read + 64 B of the
+# descriptor; pixels (k_pixels, after k_pixprep): frame written + the 848 /
+# 560 B per-env scratch read
 OBS_KERNEL_BYTES = {("extended", "symbolic"): 33072 + 99 + 255 + 64,
                     ("classic", "symbolic"): 5380 + 63 + 64,
-                    ("extended", "pixels"): 42900 + 99 + 255 + 64,
-                    ("classic", "pixels"): 11907 + 63 + 64}
+                    ("extended", "pixels"): 42900 + 848,
+                    ("classic", "pixels"): 11907 + 560}
 
 
 def log(*a):

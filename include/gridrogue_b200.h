@@ -211,8 +211,9 @@ int gr_episodes_completed(gr_env *env, int64_t *out);         /* info["episodes_
 /* count of kernels this library launched since creation (bench evidence) */
 int64_t gr_kernel_launches(const gr_env *env);
 /* per-kernel device timing with CUDA events on the launching stream:
- * classes 0..8 = step, scan, info, worldgen, install, obs (envs not reset),
- * policy, other, obs_reset (envs reset this step) */
+ * classes 0..9 = step, scan, info, worldgen, install, obs (writer, envs not
+ * reset), policy, other, obs_reset (envs reset this step), obs_prep (the
+ * per-env pass before the writer) */
 int gr_set_profiling(gr_env *env, int32_t on);
 int gr_kernel_times(gr_env *env, double *ms, int64_t *counts, int32_t n_classes);
 /* worldgen diagnostics: [worlds generated, floors retried, template floors,

@@ -102,7 +102,8 @@ static int fail(int code, const char* fmt, ...) {
   } while (0)
 
 // per-kernel CUDA-event timing (gr_set_profiling / gr_kernel_times)
-enum { PK_STEP, PK_SCAN, PK_INFO, PK_WORLDGEN, PK_INSTALL, PK_OBS, PK_POLICY, PK_OTHER, PK_OBS_RESET, PK_N };
+enum { PK_STEP, PK_SCAN, PK_INFO, PK_WORLDGEN, PK_INSTALL, PK_OBS, PK_POLICY, PK_OTHER, PK_OBS_RESET, PK_OBS_PREP,
+       PK_N };
 
 struct Prof {
   bool on = false;
@@ -399,14 +400,15 @@ static int observe(gr_env* e, void* obs_dev, cudaStream_t st, bool recompute_fla
   ObsArgs oa{obs_dev, e->n, recompute_flags ? e->cur_flags : e->prev_flags, e->cfg.tile_px, e->last_done, sel,
              e->tma ? 1 : 0, sel == 1 ? e->obs_ctas_overlap : e->obs_ctas_solo, e->done_list, e->info,
              e->pix};
+  const bool pixels = e->cfg.obs_mode == GR_OBS_PIXELS;
+  if (pixels) {   // k_pixprep
+    PTimer t(e, sel == 2 ? PK_OBS_RESET : PK_OBS_PREP, st);
+    launch_pixprep(e->ext, e->S, oa, st);
+  }
   {
     PTimer t(e, sel == 2 ? PK_OBS_RESET : PK_OBS, st);
-    if (e->cfg.obs_mode == GR_OBS_SYMBOLIC) {
-      launch_symbolic(e->ext, e->S, oa, st);
-    } else {
-      launch_pixels(e->ext, e->S, oa, st);   // k_pixprep + k_pixels
-      e->launches++;
-    }
+    if (pixels) launch_pixels(e->ext, e->S, oa, st);
+    else launch_symbolic(e->ext, e->S, oa, st);
   }
   CK(cudaGetLastError());
   return GR_OK;

@@ -106,6 +106,7 @@ void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st);
 // make_level_params(seed) for params slots [first, first + count) (seeds already set)
 void launch_level_params(const LevelParamsBuf& p, int64_t first, int64_t count, cudaStream_t st);
 void launch_install(bool ext, const DS& S, const InstallArgs& a, int64_t grid_envs, cudaStream_t st);
+void launch_pixprep(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st);
 void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st);
 void launch_pixels(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st);
 

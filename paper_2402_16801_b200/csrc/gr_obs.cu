@@ -460,8 +460,7 @@ static void launch_pixels_px(const DS& S, const ObsArgs& a, int sms, cudaStream_
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pixels<EXT, PX>, 128, smem);
     if (per_sm < 1) per_sm = 1;
   }
-  // persistent grids: every CTA resident from the start
-  k_pixprep<EXT><<<(int)std::min<int64_t>((a.n + 3) / 4, (int64_t)sms * 16), 128, 0, st>>>(S, a);
+  // persistent grid: every CTA resident from the start (k_pixprep ran before, launch_pixprep)
   k_pixels<EXT, PX><<<(int)std::min<int64_t>(a.n, (int64_t)sms * per_sm), 128, smem, st>>>(S, a);
 }
 
@@ -661,6 +660,18 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
   }
   // bulk stores must complete before the CTA retires
   if (tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// the per-env pass before the pixel writer (k_pixprep); persistent grid,
+// 4 envs per CTA
+void launch_pixprep(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
+  if (a.n <= 0 || !a.pix) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>((a.n + 3) / 4, (int64_t)sms * 16);
+  if (ext) k_pixprep<true><<<grid, 128, 0, st>>>(S, a);
+  else k_pixprep<false><<<grid, 128, 0, st>>>(S, a);
 }
 
 void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {

@@ -253,7 +253,8 @@ class GridrogueBatch:
     def kernel_launches(self) -> int:
         return int(lib().gr_kernel_launches(self.h))
 
-    KERNEL_CLASSES = ("step", "scan", "info", "worldgen", "install", "obs", "policy", "other", "obs_reset")
+    KERNEL_CLASSES = ("step", "scan", "info", "worldgen", "install", "obs", "policy", "other", "obs_reset",
+                      "obs_prep")
 
     def set_profiling(self, on: bool) -> None:
         check(lib().gr_set_profiling(self.h, 1 if on else 0))
