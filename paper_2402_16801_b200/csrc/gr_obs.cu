@@ -105,6 +105,12 @@ struct PG {
 // lanes reading words 16 bytes apart (consecutive 16-byte chunks) hit
 // distinct shared-memory banks: logical byte B of a row sits at pix_off(B).
 __device__ __forceinline__ int pix_off(int B) { return B + ((B >> 7) << 2); }
+__device__ __forceinline__ int pix_word(int L) { return L + (L >> 5); }   // the same for word L
+// the 4 bytes at logical byte offset off >= 0 of a padded pattern row
+__device__ __forceinline__ uint32_t pat_word(const uint32_t* w, int off) {
+  const int L = off >> 2;
+  return __funnelshift_r(w[pix_word(L)], w[pix_word(L + 1)], (off & 3) * 8);
+}
 
 // The frame rows fall into a few classes that depend on the geometry only:
 // within a tile row, the rows outside / inside the inset squares, with or
@@ -269,8 +275,14 @@ __global__ void __launch_bounds__(128) k_pixprep(DS S, ObsArgs a) {
 //     meanwhile the next env's inputs (k_pixprep scratch) arrive in the
 //     other buffer by cp.async.  (4-byte words per lane measured slower:
 //     4x the loop overhead.)
+// threads per frame CTA: large frames stream faster with more (extended 10 px:
+// 128 -> 384 took the writer from 0.95 to 0.84 ms; 512+ slower), small
+// frames prefer 128 (classic 7 px: 384 was 10 % slower)
 template <bool EXT, int PX>
-__global__ void __launch_bounds__(128) k_pixels(DS S, ObsArgs a) {
+__host__ __device__ constexpr int pix_threads() { return PG<EXT, PX>::FB >= 32768 ? 384 : 128; }
+
+template <bool EXT, int PX>
+__global__ void __launch_bounds__(pix_threads<EXT, PX>()) k_pixels(DS S, ObsArgs a) {
   using O = OT<EXT>;
   using G = PG<EXT, PX>;
   constexpr int PW = pix_words<EXT>();
@@ -409,12 +421,23 @@ __global__ void __launch_bounds__(128) k_pixels(DS S, ObsArgs a) {
         const int64_t bnd = f0 + (int64_t)(q + 1) * G::RB;
         const int64_t c = bnd & ~(int64_t)15;
         if (c == bnd || c < c0 || c >= c1) continue;
-        const int b = (int)(c - f0);
+        // n bytes from the tail of row q, the rest from the head of row q + 1
+        const int b = (int)(c - f0), o = b - q * G::RB, n = G::RB - o;
+        const uint32_t* wa = reinterpret_cast<const uint32_t*>(pat + rowcls[q] * G::PS);
+        const uint32_t* wb = reinterpret_cast<const uint32_t*>(pat + rowcls[q + 1] * G::PS);
         uint32_t wv[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          wv[k] = byte_at(b + 4 * k) | byte_at(b + 4 * k + 1) << 8 | byte_at(b + 4 * k + 2) << 16 |
-                  byte_at(b + 4 * k + 3) << 24;
+        for (int k = 0; k < 4; ++k) {
+          const int m = n - 4 * k;   // bytes of word k from row q
+          if (m >= 4) {
+            wv[k] = pat_word(wa, o + 4 * k);
+          } else if (m <= 0) {
+            wv[k] = pat_word(wb, -m);
+          } else {
+            const uint32_t keep = 0xFFFFFFFFu >> (32 - 8 * m);
+            wv[k] = (pat_word(wa, o + 4 * k) & keep) | (wb[pix_word(0)] << (8 * m));
+          }
+        }
         *reinterpret_cast<uint4*>(out + c) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
       } else {
         const int r = q - (G::FH - 1);
@@ -438,10 +461,10 @@ __global__ void __launch_bounds__(128) k_pixels(DS S, ObsArgs a) {
         const int L = o >> 2, sh = (o & 3) * 8;
         uint32_t x[5];
 #pragma unroll
-        for (int k = 0; k < 5; ++k) x[k] = w[(L + k) + ((L + k) >> 5)];
-        *reinterpret_cast<uint4*>(out + c0 + 16 * (int64_t)q) =
-            make_uint4(__funnelshift_r(x[0], x[1], sh), __funnelshift_r(x[1], x[2], sh), __funnelshift_r(x[2], x[3], sh),
-                       __funnelshift_r(x[3], x[4], sh));
+        for (int k = 0; k < 5; ++k) x[k] = w[pix_word(L + k)];
+        const uint4 val = make_uint4(__funnelshift_r(x[0], x[1], sh), __funnelshift_r(x[1], x[2], sh),
+                                     __funnelshift_r(x[2], x[3], sh), __funnelshift_r(x[3], x[4], sh));
+        *reinterpret_cast<uint4*>(out + c0 + 16 * (int64_t)q) = val;
       }
     }
     if (warp == 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -457,11 +480,11 @@ static void launch_pixels_px(const DS& S, const ObsArgs& a, int sms, cudaStream_
   static int per_sm = 0;
   if (!per_sm) {
     cudaFuncSetAttribute(k_pixels<EXT, PX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pixels<EXT, PX>, 128, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pixels<EXT, PX>, pix_threads<EXT, PX>(), smem);
     if (per_sm < 1) per_sm = 1;
   }
   // persistent grid: every CTA resident from the start (k_pixprep ran before, launch_pixprep)
-  k_pixels<EXT, PX><<<(int)std::min<int64_t>(a.n, (int64_t)sms * per_sm), 128, smem, st>>>(S, a);
+  k_pixels<EXT, PX><<<(int)std::min<int64_t>(a.n, (int64_t)sms * per_sm), pix_threads<EXT, PX>(), smem, st>>>(S, a);
 }
 
 // ---------------------------------------------------- symbolic writer
