@@ -27,13 +27,17 @@
 
 namespace gr {
 
-constexpr int WG_THREADS = 128;
-constexpr int WG_WARPS = WG_THREADS / 32;
 constexpr double PI_D = 3.141592653589793;
 
 template <bool EXT>
 struct WT {
   static constexpr int H = EXT ? 48 : 64, W = H, HW = H * W, F = EXT ? 9 : 1;
+  // threads per (world, floor) CTA: the classic tier has one floor per world
+  // and few worlds per step, so its single floor gets more threads (classic
+  // 65,536 envs: 128 / 256 / 512 / 1024 threads -> 0.090 / 0.083 / 0.087 /
+  // 0.102 ms of worldgen per step)
+  static constexpr int THREADS = EXT ? 128 : 256, WARPS = THREADS / 32;
+  static constexpr int MINB = EXT ? 8 : 1024 / THREADS;   // resident CTAs the registers are fitted to
 };
 
 template <bool EXT>
@@ -46,10 +50,11 @@ struct WSmem {
   float prof[2][8][32];                   // [coarse/fine][a1..a4,b0..b3][i]
   double dprof[EXT ? 2 : 1][8][12];
   float ang[252];
-  float rf[WG_WARPS];
-  double rd[WG_WARPS];
+  static constexpr int NWARP = WT<EXT>::WARPS;
+  float rf[NWARP];
+  double rd[NWARP];
   int ri[32];
-  unsigned long long ru[WG_WARPS];
+  unsigned long long ru[NWARP];
   int res_i;
   unsigned long long res_u;
   int spawn;
@@ -74,7 +79,7 @@ __device__ __noinline__ int block_argmax_f(SM& sm, float v, int idx) {   // idx 
   if (threadIdx.x == 0) {
     float bv = sm.rf[0];
     int bi = sm.ri[0];
-    for (int k = 1; k < WG_WARPS; ++k) {
+    for (int k = 1; k < SM::NWARP; ++k) {
       int oi = sm.ri[k];
       float ov = sm.rf[k];
       if (oi != INT_MAX && (bi == INT_MAX || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
@@ -100,7 +105,7 @@ __device__ __noinline__ int block_argmax_d(SM& sm, double v, int idx) {
   if (threadIdx.x == 0) {
     double bv = sm.rd[0];
     int bi = sm.ri[0];
-    for (int k = 1; k < WG_WARPS; ++k) {
+    for (int k = 1; k < SM::NWARP; ++k) {
       int oi = sm.ri[k];
       double ov = sm.rd[k];
       if (oi != INT_MAX && (bi == INT_MAX || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
@@ -123,7 +128,7 @@ __device__ __noinline__ unsigned long long block_min_u64(SM& sm, unsigned long l
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long b = sm.ru[0];
-    for (int k = 1; k < WG_WARPS; ++k) b = sm.ru[k] < b ? sm.ru[k] : b;
+    for (int k = 1; k < SM::NWARP; ++k) b = sm.ru[k] < b ? sm.ru[k] : b;
     sm.res_u = b;
   }
   __syncthreads();
@@ -139,7 +144,7 @@ __device__ __noinline__ unsigned long long block_or_u64(SM& sm, unsigned long lo
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long b = 0;
-    for (int k = 0; k < WG_WARPS; ++k) b |= sm.ru[k];
+    for (int k = 0; k < SM::NWARP; ++k) b |= sm.ru[k];
     sm.res_u = b;
   }
   __syncthreads();
@@ -160,7 +165,7 @@ __device__ __noinline__ int block_excl_scan(SM& sm, int v, int* total) {
   if (lane == 31) sm.ri[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    int w = lane < WG_WARPS ? sm.ri[lane] : 0;
+    int w = lane < SM::NWARP ? sm.ri[lane] : 0;
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += y;
@@ -169,7 +174,7 @@ __device__ __noinline__ int block_excl_scan(SM& sm, int v, int* total) {
   }
   __syncthreads();
   const int r = (warp ? sm.ri[warp - 1] : 0) + x - v;
-  *total = sm.ri[WG_WARPS - 1];
+  *total = sm.ri[SM::NWARP - 1];
   __syncthreads();
   return r;
 }
@@ -177,7 +182,7 @@ __device__ __noinline__ int block_excl_scan(SM& sm, int v, int* total) {
 template <bool EXT>
 __device__ __noinline__ unsigned long long census(WSmem<EXT>& sm) {
   unsigned long long m = 0;
-  for (int t = threadIdx.x; t < WT<EXT>::HW; t += WG_THREADS) m |= 1ull << sm.blk[t];
+  for (int t = threadIdx.x; t < WT<EXT>::HW; t += WT<EXT>::THREADS) m |= 1ull << sm.blk[t];
   return block_or_u64(sm, m);
 }
 
@@ -188,7 +193,7 @@ template <bool EXT, class P, class S>
 __device__ int pick(WSmem<EXT>& sm, P pred, S score) {
   float bv = 0.0f;
   int bi = INT_MAX;
-  for (int t = threadIdx.x; t < WT<EXT>::HW; t += WG_THREADS)
+  for (int t = threadIdx.x; t < WT<EXT>::HW; t += WT<EXT>::THREADS)
     if (pred(t)) {
       const float s = score(t);
       if (bi == INT_MAX || s > bv) { bv = s; bi = t; }
@@ -209,7 +214,7 @@ template <bool EXT>
 __device__ void build_profiles_f32(WSmem<EXT>& sm) {
   const int H = WT<EXT>::H;
   const int dims[2] = {H / 2, H / 8};
-  for (int k = threadIdx.x; k < 2 * 32; k += WG_THREADS) {
+  for (int k = threadIdx.x; k < 2 * 32; k += WT<EXT>::THREADS) {
     const int o = k / 32, i = k % 32, d = dims[o];
     if (i >= d) continue;
     float f = __fdiv_rn((float)i, (float)d);
@@ -290,7 +295,7 @@ __device__ bool ensure_f32(WSmem<EXT>& sm, uint8_t block, S hfun, bool low, int 
   const int sr = spawn >= 0 ? spawn / T::W : 0, sc = spawn >= 0 ? spawn % T::W : 0;
   auto near = [&](int t) { return spawn >= 0 && t != spawn && cheb(t / T::W, t % T::W, sr, sc) <= 8; };
   int any_near = 0, any_grass = 0;
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+  for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS) {
     any_grass |= sm.blk[t] == B_GRASS;
     any_near |= sm.blk[t] == B_GRASS && near(t);
   }
@@ -312,7 +317,7 @@ template <bool EXT>
 __device__ __noinline__ int nearest_walkable(WSmem<EXT>& sm) {
   using T = WT<EXT>;
   unsigned long long best = ~0ull;
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
+  for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS)
     if (in_set(WALK_SET, sm.blk[t])) {
       unsigned long long k = ((unsigned long long)cheb(t / T::W, t % T::W, T::H / 2, T::W / 2) << 32) | (unsigned)t;
       best = k < best ? k : best;
@@ -327,7 +332,7 @@ template <bool EXT>
 __device__ __noinline__ bool gen_overworld(WSmem<EXT>& sm, uint64_t seed0, bool extended, int attempt, int* ld) {
   using T = WT<EXT>;
   const UField u(hash2(seed0, (uint64_t)attempt), 1);
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+  for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS) {
     const int r = t / T::W, c = t % T::W;
     const float forest = octave_at<EXT>(sm, 1, sm.gx + 90, sm.gy + 90, 8, r, c);
     const float special = octave_at<EXT>(sm, 1, sm.gx + 171, sm.gy + 171, 8, r, c);
@@ -379,7 +384,7 @@ __device__ __noinline__ bool gen_overworld(WSmem<EXT>& sm, uint64_t seed0, bool 
 // gradients of the 252 angles in sm.ang (numpy float32 sin/cos)
 template <bool EXT>
 __device__ void overworld_gradients(WSmem<EXT>& sm) {
-  for (int k = threadIdx.x; k < 252; k += WG_THREADS) {
+  for (int k = threadIdx.x; k < 252; k += WT<EXT>::THREADS) {
     sm.gx[k] = np_sincosf(sm.ang[k], true);
     sm.gy[k] = np_sincosf(sm.ang[k], false);
   }
@@ -396,14 +401,14 @@ template <bool EXT>
 __device__ __noinline__ bool gen_realm(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo) {
   using T = WT<EXT>;
   const Stream s = Stream::raw(seed).split(3000 + (uint64_t)attempt);
-  for (int k = threadIdx.x; k < 252; k += WG_THREADS) sm.ang[k] = angle_of(s.at((uint64_t)k));
+  for (int k = threadIdx.x; k < 252; k += WT<EXT>::THREADS) sm.ang[k] = angle_of(s.at((uint64_t)k));
   __syncthreads();
   overworld_gradients<EXT>(sm);
   int ld_unused;
   if (!gen_overworld<EXT>(sm, hash2(seed, 4000 + (uint64_t)attempt), false, attempt, &ld_unused)) return false;
   const UField u(hash2(seed, 13 + (uint64_t)attempt), 6);
   const uint8_t gem = floor == 6 ? B_RUBY : B_SAPPHIRE;
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+  for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS) {
     uint8_t b = sm.blk[t], d = b;
     if (floor == 6) {
       if (b == B_GRASS) d = B_FIRE_GRASS; else if (b == B_TREE) d = B_FIRE_TREE;
@@ -433,7 +438,7 @@ __device__ __noinline__ bool gen_realm(WSmem<EXT>& sm, uint64_t seed, int floor,
     down = pick(sm, [&](int t) { return in_set(WALK_SET, sm.blk[t]); },
                 [&](int t) { return __fsub_rn(1.0f, u(t)); });
   if (down < 0 || down == spawn) return false;
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) sm.itm[t] = 0;
+  for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS) sm.itm[t] = 0;
   __syncthreads();
   if (threadIdx.x == 0) { sm.itm[spawn] = I_LADDER_UP; sm.itm[down] = I_LADDER_DOWN; }
   __syncthreads();
@@ -469,7 +474,7 @@ __device__ __noinline__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floo
     sm.room[k][0] = r0; sm.room[k][1] = r0 + rh; sm.room[k][2] = c0; sm.room[k][3] = c0 + rw;
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+  for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS) {
     const int r = t / T::W, c = t % T::W;
     bool in = false;
     for (int k = 0; k < n; ++k)
@@ -488,11 +493,11 @@ __device__ __noinline__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floo
   // moss / sewer water / vault gravel read the pre-pass PATH mask: compute
   // into registers first, write after the barrier
   const UField u(hash2(seed, 7 + (uint64_t)attempt), 4);
-  constexpr int PER = (T::HW + WG_THREADS - 1) / WG_THREADS;
+  constexpr int PER = (T::HW + WT<EXT>::THREADS - 1) / WT<EXT>::THREADS;
   uint8_t nb[PER];
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    const int t = threadIdx.x + q * WG_THREADS;
+    const int t = threadIdx.x + q * WT<EXT>::THREADS;
     if (t >= T::HW) break;
     const int r = t / T::W, c = t % T::W;
     const float uu = u(t);
@@ -509,7 +514,7 @@ __device__ __noinline__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floo
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    const int t = threadIdx.x + q * WG_THREADS;
+    const int t = threadIdx.x + q * WT<EXT>::THREADS;
     if (t < T::HW) sm.blk[t] = nb[q];
   }
   __syncthreads();
@@ -531,7 +536,7 @@ template <bool EXT>
 __device__ void build_profiles_f64(WSmem<EXT>& sm) {
   const int H = WT<EXT>::H;
   const int dims[2] = {H / 4, H / 8};
-  for (int k = threadIdx.x; k < 2 * 12; k += WG_THREADS) {
+  for (int k = threadIdx.x; k < 2 * 12; k += WT<EXT>::THREADS) {
     const int o = k / 12, i = k % 12, d = dims[o];
     if (i >= d) continue;
     double f = __ddiv_rn((double)i, (double)d);
@@ -579,7 +584,7 @@ template <bool EXT>
 __device__ __noinline__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo, bool* fragile) {
   using T = WT<EXT>;
   const Stream s = Stream::raw(seed).split(2000 + (uint64_t)attempt);
-  for (int k = threadIdx.x; k < 106; k += WG_THREADS) {
+  for (int k = threadIdx.x; k < 106; k += WT<EXT>::THREADS) {
     const float a = angle_of(s.at((uint64_t)k));
     double sn, cs;
     dd_sincos((double)a, &sn, &cs);
@@ -589,7 +594,7 @@ __device__ __noinline__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, 
   __syncthreads();
   const UField u(hash2(seed, 11 + (uint64_t)attempt), 5);
   int frag = 0;
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+  for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS) {
     const double field = cave_field_at<EXT>(sm, t);
     frag |= fabs(field + 0.02) < 1e-12 || fabs(field + 0.62) < 1e-12;
     const float uu = u(t);
@@ -623,7 +628,7 @@ __device__ __noinline__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, 
     if ((cen0 >> b) & 1ull) continue;
     double bv = 0.0;
     int bi = INT_MAX;
-    for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
+    for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS)
       if (sm.blk[t] == B_STONE) {
         const double sc = -cave_field_at<EXT>(sm, t);
         if (bi == INT_MAX || sc > bv) { bv = sc; bi = t; }
@@ -634,7 +639,7 @@ __device__ __noinline__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, 
     __syncthreads();
   }
   int cnt = 0;
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) cnt += sm.blk[t] == B_PATH;
+  for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS) cnt += sm.blk[t] == B_PATH;
   int total;
   block_excl_scan(sm, cnt, &total);
   if (total < 40) return false;
@@ -643,7 +648,7 @@ __device__ __noinline__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, 
   const int ur = up / T::W, uc = up % T::W;
   // argmax of chebyshev(up)/max over open tiles == argmax of the distance
   unsigned long long best = ~0ull;
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS)
+  for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS)
     if (sm.blk[t] == B_PATH) {
       unsigned long long k = ((unsigned long long)(1000 - cheb(t / T::W, t % T::W, ur, uc)) << 32) | (unsigned)t;
       best = k < best ? k : best;
@@ -668,7 +673,7 @@ template <bool EXT>
 __device__ __noinline__ void gen_graveyard(WSmem<EXT>& sm, FloorOut* fo) {
   using T = WT<EXT>;
   const int cr = T::H / 2, cc = T::W / 2;
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+  for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS) {
     const int r = t / T::W, c = t % T::W;
     uint8_t b = B_DARKNESS;
     if (r >= cr - 10 && r <= cr + 10 && c >= cc - 10 && c <= cc + 10) b = B_WALL;
@@ -698,7 +703,7 @@ template <bool EXT>
 __device__ __noinline__ void gen_template(WSmem<EXT>& sm, int floor, FloorOut* fo) {
   using T = WT<EXT>;
   const int H = T::H, W = T::W, cr = H / 2, cc = W / 2;
-  for (int t = threadIdx.x; t < T::HW; t += WG_THREADS) {
+  for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS) {
     const int r = t / W, c = t % W;
     uint8_t b = floor == 0 ? B_GRASS : B_PATH;
     if (floor != 0 && (r == 0 || r == H - 1 || c == 0 || c == W - 1)) b = B_WALL;
@@ -737,7 +742,7 @@ __device__ __noinline__ void assign_chests(WSmem<EXT>& sm, uint64_t world_seed, 
     return;
   }
   // the row-major list of PATH tiles (np.nonzero) via a block scan
-  constexpr int PER = (T::HW + WG_THREADS - 1) / WG_THREADS;
+  constexpr int PER = (T::HW + WT<EXT>::THREADS - 1) / WT<EXT>::THREADS;
   const int t0 = threadIdx.x * PER, t1 = min(t0 + PER, T::HW);
   int cnt = 0;
   for (int t = t0; t < t1; ++t) cnt += sm.blk[t] == B_PATH;
@@ -784,7 +789,7 @@ __device__ __noinline__ void assign_chests(WSmem<EXT>& sm, uint64_t world_seed, 
 }
 
 template <bool EXT>
-__global__ void __launch_bounds__(WG_THREADS, 8) k_worldgen(WorldJob job) {
+__global__ void __launch_bounds__(WT<EXT>::THREADS, WT<EXT>::MINB) k_worldgen(WorldJob job) {
   using T = WT<EXT>;
   __shared__ WSmem<EXT> sm;
   const int64_t nworlds = job.mode == 1 ? (int64_t)job.info->n_pool : job.count;
@@ -820,7 +825,7 @@ __global__ void __launch_bounds__(WG_THREADS, 8) k_worldgen(WorldJob job) {
     bool ok = false;
     if (f == 0) {
       const uint64_t k1 = hash2(base, hash2(1, 0));
-      for (int k = threadIdx.x; k < 252; k += WG_THREADS)
+      for (int k = threadIdx.x; k < 252; k += WT<EXT>::THREADS)
         sm.ang[k] = job.mode == 2 ? job.params.angles[w * 252 + k] : angle_of(u64d(k1, (uint64_t)k));
       __syncthreads();
       overworld_gradients<EXT>(sm);
@@ -851,7 +856,7 @@ __global__ void __launch_bounds__(WG_THREADS, 8) k_worldgen(WorldJob job) {
     // write the floor out (16-byte vectors)
     uint8_t* ob = job.out.blocks + ((size_t)w * T::F + f) * T::HW;
     uint8_t* oi = job.out.items + ((size_t)w * T::F + f) * T::HW;
-    for (int q = threadIdx.x; q < T::HW / 16; q += WG_THREADS) {
+    for (int q = threadIdx.x; q < T::HW / 16; q += WT<EXT>::THREADS) {
       reinterpret_cast<uint4*>(ob)[q] = reinterpret_cast<const uint4*>(sm.blk)[q];
       reinterpret_cast<uint4*>(oi)[q] = reinterpret_cast<const uint4*>(sm.itm)[q];
     }
@@ -916,10 +921,11 @@ void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int64_t max_items = (j.mode == 1 ? j.out.cap : j.count) * (ext ? 9 : 1);
-  int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * (j.ctas_per_sm > 0 ? j.ctas_per_sm : 8));
+  int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * (j.ctas_per_sm > 0 ? j.ctas_per_sm
+                                                                : ext ? WT<true>::MINB : WT<false>::MINB));
   if (grid <= 0) return;
-  if (ext) k_worldgen<true><<<grid, WG_THREADS, 0, st>>>(j);
-  else k_worldgen<false><<<grid, WG_THREADS, 0, st>>>(j);
+  if (ext) k_worldgen<true><<<grid, WT<true>::THREADS, 0, st>>>(j);
+  else k_worldgen<false><<<grid, WT<false>::THREADS, 0, st>>>(j);
 }
 
 }  // namespace gr
