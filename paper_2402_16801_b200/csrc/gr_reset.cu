@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(128) k_install_initial(DS S, WBuf wb, int64_t 
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) install_one<EXT>(S, i, wb.meta[i], nullptr, nullptr);
 }
 
-// done envs in ascending order: local rank = block offset (k_scan) + rank
+// done envs in ascending order: local rank = block offset (k_step's tail scan) + rank
 // inside the 128-env block (ballots)
 __global__ void __launch_bounds__(128) k_compact(const uint8_t* done, int64_t n, const int32_t* block_off,
                                                  int32_t* list) {

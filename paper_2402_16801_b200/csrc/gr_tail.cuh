@@ -1,9 +1,9 @@
 // gr_tail.cuh -- the per-step bookkeeping after the env update: exclusive
 // scan of the per-block done counts, the exchange record, and the combine
-// of the all-gathered records into StepInfo (batch.py:206-231).  Used by
-// the standalone kernels (k_scan, k_finish_info: multi-shard steps, where an
-// all-gather runs in between) and by the last CTA of k_step (one-shard
-// steps, so the bookkeeping costs no extra launches).
+// of the all-gathered records into StepInfo (batch.py:206-231).  The last
+// CTA of k_step runs the scan and writes the exchange record; the combine
+// runs there too for one-shard steps (no extra launches), or in
+// k_finish_info after the all-gather of a multi-shard step.
 #pragma once
 #include <cstdint>
 #include "gr_device.cuh"
