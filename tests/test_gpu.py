@@ -506,3 +506,36 @@ def test_long_rollout_parity_10k(torch_cuda, oracle_lib, tier, obs_mode, n):
     s1, s2 = gb.stats(), ob.stats()
     assert s1["episodes"] == s2["episodes"] >= n * (steps // max_len)
     assert np.array_equal(s1["ach_episodes"], s2["ach_episodes"])
+
+
+def test_batchenv_determinism_and_no_allocation_growth(torch_cuda):
+    """bindings/tests/test_bindings.py: two envs with one seed agree step for step;
+    stepping allocates nothing per step (host: tracemalloc; device: the CUDA
+    allocator and the library's captured step graphs)."""
+    import tracemalloc
+    from paper_2402_16801_b200 import BatchEnv
+    a, b = BatchEnv(8, tier="classic", seed=5), BatchEnv(8, tier="classic", seed=5)
+    a.reset(); b.reset()
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        acts = rng.integers(0, 17, size=8)
+        oa, ra, da, _ = a.step(acts)
+        ob, rb, db, _ = b.step(acts)
+        assert np.array_equal(ra, rb) and np.array_equal(da, db) and np.array_equal(oa, ob)
+    env = BatchEnv(16, tier="classic", seed=3, obs_mode="none")
+    env.reset()
+    acts = np.zeros(16, np.int64)
+    for _ in range(200):
+        env.step(acts)
+    torch_cuda.cuda.synchronize()
+    dev0 = torch_cuda.cuda.memory_allocated()
+    tracemalloc.start()
+    s0 = tracemalloc.take_snapshot()
+    for _ in range(400):
+        env.step(acts)
+    s1 = tracemalloc.take_snapshot()
+    tracemalloc.stop()
+    growth = sum(st.size_diff for st in s1.compare_to(s0, "filename") if st.size_diff > 0)
+    assert growth < 2_000_000
+    torch_cuda.cuda.synchronize()
+    assert torch_cuda.cuda.memory_allocated() == dev0
