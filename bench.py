@@ -116,8 +116,11 @@ class ClockSampler:
 
 
 def cpu_baseline(tier: str, obs: str, n_envs: int, budget_s: float = 15.0, tile_px=None,
-                 max_episode_length=None) -> dict:
-    """The oracle port on the host cores, bounded sample (BatchEnv semantics)."""
+                 max_episode_length=None, steps: int | None = None, warmup: int = 0) -> dict:
+    """The oracle port on the host cores (BatchEnv semantics): ``warmup``
+    untimed steps, then ``steps`` timed steps -- or, without ``steps``, as
+    many as fit in ``budget_s`` (a bounded sample); the timed loop also stops
+    at ``budget_s`` so a run always ends in minutes."""
     import numpy as np
     import oracle as O
     threads = os.cpu_count() or 1
@@ -126,31 +129,44 @@ def cpu_baseline(tier: str, obs: str, n_envs: int, budget_s: float = 15.0, tile_
     init_s = time.time() - t0
     na = O.TIERS[tier]["NA"]
     px = tile_px or (7 if tier == "classic" else 10)
-    steps = 0
-    t0 = time.time()
-    while True:
-        a = O.random_actions(SEED, steps, n_envs, na)
-        b.step(a)
+
+    def one(t):
+        b.step(O.random_actions(SEED, t, n_envs, na))
         if obs == "symbolic":
             b.state.encode_symbolic()
         elif obs == "pixels":
             b.state.render_pixels(px)
-        steps += 1
+
+    t = 0
+    for _ in range(warmup):
+        one(t)
+        t += 1
+    done = 0
+    t0 = time.time()
+    while steps is None or done < steps:
+        one(t)
+        t += 1
+        done += 1
         if time.time() - t0 > budget_s:
             break
     dt = time.time() - t0
-    return {"value": steps * n_envs / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{tier}/{obs}, {n_envs} envs x {steps} steps (time-capped {budget_s:.0f} s, "
-                      f"after a {init_s:.1f} s batch_reset), oracle/ C port, OpenMP over envs"}
+    cap = f"{done} of {steps} steps" if steps is not None else f"{done} steps (time-capped {budget_s:.0f} s)"
+    return {"value": done * n_envs / dt, "unit": UNIT, "cores": threads, "kind": "port", "steps": done,
+            "sample": f"{tier}/{obs}, {n_envs} envs x {cap} after {warmup} warm-up steps and a {init_s:.1f} s "
+                      f"batch_reset; oracle/ C port of the reference, OpenMP over envs"}
 
 
 def run_reference(args, world: int, rank: int):
     if rank != 0:
         return
-    budget = float(os.environ.get("GR_REF_BUDGET_S", "60"))
-    cb = cpu_baseline(args.tier, args.obs, args.envs, budget, args.tile_px, args.max_episode_length)
+    # the requested K steps after W warm-up steps, on all host cores; the
+    # timed loop stops early at GR_REF_BUDGET_S (default 180 s)
+    budget = float(os.environ.get("GR_REF_BUDGET_S", "180"))
+    cb = cpu_baseline(args.tier, args.obs, args.envs, budget, args.tile_px, args.max_episode_length,
+                      steps=args.steps, warmup=args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
-            "steps": None, "warmup": 0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "steps": cb["steps"], "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (procedural worlds, seed 0)",
             "config": workload_config(args, world),
             "cpu_baseline": cb,
