@@ -279,11 +279,16 @@ __device__ void load_env(Ctx& e, const DS& S) {
   e.visited = 0;
   e.cleared = 0;
   if (EXT) {
+    // accumulate in registers: 18 independent loads in flight, not 9 load ->
+    // local-store round trips
+    uint32_t vis = 0, clr = 0;
 #pragma unroll
     for (int f = 0; f < T::F; ++f) {
-      e.visited |= (uint16_t)(LD(GR_F_FLOORS_VISITED, uint8_t, f) ? 1u << f : 0u);
-      e.cleared |= (uint16_t)(LD(GR_F_FLOOR_CLEARED, uint8_t, f) ? 1u << f : 0u);
+      vis |= LD(GR_F_FLOORS_VISITED, uint8_t, f) ? 1u << f : 0u;
+      clr |= LD(GR_F_FLOOR_CLEARED, uint8_t, f) ? 1u << f : 0u;
     }
+    e.visited = (uint16_t)vis;
+    e.cleared = (uint16_t)clr;
     e.boss_hp = LD(GR_F_BOSS_HP, float, 0);
     e.boss_wave = LD(GR_F_BOSS_WAVE, uint8_t, 0);
     e.boss_vuln = LD(GR_F_BOSS_VULN, uint8_t, 0);
