@@ -26,8 +26,13 @@ struct OT {
 };
 
 
-__constant__ int8_t C_CLASSIC_LOCAL[37] = {0, 0, 1, 2, 3, 4, 0, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 0, 0,
-                                           0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+// obs._CLASSIC_BLOCK_LOCAL (obs.py:46-57): block id -> classic channel,
+// 4 bits per block packed in registers (lanes index it by their own tile's
+// block: a __constant__ table would serialise)
+__device__ __forceinline__ uint32_t classic_local(uint32_t b) {
+  const uint64_t w = b < 16 ? 0xdcba987650432100ull : b < 32 ? 0xeull : 0x0ull;
+  return (uint32_t)(w >> (4 * (b & 15))) & 15u;
+}
 
 // the window of env i's current floor: lane t (+32q) holds tile t's block and item
 template <bool EXT>
@@ -130,34 +135,37 @@ __device__ __forceinline__ int row_class(int y) {
   return OT<EXT>::VR * 4 + 5;
 }
 
-// the 12 bar fills (f64, rounded half-even like Python round)
+// the 12 bar fills (f64, rounded half-even like Python round): bar k is
+// computed by lane k of the warp, so the state loads and the float64
+// divisions of the 12 bars overlap instead of running one after another
 template <bool EXT>
-__device__ __forceinline__ void bar_fills(const DS& S, int64_t i, int px, int* fill) {
+__device__ __forceinline__ void bar_fills(const DS& S, int64_t i, int px, int* fill, int lane) {
   // vital bars (tiles.py:147-166) and gear panel (:169-186), float64
   using O = OT<EXT>;
+  if (lane >= (EXT ? 12 : 5)) return;
   const float str_ = (float)GR_AT(S, GR_F_STR, uint8_t, 0, i), dex = (float)GR_AT(S, GR_F_DEX, uint8_t, 0, i);
   const float intel = (float)GR_AT(S, GR_F_INTEL, uint8_t, 0, i);
-  const double hmax = (double)__fadd_rn(9.0f, str_), fmax = (double)__fadd_rn(12.0f, dex);
-  double st[5] = {(double)GR_AT(S, GR_F_HEALTH, float, 0, i) / hmax, (double)GR_AT(S, GR_F_FOOD, float, 0, i) / fmax,
-                  (double)GR_AT(S, GR_F_DRINK, float, 0, i) / fmax, (double)GR_AT(S, GR_F_ENERGY, float, 0, i) / fmax,
-                  EXT ? (double)GR_AT(S, GR_F_MANA, float, 0, i) / (double)__fadd_rn(16.0f, intel) : 0.0};
-  const int width = O::VC * px - 2;
-  for (int k = 0; k < 5; ++k) {
-    const double f = st[k] < 0.0 ? 0.0 : (st[k] > 1.0 ? 1.0 : st[k]);
-    fill[k] = (int)rint(__dmul_rn(f, (double)width));
+  double x;
+  int width;
+  if (lane < 5) {
+    if (lane == 0) x = (double)GR_AT(S, GR_F_HEALTH, float, 0, i) / (double)__fadd_rn(9.0f, str_);
+    else if (lane == 4) x = EXT ? (double)GR_AT(S, GR_F_MANA, float, 0, i) / (double)__fadd_rn(16.0f, intel) : 0.0;
+    else x = (double)GR_AT(S, lane == 1 ? GR_F_FOOD : lane == 2 ? GR_F_DRINK : GR_F_ENERGY, float, 0, i) /
+             (double)__fadd_rn(12.0f, dex);
+    width = O::VC * px - 2;
+  } else {
+    const int k = lane - 5;
+    if (k == 0) x = (double)GR_AT(S, GR_F_SWORD_TIER, uint8_t, 0, i) / 4.0;
+    else if (k == 1) x = (double)GR_AT(S, GR_F_PICK_TIER, uint8_t, 0, i) / 4.0;
+    else if (k == 2)
+      x = (double)(GR_AT(S, GR_F_ARMOUR, uint8_t, 0, i) + GR_AT(S, GR_F_ARMOUR, uint8_t, 1, i) +
+                   GR_AT(S, GR_F_ARMOUR, uint8_t, 2, i) + GR_AT(S, GR_F_ARMOUR, uint8_t, 3, i)) / 8.0;
+    else if (k == 3) x = (double)GR_AT(S, GR_F_XP, uint8_t, 0, i) / 8.0;
+    else x = (double)(k == 4 ? dex : k == 5 ? str_ : intel) / 5.0;
+    width = 2 * px - 2;
   }
-  if (EXT) {
-    const int arm = GR_AT(S, GR_F_ARMOUR, uint8_t, 0, i) + GR_AT(S, GR_F_ARMOUR, uint8_t, 1, i) +
-                    GR_AT(S, GR_F_ARMOUR, uint8_t, 2, i) + GR_AT(S, GR_F_ARMOUR, uint8_t, 3, i);
-    double gr[7] = {(double)GR_AT(S, GR_F_SWORD_TIER, uint8_t, 0, i) / 4.0,
-                    (double)GR_AT(S, GR_F_PICK_TIER, uint8_t, 0, i) / 4.0, (double)arm / 8.0,
-                    (double)GR_AT(S, GR_F_XP, uint8_t, 0, i) / 8.0, (double)dex / 5.0, (double)str_ / 5.0,
-                    (double)intel / 5.0};
-    for (int k = 0; k < 7; ++k) {
-      const double f = gr[k] < 0.0 ? 0.0 : (gr[k] > 1.0 ? 1.0 : gr[k]);
-      fill[5 + k] = (int)rint(__dmul_rn(f, (double)(2 * px - 2)));
-    }
-  }
+  const double f = x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x);
+  fill[lane] = (int)rint(__dmul_rn(f, (double)width));
 }
 
 // Per-env pixel inputs, written by k_pixprep into global scratch and read
@@ -177,7 +185,16 @@ __global__ void __launch_bounds__(128) k_pixprep(DS S, ObsArgs a) {
   constexpr int TQ = (O::T + 31) / 32;
   __shared__ float light_s[4][O::T];
   __shared__ uint8_t cre_s[4][O::T];
+  // colour tables in shared memory: lanes index them by their own tile's
+  // block / item, which a __constant__ table would serialise
+  __shared__ float pal[37][3];
+  __shared__ uint32_t itemc[5];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = threadIdx.x; k < 37 * 3; k += blockDim.x) pal[k / 3][k % 3] = (float)C_PALETTE[k / 3][k % 3];
+  if (threadIdx.x < 5)
+    itemc[threadIdx.x] = ((uint32_t)C_ITEMC[threadIdx.x][0] << 16) | ((uint32_t)C_ITEMC[threadIdx.x][1] << 8) |
+                         C_ITEMC[threadIdx.x][2];
+  __syncthreads();
   float* light = light_s[warp];
   uint8_t* cre = cre_s[warp];
   const int64_t count = a.sel == 2 ? (int64_t)a.info->k_local : a.n;
@@ -186,7 +203,7 @@ __global__ void __launch_bounds__(128) k_pixprep(DS S, ObsArgs a) {
     if (a.sel == 1 && a.done[i]) continue;                      // warp-uniform env filter
     const uint2 dw = reinterpret_cast<const uint2*>(S.desc + (size_t)i * DESC_WORDS)[lane];
     PixSmem<EXT>* dst = reinterpret_cast<PixSmem<EXT>*>(a.pix + (size_t)i * pix_words<EXT>());
-    if (lane == 0) bar_fills<EXT>(S, i, a.tile_px, dst->fill);   // independent loads, in flight meanwhile
+    bar_fills<EXT>(S, i, a.tile_px, dst->fill, lane);   // independent loads, in flight meanwhile
     const uint32_t pos = __shfl_sync(0xffffffffu, dw.y, D_POS / 2), fl = __shfl_sync(0xffffffffu, dw.x, D_FLAGS / 2);
     const float base = __uint_as_float(__shfl_sync(0xffffffffu, dw.x, D_BASE / 2));
     const int pr = (int16_t)(pos & 0xFFFF), pc = (int16_t)(pos >> 16), pf = fl & 0xFF;
@@ -246,12 +263,12 @@ __global__ void __launch_bounds__(128) k_pixprep(DS S, ObsArgs a) {
       uint32_t rgb = 0;
       if (!dark)
         for (int k = 0; k < 3; ++k)
-          rgb |= (uint32_t)(uint8_t)(int)__fmul_rn((float)C_PALETTE[b][k], sh) << (16 - 8 * k);
+          rgb |= (uint32_t)(uint8_t)(int)__fmul_rn(pal[b][k], sh) << (16 - 8 * k);
       dst->tile_rgb[t] = rgb;
       uint32_t ins = 0xFF000000u;
       if (!dark) {
         const int it = iq[q];
-        if (it) ins = ((uint32_t)C_ITEMC[it][0] << 16) | ((uint32_t)C_ITEMC[it][1] << 8) | C_ITEMC[it][2];
+        if (it) ins = itemc[it];
         if (cre[t]) ins = creature_rgb(EXT, cre[t]);
       }
       if (t == (O::VR / 2) * O::VC + O::VC / 2) ins = 0xFA3C3Cu;   // the player
@@ -609,7 +626,7 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
       if (t < O::T) {
         if (sleeping) v.light[t] = 0.0f;
         const bool lit = v.light[t] >= 0.05f;
-        const uint32_t bc = EXT ? bq[q] : (uint32_t)C_CLASSIC_LOCAL[bq[q]];
+        const uint32_t bc = EXT ? bq[q] : classic_local(bq[q]);
         const uint32_t ic = EXT ? (uint32_t)(O::BCH + iq[q]) : 0xFFu;
         v.tgt[t] = lit ? (bc | ic << 8 | (uint32_t)(O::BCH + O::ICH) << 16) : 0xFFFFFFu;
       }
