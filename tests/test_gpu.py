@@ -539,3 +539,26 @@ def test_batchenv_determinism_and_no_allocation_growth(torch_cuda):
     assert growth < 2_000_000
     torch_cuda.cuda.synchronize()
     assert torch_cuda.cuda.memory_allocated() == dev0
+
+
+@pytest.mark.parametrize("tier,obs_mode,n", [("classic", "symbolic", 1), ("extended", "symbolic", 1),
+                                             ("extended", "pixels", 3), ("classic", "pixels", 1),
+                                             ("extended", "symbolic", 129)])
+def test_tiny_and_ragged_batches(torch_cuda, oracle_lib, tier, obs_mode, n):
+    """Edge sizes: a single env, odd counts, one env past a 128-env block."""
+    from paper_2402_16801_b200 import GridrogueBatch
+    O = oracle_lib
+    torch = torch_cuda
+    gb = GridrogueBatch(n, tier, 44, obs_mode, 9)
+    obs = gb.reset()
+    ob = O.OracleBatch(tier, n, 44, max_episode_length=9)
+    px = gb.tile_px
+    ref = (lambda: ob.state.encode_symbolic()) if obs_mode == "symbolic" else (lambda: ob.state.render_pixels(px))
+    assert np.array_equal(obs.cpu().numpy(), ref())
+    for k in range(40):
+        a = O.random_actions(44, k, n, O.TIERS[tier]["NA"])
+        obs, rew, done, *_ = gb.step(torch.from_numpy(a).cuda())
+        r2, d2, _, _ = ob.step(a)
+        assert np.array_equal(rew.cpu().numpy(), r2.astype(np.float32)), f"reward step {k}"
+        assert np.array_equal(obs.cpu().numpy(), ref()), f"obs step {k}"
+    _cmp_state(O, gb, ob.state, tier, n)
