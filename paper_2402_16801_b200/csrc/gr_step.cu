@@ -42,48 +42,57 @@ struct TD {
   static constexpr int HW = H * W;
 };
 
-// per-env working copy: scalars + the active floor's creature lanes
+// per-env working copy: scalars + the active floor's creature lanes.  k_step
+// keeps one per thread in shared memory (Ctx-per-thread array, stride an odd
+// number of words: bank-conflict free); members sorted by size so the struct
+// packs with 4-byte alignment.  The env's map planes are at
+// s_blk_base / s_itm_base + i * F * H * W (CTA-wide bases, set by the kernel).
 struct Ctx {
-  int64_t i;
-  uint8_t* blk;   // this env's blocks [F][H][W]
-  uint8_t* itm;
-  uint8_t pfloor, facing, xp, dex, str_, intel, sword_tier, pick_tier, has_bow, sword_ench, bow_ench;
-  int16_t prow, pcol;
+  // 4-byte members
+  uint32_t i;
   float health, food, drink, energy, mana;
+  int lf;   // lanes of floor `lf`: class 0 melee (3), 1 ranged (2), 2 passive (3)
+  float lhp[8];
+  float ppdmg[3][3];
+  float epdmg[3][3];
+  uint32_t ach[3];
+  uint32_t time;
+  uint32_t key_lo;   // low word of rng_key: the only part the step uses (_kern.py:38-46)
+  float boss_hp;
+  uint32_t unlock[3];   // workspace (_kern.Workspace)
+  float health0;
+  uint32_t base;
+  // 2-byte members
+  int16_t prow, pcol;
+  int16_t lr[8], lc[8];
+  int16_t ppr[3], ppc[3];
+  int16_t epr[3], epc[3];
+  int16_t plr[10], plc[10];
+  uint16_t plage[10];
+  uint16_t visited, cleared;
+  uint16_t torch;     // floors that may hold a torch (DS.torch_bits)
+  uint16_t clocks[6];
+  int16_t nr, nc;     // necro_pos
+  // 1-byte members
+  uint8_t pfloor, facing, xp, dex, str_, intel, sword_tier, pick_tier, has_bow, sword_ench, bow_ench;
   uint8_t armour[4], armour_ench[4];
   uint8_t learned_fire, learned_ice, sleeping, resting;
   uint8_t inv_wood, inv_stone, inv_coal, inv_iron, inv_diamond, inv_sapphire, inv_ruby, inv_sapling,
       inv_torch, inv_arrow, inv_book;
   uint8_t inv_potion[6];
-  // lanes of floor `lf`: class 0 melee (3), 1 ranged (2), 2 passive (3)
-  int lf;
-  int16_t lr[8], lc[8];
-  float lhp[8];
   uint8_t lcd[8], lal[8], lty[8];
-  int16_t ppr[3], ppc[3];
   uint8_t ppdir[3], pptype[3], ppttl[3], ppal[3];
-  float ppdmg[3][3];
-  int16_t epr[3], epc[3];
   uint8_t epdir[3], eptype[3], epttl[3], epal[3];
-  float epdmg[3][3];
-  int16_t plr[10], plc[10];
-  uint16_t plage[10];
   uint8_t plal[10];
-  uint32_t ach[3];
-  uint32_t time;
-  uint64_t key;
-  uint16_t visited, cleared;
-  uint16_t torch;     // floors that may hold a torch (DS.torch_bits)
-  float boss_hp;
   uint8_t boss_wave, boss_vuln, boss_timer;
-  uint16_t clocks[6];
-  int16_t nr, nc;     // necro_pos
-  // workspace (_kern.Workspace)
-  uint32_t unlock[3];
   bool hurt;
-  float health0;
-  uint32_t base;
 };
+static_assert(alignof(Ctx) == 4, "Ctx packs at 4-byte alignment");
+static_assert((sizeof(Ctx) / 4) % 2 == 1, "Ctx stride must be an odd number of words (shared-memory banks)");
+
+// CTA-wide map plane bases (k_step / k_make_desc set them before any access)
+__shared__ uint8_t* s_blk_base;
+__shared__ uint8_t* s_itm_base;
 
 // lane slot layout inside Ctx: melee 0..2, ranged 3..4, passive 5..7
 __host__ __device__ constexpr int l0_of(int cls) { return cls == 0 ? 0 : cls == 1 ? 3 : 5; }
@@ -95,18 +104,18 @@ template <bool EXT>
 __device__ __forceinline__ uint8_t gblock(const Ctx& e, int f, int r, int c) {
   using T = TD<EXT>;
   if (r < 0 || r >= T::H || c < 0 || c >= T::W) return B_OOB;
-  return e.blk[f * T::HW + r * T::W + c];
+  return s_blk_base[(size_t)e.i * (T::F * T::HW) + f * T::HW + r * T::W + c];
 }
 template <bool EXT>
 __device__ __forceinline__ uint8_t gitem(const Ctx& e, int f, int r, int c) {
   using T = TD<EXT>;
   if (r < 0 || r >= T::H || c < 0 || c >= T::W) return 0;
-  return e.itm[f * T::HW + r * T::W + c];
+  return s_itm_base[(size_t)e.i * (T::F * T::HW) + f * T::HW + r * T::W + c];
 }
 template <bool EXT>
 __device__ __forceinline__ void sblock(Ctx& e, int f, int r, int c, uint8_t v) {
   using T = TD<EXT>;
-  e.blk[f * T::HW + r * T::W + c] = v;
+  s_blk_base[(size_t)e.i * (T::F * T::HW) + f * T::HW + r * T::W + c] = v;
 }
 
 template <bool EXT>
@@ -274,7 +283,7 @@ __device__ void load_env(Ctx& e, const DS& S) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) e.ach[k] = LD(GR_F_ACH, uint32_t, k);
   e.time = LD(GR_F_TIME, uint32_t, 0);
-  e.key = LD(GR_F_RNG_KEY, uint64_t, 0);
+  e.key_lo = (uint32_t)LD(GR_F_RNG_KEY, uint64_t, 0);
   e.torch = EXT ? S.torch_bits[i] : 0;
   e.visited = 0;
   e.cleared = 0;
@@ -571,7 +580,7 @@ __device__ void place_action(Ctx& e, int a, int af) {
       e.inv_sapling -= 1;
     }
   } else if (EXT && a == 28 && e.inv_torch > 0 && in_set(WALK_SET, tb)) {
-    e.itm[af * T::HW + tr * T::W + tc] = I_TORCH;
+    s_itm_base[(size_t)e.i * (T::F * T::HW) + af * T::HW + tr * T::W + tc] = I_TORCH;
     e.torch |= (uint16_t)(1u << af);
     e.inv_torch -= 1;
     award<EXT>(e, 24);
@@ -1185,11 +1194,14 @@ template <bool EXT>
 __global__ void __launch_bounds__(128) k_make_desc(DS S, int64_t n) {
   using T = TD<EXT>;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (threadIdx.x == 0) {
+    s_blk_base = (uint8_t*)S.f[GR_F_BLOCKS];
+    s_itm_base = (uint8_t*)S.f[GR_F_ITEMS];
+  }
+  __syncthreads();
   if (i >= n) return;
   Ctx e;
-  e.i = i;
-  e.blk = (uint8_t*)S.f[GR_F_BLOCKS] + (size_t)i * T::F * T::HW;
-  e.itm = (uint8_t*)S.f[GR_F_ITEMS] + (size_t)i * T::F * T::HW;
+  e.i = (uint32_t)i;
   load_env<EXT>(e, S);
   load_lanes<EXT>(e, S, e.pfloor);
   write_desc<EXT>(e, S.desc + (size_t)i * DESC_WORDS, S.lut);
@@ -1215,6 +1227,9 @@ __device__ __forceinline__ void apply_pending(Ctx& e, uint8_t pend, uint32_t pre
     if (ran && ((pend >> (3 + l)) & 1) && e.lcd[3 + l] > 0) e.lcd[3 + l] -= 1;
 }
 
+#ifndef GR_STEP_SMEM_CTX
+#define GR_STEP_SMEM_CTX 1   // per-thread working copy in shared memory (0: registers + local memory)
+#endif
 template <bool EXT>
 #ifndef GR_STEP_MINB
 #define GR_STEP_MINB 4   // resident CTAs per SM the register budget is fitted to (128 regs/thread)
@@ -1225,11 +1240,19 @@ __global__ void __launch_bounds__(128, GR_STEP_MINB) k_step(DS S, StepArgs a) {
   const bool valid = i < a.n && !(a.bad && a.bad[0] >= 0);
   uint32_t my_flags = 0;
   int my_done = 0;
+  if (threadIdx.x == 0) {
+    s_blk_base = (uint8_t*)S.f[GR_F_BLOCKS];
+    s_itm_base = (uint8_t*)S.f[GR_F_ITEMS];
+  }
+#if GR_STEP_SMEM_CTX
+  extern __shared__ __align__(16) unsigned char s_ctx_raw[];
+  Ctx& e = reinterpret_cast<Ctx*>(s_ctx_raw)[threadIdx.x];
+#else
+  Ctx e;
+#endif
+  __syncthreads();
   if (valid) {
-    Ctx e;
-    e.i = i;
-    e.blk = (uint8_t*)S.f[GR_F_BLOCKS] + (size_t)i * T::F * T::HW;
-    e.itm = (uint8_t*)S.f[GR_F_ITEMS] + (size_t)i * T::F * T::HW;
+    e.i = (uint32_t)i;
     load_env<EXT>(e, S);
     load_lanes<EXT>(e, S, e.pfloor);
     uint8_t pend = S.cd_pending[i];
@@ -1239,7 +1262,7 @@ __global__ void __launch_bounds__(128, GR_STEP_MINB) k_step(DS S, StepArgs a) {
     e.unlock[0] = e.unlock[1] = e.unlock[2] = 0;
     e.hurt = false;
     e.health0 = e.health;
-    e.base = mix32((uint32_t)(e.key & 0xFFFFFFFFull) ^ (e.time * 0x9E3779B9u));
+    e.base = mix32(e.key_lo ^ (e.time * 0x9E3779B9u));
     const int action = (int)a.actions[i];
     const int f0 = e.pfloor;
     player_actions<EXT>(e, S, action);
@@ -1342,8 +1365,19 @@ void launch_step(bool ext, const DS& S, const StepArgs& a, cudaStream_t st) {
   const int bs = 128;
   const int grid = (int)((a.n + bs - 1) / bs);
   if (grid == 0) return;
-  if (ext) k_step<true><<<grid, bs, 0, st>>>(S, a);
-  else k_step<false><<<grid, bs, 0, st>>>(S, a);
+#if GR_STEP_SMEM_CTX
+  const size_t smem = (size_t)bs * sizeof(Ctx);
+  static bool attr_set = false;   // idempotent; a race only repeats the call
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+#else
+  const size_t smem = 0;
+#endif
+  if (ext) k_step<true><<<grid, bs, smem, st>>>(S, a);
+  else k_step<false><<<grid, bs, smem, st>>>(S, a);
 }
 
 }  // namespace gr

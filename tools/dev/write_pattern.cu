@@ -108,6 +108,39 @@ __global__ void k_tma2(float* out) {
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+
+// G consecutive rows per CTA staged contiguously and drained by ONE bulk copy
+// (the SM's write front is one G*33 KB stream instead of G 33 KB streams);
+// NS stage sets, the wait deferred by NS-1 groups
+template <int G, int NS>
+__global__ void k_tma_grp(float* out, int pitch) {
+  extern __shared__ float4 sm[];
+  float* st = reinterpret_cast<float*>(sm);
+  for (int q = threadIdx.x; q < NS * G * L / 4; q += blockDim.x) reinterpret_cast<float4*>(st)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  int b = 0;
+  for (int64_t g = blockIdx.x; g * G < N; g += gridDim.x) {
+    if (threadIdx.x == 0) {
+      if (NS > 1) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NS - 1) : "memory");
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(st + b * G * L);
+      if (pitch == L) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + g * G * L), "r"(sa),
+                     "r"(G * L * 4) : "memory");
+      } else {
+        for (int k = 0; k < G; ++k)
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + (g * G + k) * (int64_t)pitch),
+                       "r"(sa + k * L * 4), "r"(L * 4) : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (NS == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    b = (b + 1) % NS;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <class F>
 float timeit(F f) {
   cudaEvent_t a, b;
@@ -172,6 +205,22 @@ int main() {
     char nm[64];
     snprintf(nm, 64, "tma2 (2 stages) 1w x %d CTA", ctas);
     rep(nm, timeit([&] { k_tma2<<<sms * ctas, 32, 2 * 8272 * 4>>>(out); }));
+  }
+  {
+    float* out2;
+    cudaMalloc(&out2, (size_t)N * 8320 * 4);
+#define GRP(G, NS, CT, P, O)                                                                              \
+    {                                                                                                     \
+      cudaFuncSetAttribute(k_tma_grp<G, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, NS * G * L * 4); \
+      char nm[64];                                                                                        \
+      snprintf(nm, 64, "tma_grp G%d NS%d %dCTA/SM pitch %d", G, NS, CT, P);                               \
+      rep(nm, timeit([&] { k_tma_grp<G, NS><<<sms * CT, 32, NS * G * L * 4>>>(O, P); }));                 \
+    }
+    GRP(1, 1, 4, L, out) GRP(1, 2, 3, L, out) GRP(2, 1, 2, L, out) GRP(2, 2, 1, L, out) GRP(3, 1, 2, L, out)
+    GRP(4, 1, 1, L, out) GRP(6, 1, 1, L, out) GRP(3, 2, 1, L, out)
+    GRP(1, 1, 4, 8320, out2) GRP(2, 1, 2, 8320, out2) GRP(4, 1, 1, 8320, out2)
+    GRP(1, 1, 4, 8320 - 8, out2) GRP(1, 1, 4, 8288, out2)
+    cudaFree(out2);
   }
   return 0;
 }
