@@ -94,6 +94,15 @@ static_assert((sizeof(Ctx) / 4) % 2 == 1, "Ctx stride must be an odd number of w
 __shared__ uint8_t* s_blk_base;
 __shared__ uint8_t* s_itm_base;
 
+// code-size knobs (dev A/B): GR_STEP_NI on the once-called phase / action
+// handlers, GR_STEP_NI2 on the many-call-site lane helpers
+#ifndef GR_STEP_NI
+#define GR_STEP_NI
+#endif
+#ifndef GR_STEP_NI2
+#define GR_STEP_NI2
+#endif
+
 // lane slot layout inside Ctx: melee 0..2, ranged 3..4, passive 5..7
 __host__ __device__ constexpr int l0_of(int cls) { return cls == 0 ? 0 : cls == 1 ? 3 : 5; }
 __host__ __device__ constexpr int cap_of(int cls) { return cls == 1 ? 2 : 3; }
@@ -424,7 +433,7 @@ __device__ __forceinline__ bool occupied(const Ctx& e, int r, int c) {
 // creatures.damage_creatures_at for one lane; `write` false reproduces the
 // extended tier's discarded act0 copy (engine.py:573, creatures.py:90-94)
 template <bool EXT>
-__device__ void damage_lane(Ctx& e, int s, const float d[3], bool write) {
+GR_STEP_NI __device__ void damage_lane(Ctx& e, int s, const float d[3], bool write) {
   int kind = e.lty[s];
   float dealt = resolve(d[0], d[1], d[2], C_DEF[kind][0], C_DEF[kind][1], C_DEF[kind][2]);
   float hp = q1(__fsub_rn(e.lhp[s], dealt));
@@ -445,7 +454,7 @@ __device__ void damage_lane(Ctx& e, int s, const float d[3], bool write) {
 
 // creatures._check_boss_death
 template <bool EXT>
-__device__ void check_boss_death(Ctx& e) {
+GR_STEP_NI __device__ void check_boss_death(Ctx& e) {
   if (!(e.boss_vuln && e.boss_hp <= 0.0f)) return;
   award<EXT>(e, 49);
   e.cleared |= 1u << 8;
@@ -455,7 +464,7 @@ __device__ void check_boss_death(Ctx& e) {
 
 // engine._open_chests (engine.py:240-272)
 template <bool EXT>
-__device__ void open_chest(Ctx& e, const DS& S, int af, int tr, int tc) {
+GR_STEP_NI __device__ void open_chest(Ctx& e, const DS& S, int af, int tr, int tc) {
   const int64_t i = e.i;
   int lane = -1;
   for (int j = 0; j < 6; ++j) {
@@ -488,7 +497,7 @@ __device__ void open_chest(Ctx& e, const DS& S, int af, int tr, int tc) {
 
 // engine._do_interact (engine.py:143-237)
 template <bool EXT>
-__device__ void do_interact(Ctx& e, const DS& S, int af) {
+GR_STEP_NI __device__ void do_interact(Ctx& e, const DS& S, int af) {
   int tr = e.prow + C_DIR[e.facing][0], tc = e.pcol + C_DIR[e.facing][1];
 #pragma unroll
   for (int cls = 0; cls < 3; ++cls) {
@@ -557,7 +566,7 @@ __device__ void do_interact(Ctx& e, const DS& S, int af) {
 
 // engine._place_actions (engine.py:275-336)
 template <bool EXT>
-__device__ void place_action(Ctx& e, int a, int af) {
+GR_STEP_NI __device__ void place_action(Ctx& e, int a, int af) {
   using T = TD<EXT>;
   int tr = e.prow + C_DIR[e.facing][0], tc = e.pcol + C_DIR[e.facing][1];
   uint8_t tb = gblock<EXT>(e, af, tr, tc);
@@ -589,7 +598,7 @@ __device__ void place_action(Ctx& e, int a, int af) {
 
 // engine._craft_actions (engine.py:346-457)
 template <bool EXT>
-__device__ void craft_action(Ctx& e, int a, int af) {
+GR_STEP_NI __device__ void craft_action(Ctx& e, int a, int af) {
   bool near_table = false, near_furnace = false, near_fire = false, near_ice = false;
 #pragma unroll
   for (int dr = -1; dr <= 1; ++dr)
@@ -684,7 +693,7 @@ __device__ __forceinline__ bool spawn_pproj(Ctx& e, int kind, float d0, float d1
 
 // engine._ladder_moves (engine.py:533-565)
 template <bool EXT>
-__device__ void ladder_move(Ctx& e, const DS& S, int a) {
+GR_STEP_NI __device__ void ladder_move(Ctx& e, const DS& S, int a) {
   using T = TD<EXT>;
   uint8_t here = gitem<EXT>(e, e.pfloor, e.prow, e.pcol);
   bool down = a == 18 && here == I_LADDER_DOWN && e.pfloor + 1 < T::F;
@@ -792,7 +801,7 @@ __device__ void player_actions(Ctx& e, const DS& S, int action) {
 
 // ---------------------------------------------------------- projectiles
 template <bool EXT>
-__device__ void advance_projectiles(Ctx& e) {
+GR_STEP_NI __device__ void advance_projectiles(Ctx& e) {
   const int af = e.pfloor;
   if (EXT) {
 #pragma unroll
@@ -863,7 +872,7 @@ __device__ __forceinline__ uint64_t walk_set_of(const Ctx& e, int s) {
 }
 
 template <bool EXT>
-__device__ void move_lane(Ctx& e, int s, int sr, int sc) {
+GR_STEP_NI2 __device__ void move_lane(Ctx& e, int s, int sr, int sc) {
   int tr = e.lr[s] + sr, tc = e.lc[s] + sc;
   if (in_set(walk_set_of<EXT>(e, s), gblock<EXT>(e, e.lf, tr, tc)) && !(tr == e.prow && tc == e.pcol)) {
     e.lr[s] = (int16_t)tr; e.lc[s] = (int16_t)tc;
@@ -871,7 +880,7 @@ __device__ void move_lane(Ctx& e, int s, int sr, int sc) {
 }
 
 template <bool EXT>
-__device__ void chase_move(Ctx& e, int s, int dr, int dc) {
+GR_STEP_NI2 __device__ void chase_move(Ctx& e, int s, int dr, int dc) {
   int sr = isgn(dr), sc = isgn(dc);
   bool row_first = abs(dr) >= abs(dc);
   int pr = row_first ? sr : 0, pc = row_first ? 0 : sc;
@@ -998,7 +1007,7 @@ __device__ void creatures_act(Ctx& e, uint8_t* pending) {
 
 // engine._survival_tick (engine.py:640-700)
 template <bool EXT>
-__device__ void survival_tick(Ctx& e) {
+GR_STEP_NI __device__ void survival_tick(Ctx& e) {
   const uint16_t dex = e.dex;
   const float hmax = health_max(e), fmax = food_max(e);
 #pragma unroll
@@ -1039,7 +1048,7 @@ __device__ void survival_tick(Ctx& e) {
 
 // creatures._spawn_class (creatures.py:387-423)
 template <bool EXT>
-__device__ void spawn_class(Ctx& e, int cls, int kind, double prob, int sub, uint8_t* pending) {
+GR_STEP_NI2 __device__ void spawn_class(Ctx& e, int cls, int kind, double prob, int sub, uint8_t* pending) {
   const int cap = LCAP(cls), s0 = L0(cls);
   int n_alive = 0;
   for (int l = 0; l < cap; ++l) n_alive += e.lal[s0 + l];
@@ -1070,7 +1079,7 @@ __device__ void spawn_class(Ctx& e, int cls, int kind, double prob, int sub, uin
 
 // creatures._spawn_wave (creatures.py:455-486); the active floor is 8
 template <bool EXT>
-__device__ void spawn_wave(Ctx& e, int wf, uint8_t* pending) {
+GR_STEP_NI __device__ void spawn_wave(Ctx& e, int wf, uint8_t* pending) {
   using T = TD<EXT>;
   uint8_t mk = (uint8_t)C_MEL_KIND[wf], rk = (uint8_t)C_RAN_KIND[wf];
 #pragma unroll
@@ -1089,7 +1098,7 @@ __device__ void spawn_wave(Ctx& e, int wf, uint8_t* pending) {
 
 // creatures._boss_logic (creatures.py:489-520)
 template <bool EXT>
-__device__ void boss_logic(Ctx& e, uint8_t* pending) {
+GR_STEP_NI __device__ void boss_logic(Ctx& e, uint8_t* pending) {
   if (!(e.pfloor == 8 && e.boss_hp > 0.0f)) return;
   int enemies = e.lal[0] + e.lal[1] + e.lal[2] + e.lal[3] + e.lal[4];
   if (enemies != 0) return;
@@ -1130,7 +1139,7 @@ __device__ void spawn_despawn(Ctx& e, uint8_t* pending) {
 
 // creatures.grow_plants (creatures.py:525-541)
 template <bool EXT>
-__device__ void grow_plants(Ctx& e) {
+GR_STEP_NI __device__ void grow_plants(Ctx& e) {
 #pragma unroll
   for (int l = 0; l < 10; ++l) {
     if (!e.plal[l]) continue;
@@ -1226,6 +1235,7 @@ __device__ __forceinline__ void apply_pending(Ctx& e, uint8_t pend, uint32_t pre
   for (int l = 0; l < 2; ++l)
     if (ran && ((pend >> (3 + l)) & 1) && e.lcd[3 + l] > 0) e.lcd[3 + l] -= 1;
 }
+
 
 #ifndef GR_STEP_SMEM_CTX
 #define GR_STEP_SMEM_CTX 1   // per-thread working copy in shared memory (0: registers + local memory)
