@@ -1,8 +1,8 @@
 """Aggregate an ncu source page (cuda,sass) per CUDA source line."""
-import csv, sys, collections, subprocess, io
+import csv, sys, collections, subprocess, io, os
 
 def lines(rep, top=25):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+    out = subprocess.run(["ncu", "-i", rep, *(["--launch-skip", os.environ["NCU_SKIP"], "--launch-count", "1"] if os.environ.get("NCU_SKIP") else []), "--page", "source", "--csv", "--print-source=cuda,sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     agg = collections.defaultdict(lambda: [0.0, 0.0, ""])
