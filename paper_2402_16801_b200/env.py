@@ -104,7 +104,10 @@ class GridrogueBatch:
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:
-            lib().gr_destroy(h)
+            try:
+                lib().gr_destroy(h)
+            except Exception:   # interpreter shutdown: module globals already gone
+                pass
             self.h = None
 
     # --- hot path -----------------------------------------------------

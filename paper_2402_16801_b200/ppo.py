@@ -54,6 +54,7 @@ class PPOConfig:
     total_timesteps: int = 1_000_000_000
     seed: int = 0
     bf16: bool = True             # autocast the MLPs to bf16 (tensor cores)
+    graphs: bool = True           # one GPU: rollout step, GAE and minibatch update as CUDA graphs
 
 
 def gae(rewards, values, dones, last_value, gamma: float, lam: float):
@@ -103,6 +104,34 @@ def make_model(obs_dim: int, n_actions: int, layer: int):
     return ActorCritic()
 
 
+def make_fused_model(obs_dim: int, n_actions: int, layer: int):
+    """The same actor and critic as make_model, with the two first layers
+    stored as one [2*layer, obs_dim] weight (rows [0, layer) the actor's, the
+    rest the critic's, each half orthogonally initialised on its own): one
+    GEMM over the wide observation instead of two.  Mathematically the two
+    separate MLPs."""
+    import torch
+    import torch.nn as nn
+
+    class FusedActorCritic(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.layer = layer
+            self.first = nn.Linear(obs_dim, 2 * layer)
+            with torch.no_grad():
+                for h in range(2):
+                    nn.init.orthogonal_(self.first.weight[h * layer:(h + 1) * layer], math.sqrt(2))
+                nn.init.zeros_(self.first.bias)
+            self.actor = _mlp(nn, [layer, layer, layer], n_actions, 0.01)
+            self.critic = _mlp(nn, [layer, layer, layer], 1, 1.0)
+
+        def forward(self, x):
+            h = torch.tanh(self.first(x))
+            return self.actor(h[:, :self.layer]), self.critic(h[:, self.layer:]).squeeze(-1)
+
+    return FusedActorCritic()
+
+
 def train(cfg: PPOConfig, log=print, max_updates: int | None = None) -> dict:
     import torch
     import torch.distributed as dist
@@ -112,6 +141,8 @@ def train(cfg: PPOConfig, log=print, max_updates: int | None = None) -> dict:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    if cfg.graphs and world == 1:
+        return _train_graphed(cfg, log, max_updates)
     dev = torch.device("cuda", local)
     if world > 1 and not dist.is_initialized():
         dist.init_process_group("nccl", device_id=dev)
@@ -223,6 +254,238 @@ def train(cfg: PPOConfig, log=print, max_updates: int | None = None) -> dict:
               "seconds": round(dt, 3), "sps": round(steps_done / dt, 1), "episodes_rank0": st["episodes"],
               "mean_episode_return_rank0": st["total_return"] / max(st["episodes"], 1), "history": history}
     return result
+
+
+def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
+    """Single-GPU PPO with every per-step launch sequence replayed as a CUDA graph.
+
+    The eager loop in train() issues ~40 small kernels per env step and
+    ~150 per minibatch from Python; at Craftax-1B's 1,024 envs the GPU then
+    idles between launches.  Here, after one eager warm-up update:
+      * rollout step t = one graph (obs -> bf16 rollout buffer, actor / critic
+        forward, Gumbel-max sample into the env's action buffer, log-prob,
+        value, the previous step's reward / done), then the env step (the
+        library's own captured step graph);
+      * GAE over the rollout = one graph;
+      * each minibatch = one graph (gather, forward, clipped losses,
+        backward, global-norm clip, Adam with a device-side learning rate).
+    Same algorithm and hyper-parameters as the eager loop; the sampling
+    noise comes from torch's graph-safe generator (Gumbel-max instead of
+    multinomial), so runs are not bitwise equal to eager ones.
+    """
+    import torch
+    from .env import TIERS, GridrogueBatch
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    torch.manual_seed(cfg.seed)
+    n, T = cfg.n_envs, cfg.n_steps
+    gb = GridrogueBatch(n, cfg.tier, cfg.seed, "symbolic", newly=False, info=False)
+    gb.set_validate(False)   # actions are sampled in range
+    t_info = TIERS[cfg.tier]
+    obs_dim, n_actions = t_info["obs"], t_info["n_actions"]
+    # rows padded to a multiple of 64 elements (8268 -> 8320): cuBLAS runs the
+    # first layer's GEMMs on its fast tensor-core path only with 16-byte
+    # aligned leading dimensions; the pad columns hold zeros, so they add
+    # nothing to the pre-activations and their weights get zero gradients
+    obs_pad = (obs_dim + 63) // 64 * 64
+    model = make_fused_model(obs_pad, n_actions, cfg.layer_size).to(dev)
+    params = list(model.parameters())
+    # rollout weights: bf16 copies refreshed once per rollout (the weights do
+    # not change within one), so the 64 per-step graphs cast nothing
+    roll_w = [p.detach().to(torch.bfloat16 if cfg.bf16 else torch.float32) for p in params]
+    lr_t = torch.tensor(cfg.lr, dtype=torch.float32, device=dev)
+    opt = torch.optim.Adam(params, lr=lr_t, eps=1e-5, capturable=True, fused=True)
+    batch_size = n * T
+    n_updates = max(1, cfg.total_timesteps // batch_size)
+    if max_updates is not None:
+        n_updates = min(n_updates, max_updates)
+    mb = batch_size // cfg.n_minibatches
+    odt = torch.bfloat16 if cfg.bf16 else torch.float32   # autocast casts the input to bf16 anyway
+
+    buf_obs = torch.zeros((T, n, obs_pad), dtype=odt, device=dev)
+    last_obs = torch.zeros((n, obs_pad), dtype=odt, device=dev)
+    buf_act = torch.empty((T, n), dtype=torch.int64, device=dev)
+    buf_logp = torch.empty((T, n), dtype=torch.float32, device=dev)
+    buf_val = torch.empty((T, n), dtype=torch.float32, device=dev)
+    buf_rew = torch.empty((T, n), dtype=torch.float32, device=dev)
+    buf_done = torch.empty((T, n), dtype=torch.float32, device=dev)
+    adv = torch.empty((T, n), dtype=torch.float32, device=dev)
+    ret = torch.empty((T, n), dtype=torch.float32, device=dev)
+    last_v = torch.empty(n, dtype=torch.float32, device=dev)
+    idx_s = torch.zeros(mb, dtype=torch.int64, device=dev)
+    stats_s = torch.zeros(4, dtype=torch.float32, device=dev)
+    stats_acc = torch.zeros(4, dtype=torch.float32, device=dev)
+
+    def policy(x):
+        # no autocast weight cache: graphs must own their casts
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.bf16, cache_enabled=False):
+            logits, v = model(x)
+        return logits.float(), v.float()
+
+    lin_ix = [(k, k + 1) for k in range(0, len(params), 2)]   # (weight, bias) per Linear, module order
+
+    def roll_policy(x):
+        """Rollout forward on the pre-cast weights (module order: first,
+        actor 2 + head, critic 2 + head)."""
+        F = torch.nn.functional
+        (w0, b0), rest = lin_ix[0], lin_ix[1:]
+        h = torch.tanh(F.linear(x, roll_w[w0], roll_w[b0]))
+        L = cfg.layer_size
+        ha, hc = h[:, :L], h[:, L:]
+        na = (len(rest)) // 2
+        for j, (w, b) in enumerate(rest[:na]):
+            ha = F.linear(ha, roll_w[w], roll_w[b])
+            if j < na - 1:
+                ha = torch.tanh(ha)
+        for j, (w, b) in enumerate(rest[na:]):
+            hc = F.linear(hc, roll_w[w], roll_w[b])
+            if j < na - 1:
+                hc = torch.tanh(hc)
+        return ha.float(), hc.float().squeeze(-1)
+
+    def refresh_roll_w():
+        for dst, src in zip(roll_w, params):
+            dst.copy_(src.detach())
+
+    def roll_step(t):
+        if t > 0:
+            buf_rew[t - 1].copy_(gb.reward)
+            buf_done[t - 1].copy_(gb.done)
+        if t == T:   # closing step: the bootstrap value
+            last_obs[:, :obs_dim].copy_(gb.obs)
+            _, v = roll_policy(last_obs)
+            last_v.copy_(v)
+            return
+        buf_obs[t, :, :obs_dim].copy_(gb.obs)
+        logits, v = roll_policy(buf_obs[t])
+        u = torch.rand_like(logits).clamp_(min=1e-20)
+        a = (logits - torch.log(-torch.log(u))).argmax(-1)
+        logp = torch.log_softmax(logits, -1).gather(-1, a[:, None]).squeeze(-1)
+        gb.actions.copy_(a)
+        buf_act[t].copy_(a)
+        buf_logp[t].copy_(logp)
+        buf_val[t].copy_(v)
+
+    def gae_step():
+        a_, r_ = gae(buf_rew, buf_val, buf_done, last_v, cfg.gamma, cfg.gae_lambda)
+        adv.copy_(a_)
+        ret.copy_(r_)
+
+    b_obs = buf_obs.view(batch_size, obs_pad)
+    b_act, b_logp = buf_act.view(-1), buf_logp.view(-1)
+    b_adv, b_ret, b_val = adv.view(-1), ret.view(-1), buf_val.view(-1)
+
+    def mb_step():
+        idx = idx_s
+        logits, v = policy(b_obs.index_select(0, idx))
+        logp_all = torch.log_softmax(logits, -1)
+        logp = logp_all.gather(-1, b_act.index_select(0, idx)[:, None]).squeeze(-1)
+        ratio = torch.exp(logp - b_logp.index_select(0, idx))
+        a_ = b_adv.index_select(0, idx)
+        a_ = (a_ - a_.mean()) / (a_.std() + 1e-8)
+        pg = -torch.min(ratio * a_, ratio.clamp(1 - cfg.clip_eps, 1 + cfg.clip_eps) * a_).mean()
+        bv, br = b_val.index_select(0, idx), b_ret.index_select(0, idx)
+        v_clip = bv + (v - bv).clamp(-cfg.clip_eps, cfg.clip_eps)
+        vl = 0.5 * torch.max((v - br) ** 2, (v_clip - br) ** 2).mean()
+        ent = -(logp_all.exp() * logp_all).sum(-1).mean()
+        loss = pg + cfg.vf_coef * vl - cfg.ent_coef * ent
+        loss.backward()
+        torch.nn.utils.clip_grad_norm_(params, cfg.max_grad_norm, foreach=True)
+        opt.step()
+        stats_s.copy_(torch.stack([loss.detach(), pg.detach(), vl.detach(), ent.detach()]))
+
+    g_roll, g_gae, g_mb = None, None, None
+    pool = None
+
+    def capture(fn, *args):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, pool=pool):
+            fn(*args)
+        return g
+
+    gb.reset()
+    history = []
+    last_ep, last_ret = 0, 0.0
+    t0 = time.perf_counter()
+    steps_done = 0
+    side = torch.cuda.Stream(device=dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    for upd in range(n_updates):
+        ev[0].record()
+        if cfg.anneal_lr:
+            lr_t.fill_(cfg.lr * (1.0 - upd / n_updates))
+        # --- rollout ---------------------------------------------------------
+        with torch.no_grad():
+            refresh_roll_w()
+            for t in range(T + 1):
+                if g_roll is None:
+                    roll_step(t)
+                else:
+                    g_roll[t].replay()
+                if t < T:
+                    gb.step(gb.actions)
+            if g_gae is None:
+                gae_step()
+            else:
+                g_gae.replay()
+        ev[1].record()
+        # --- update ----------------------------------------------------------
+        stats_acc.zero_()
+        for ep in range(cfg.update_epochs):
+            perm = torch.rand(batch_size, device=dev).argsort()   # on the device (randperm builds it on the host)
+            for k in range(cfg.n_minibatches):
+                idx_s.copy_(perm[k * mb:(k + 1) * mb])
+                if g_mb is not None:
+                    g_mb.replay()
+                elif upd == 0 and ep == 0 and k == 3:
+                    # three eager minibatches above warmed autograd / cuBLAS
+                    # up; capture (captures do not execute) and replay
+                    torch.cuda.synchronize()
+                    opt.zero_grad(set_to_none=True)
+                    g_mb = capture(mb_step)
+                    g_mb.replay()
+                else:
+                    side.wait_stream(torch.cuda.current_stream())
+                    with torch.cuda.stream(side):
+                        opt.zero_grad(set_to_none=True)
+                        mb_step()
+                    torch.cuda.current_stream().wait_stream(side)
+                stats_acc.add_(stats_s)
+        if g_roll is None:   # after the eager warm-up update: capture the rollout and GAE
+            torch.cuda.synchronize()
+            with torch.no_grad():
+                # the pre-cast rollout forward is the module's forward
+                refresh_roll_w()
+                la, va = roll_policy(buf_obs[0])
+                lb, vb = policy(buf_obs[0])
+                err = max(float((la - lb).abs().max()), float((va - vb).abs().max()))
+                assert err < 5e-2, f"rollout forward differs from the module forward by {err}"
+                pool = torch.cuda.graph_pool_handle() if pool is None else pool
+                g_roll = [capture(roll_step, t) for t in range(T + 1)]
+                g_gae = capture(gae_step)
+        ev[2].record()
+        steps_done += batch_size
+        if upd % 10 == 0 or upd == n_updates - 1:
+            torch.cuda.synchronize()
+            ms_roll, ms_upd = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+            s = (stats_acc / (cfg.update_epochs * cfg.n_minibatches)).tolist()
+            st = gb.stats()
+            mean_ret = st["total_return"] / max(st["episodes"], 1)
+            window = (st["total_return"] - last_ret) / max(st["episodes"] - last_ep, 1)
+            last_ep, last_ret = st["episodes"], st["total_return"]
+            row = {"update": upd, "env_steps": steps_done, "sps": round(steps_done / (time.perf_counter() - t0), 1),
+                   "loss": s[0], "pg_loss": s[1], "v_loss": s[2], "entropy": s[3],
+                   "episodes": st["episodes"], "mean_episode_return": mean_ret,
+                   "recent_episode_return": window,
+                   "ms_rollout": round(ms_roll, 3), "ms_update": round(ms_upd, 3)}
+            history.append(row)
+            log(json.dumps(row))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    st = gb.stats()
+    return {"config": asdict(cfg), "n_gpus": 1, "updates": n_updates, "env_steps": steps_done,
+            "seconds": round(dt, 3), "sps": round(steps_done / dt, 1), "episodes_rank0": st["episodes"],
+            "mean_episode_return_rank0": st["total_return"] / max(st["episodes"], 1), "history": history}
 
 
 def main(argv=None) -> int:
