@@ -1263,17 +1263,22 @@ __global__ void __launch_bounds__(128, GR_STEP_MINB) k_step(DS S, StepArgs a) {
   __syncthreads();
   if (valid) {
     e.i = (uint32_t)i;
+    // the per-env words the tail needs are loaded with the state, not after
+    // the game logic (the compiler does not move loads across its stores)
+    const int action = (int)a.actions[i];
+    const double ep_ret0 = S.ep_return[i];
+    const int32_t ep_len0 = S.ep_length[i];
+    uint8_t pend = S.cd_pending[i];
+    const uint32_t prev_fl = a.prev_flags ? a.prev_flags[0] : 0u;
     load_env<EXT>(e, S);
     load_lanes<EXT>(e, S, e.pfloor);
-    uint8_t pend = S.cd_pending[i];
-    apply_pending(e, pend, a.prev_flags ? a.prev_flags[0] : 0u);
+    apply_pending(e, pend, prev_fl);
     pend = 0;
     // _kern.Workspace.begin_step
     e.unlock[0] = e.unlock[1] = e.unlock[2] = 0;
     e.hurt = false;
     e.health0 = e.health;
     e.base = mix32(e.key_lo ^ (e.time * 0x9E3779B9u));
-    const int action = (int)a.actions[i];
     const int f0 = e.pfloor;
     player_actions<EXT>(e, S, action);
     if (EXT && e.pfloor != f0) {   // a ladder: the creature phases act on the new floor
@@ -1317,8 +1322,8 @@ __global__ void __launch_bounds__(128, GR_STEP_MINB) k_step(DS S, StepArgs a) {
     S.cd_pending[i] = pend;
     GR_AT(S, GR_F_DONE, uint8_t, 0, i) = done;
     // batch.batch_step bookkeeping (batch.py:206-209) and outputs
-    S.ep_return[i] = __dadd_rn(S.ep_return[i], reward);
-    S.ep_length[i] += 1;
+    S.ep_return[i] = __dadd_rn(ep_ret0, reward);
+    S.ep_length[i] = ep_len0 + 1;
     a.reward[i] = (float)reward;
     a.done[i] = done;
     if (a.itime) a.itime[i] = e.time;
