@@ -215,8 +215,13 @@ __device__ inline void dd_sincos(double x, double* s_out, double* c_out) {
 __device__ __forceinline__ float q1(float x) {
   return __fmul_rn(floorf(__fadd_rn(__fmul_rn(x, 10.0f), 0.5f)), 0.1f);
 }
-// _kern.resolve_attack_vec for one (3,) damage vs (3,) percent defense
-__device__ __forceinline__ float resolve(const float d0, const float d1, const float d2, const float f0,
+// _kern.resolve_attack_vec for one (3,) damage vs (3,) percent defense.
+// Three IEEE divisions (~25 instructions each): one out-of-line copy instead
+// of one per call site keeps k_step's code (and its i-cache misses) smaller.
+#ifndef GR_RESOLVE_INLINE
+#define GR_RESOLVE_INLINE __noinline__
+#endif
+static __device__ GR_RESOLVE_INLINE float resolve(const float d0, const float d1, const float d2, const float f0,
                                          const float f1, const float f2) {
   float t0 = __fmul_rn(d0, __fsub_rn(1.0f, __fdiv_rn(f0, 100.0f)));
   float t1 = __fmul_rn(d1, __fsub_rn(1.0f, __fdiv_rn(f1, 100.0f)));

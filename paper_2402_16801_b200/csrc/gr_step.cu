@@ -807,15 +807,16 @@ GR_STEP_NI __device__ void advance_projectiles(Ctx& e) {
 #pragma unroll
     for (int l = 0; l < 3; ++l)
       if (e.ppal[l]) { e.ppr[l] += C_DIR[e.ppdir[l]][0]; e.ppc[l] += C_DIR[e.ppdir[l]][1]; }
-#pragma unroll
+#pragma unroll 1
     for (int l = 0; l < 3; ++l) {
       if (!e.ppal[l]) continue;
       int r = e.ppr[l], c = e.ppc[l];
       bool live = true;
-#pragma unroll
+#pragma unroll 1
       for (int cls = 0; cls < 3; ++cls) {
         if (!live) break;
         int hit = -1;
+#pragma unroll 1
         for (int k = LCAP(cls) - 1; k >= 0; --k) {
           int s = L0(cls) + k;
           if (e.lal[s] && e.lr[s] == r && e.lc[s] == c) hit = s;
@@ -1330,6 +1331,7 @@ __global__ void __launch_bounds__(128, GR_STEP_MINB) k_step(DS S, StepArgs a) {
     if (a.ifloor) a.ifloor[i] = e.pfloor;
     if (a.newly) {
       uint8_t* nw = a.newly + (size_t)i * T::A;
+#pragma unroll 1
       for (int k = 0; k < T::A; ++k) nw[k] = (newly[k >> 5] >> (k & 31)) & 1u;
     }
     if (a.reward64) a.reward64[i] = reward;
