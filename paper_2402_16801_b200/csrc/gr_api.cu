@@ -174,6 +174,13 @@ struct gr_env {
                               // inside a step graph the other order starves the writer (0.55 vs 0.49 ms)
   int side_prio = 0;          // side stream priority (0 default, >0 lowest)
   bool graphs = true;         // GR_GRAPH=0: launch the step kernel by kernel
+  // speculative pool (one-shard steps): the side stream generates the first
+  // spec_k worlds of this step's pool beside k_step, before the done count
+  // is known; on by default while k_step's grid leaves SMs free (GR_SPEC=0/1)
+  bool spec_on = false;
+  bool spec_pending = false;
+  int32_t* spec_k = nullptr;
+  cudaEvent_t ev_spec = nullptr;
   cudaStream_t cap_stream = nullptr;
   std::vector<StepGraph> step_graphs;
   std::vector<void*> allocs;
@@ -270,6 +277,7 @@ void gr_destroy(gr_env* e) {
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   if (e->ev_fork) cudaEventDestroy(e->ev_fork);
   if (e->ev_join) cudaEventDestroy(e->ev_join);
+  if (e->ev_spec) cudaEventDestroy(e->ev_spec);
   for (auto x : e->prof.pool) cudaEventDestroy(x);
   delete e;
 }
@@ -308,6 +316,14 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   e->n = cfg->n_envs;
   e->M = std::max<int64_t>(1, (ng + cfg->reset_ratio - 1) / cfg->reset_ratio);
   e->nb = (e->n + 127) / 128;
+  {
+    // measured (tools/dev/spec_ab.sh): classic 1,024 envs 19.4 -> 24.3 M
+    // env-steps/s, extended 4,096 28.7 -> 31.8 M; extended 16,384 88 ->
+    // 81 M and 65,536 139 -> 110 M (the speculative CTAs crowd k_step and
+    // the writer, and the extra worlds cost more than the hidden latency)
+    e->spec_on = e->nb <= 32 && ng == cfg->n_envs;
+    if (const char* sp = getenv("GR_SPEC")) e->spec_on = atoi(sp) != 0 && ng == cfg->n_envs;
+  }
   int rc = GR_OK;
   e->S.ns = e->n;
   for (int f = 0; f < GR_NFIELDS && rc == GR_OK; ++f) {
@@ -340,6 +356,8 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->exchange, 4 * sizeof(int32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->arrive, sizeof(unsigned int));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->dstep, sizeof(unsigned long long));
+  if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->spec_k, sizeof(int32_t));
+  if (rc == GR_OK && cudaMemset(e->spec_k, 0, sizeof(int32_t)) != cudaSuccess) rc = fail(GR_E_CUDA, "memset");
   if (rc == GR_OK && cfg->obs_mode == GR_OBS_PIXELS)
     rc = dev_alloc(e, (void**)&e->pix, (size_t)e->n * pix_scratch_words(e->ext) * sizeof(uint32_t));
   if (rc == GR_OK) rc = dev_alloc(e, (void**)&e->cur_flags, sizeof(uint32_t));
@@ -356,7 +374,8 @@ int gr_create(const gr_config* cfg, gr_env** out) {
     cudaDeviceGetStreamPriorityRange(&lo, &hi);   // lo: least urgent
     if (cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, e->side_prio > 0 ? lo : 0) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_spec, cudaEventDisableTiming) != cudaSuccess)
       rc = fail(GR_E_CUDA, "stream/event creation failed");
   }
   if (rc != GR_OK) {
@@ -520,6 +539,30 @@ static int step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, 
     a.M = e->M;
     a.flags_out = e->prev_flags;
   }
+  e->spec_pending = false;
+  if (fuse_info && e->spec_on) {
+    // the first spec_k worlds of this step's pool, on the side stream beside
+    // k_step; k_step leaves the step counter to k_install_pool so the
+    // speculative pass reads a stable value
+    CK(cudaEventRecord(e->ev_fork, st));
+    CK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+    WorldJob sj{};
+    sj.mode = 3;
+    sj.M = e->M;
+    sj.out = e->pool;
+    sj.counters = e->counters;
+    sj.ctas_per_sm = e->wg_ctas;
+    sj.spec_k = e->spec_k;
+    sj.pool_key = e->pool_key;
+    sj.dstep = e->dstep;
+    {
+      PTimer t(e, PK_WORLDGEN, e->side);
+      launch_worldgen(e->ext, sj, e->side);
+    }
+    CK(cudaEventRecord(e->ev_spec, e->side));
+    a.defer_advance = 1;
+    e->spec_pending = true;
+  }
   e->last_done = done_dev;
   {
     PTimer t(e, PK_STEP, st);
@@ -559,6 +602,9 @@ static int step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank,
     PTimer t(e, PK_SCAN, rs);
     launch_compact((const uint8_t*)e->S.f[GR_F_DONE], e->n, e->block_off, e->done_list, rs);
   }
+  const bool spec = e->spec_pending;
+  e->spec_pending = false;
+  if (spec && rs != e->side) CK(cudaStreamWaitEvent(rs, e->ev_spec, 0));
   WorldJob j{};
   j.mode = 1;
   j.info = e->info;
@@ -566,6 +612,7 @@ static int step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank,
   j.out = e->pool;
   j.counters = e->counters;
   j.ctas_per_sm = e->wg_ctas;
+  j.spec_k = spec ? e->spec_k : nullptr;   // only the slots the speculative pass did not make
   {
     PTimer t(e, PK_WORLDGEN, rs);
     launch_worldgen(e->ext, j, rs);
@@ -581,6 +628,11 @@ static int step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank,
   ia.st_steps = e->st_steps;
   ia.st_return = e->st_return;
   ia.st_ach = e->st_ach;
+  if (spec) {
+    ia.dstep_advance = e->dstep;
+    ia.spec_k = e->spec_k;
+    ia.spec_cap = e->pool.cap;
+  }
   {
     PTimer t(e, PK_INSTALL, rs);
     launch_install_pool(e->ext, e->S, ia, rs);

@@ -33,6 +33,7 @@ struct StepArgs {
   unsigned long long* dstep;   // device step counter (combine_info)
   int64_t M;
   uint32_t* flags_out;
+  int defer_advance;           // 1: the counter advances in k_install_pool (speculative pool)
 };
 
 // step bookkeeping shared by the post-step kernels (device memory)
@@ -65,10 +66,23 @@ struct WorldJob {
   int ctas_per_sm;               // resident CTAs per SM (0 = default)
   LevelParamsBuf params;         // mode 2: world w of the job <- params / out slot first + w
   int64_t first;
+  // speculative pool (one shard): mode 3 generates slots [0, *spec_k) of the
+  // pool of the step about to run, WorldPool(pool_key, *dstep + 1), before
+  // its done count is known; mode 1 with spec_k set then generates only
+  // slots [min(*spec_k, n_pool), n_pool)
+  const int32_t* spec_k;
+  uint64_t pool_key;
+  const unsigned long long* dstep;
 };
 
 struct InstallArgs {
   int mode;                   // 0: initial (world w -> env w, maps already in place), 1: pool
+  // speculative pool: CTA 0 advances the step counter (deferred from the
+  // step tail, so the speculative worldgen read a stable value) and sizes
+  // the next step's speculation from this step's n_pool
+  unsigned long long* dstep_advance;
+  int32_t* spec_k;
+  int64_t spec_cap;
   int64_t n;                  // mode 0 env count
   const int32_t* done_list;   // mode 1: env index per local done rank (k_compact)
   const StepInfo* info;

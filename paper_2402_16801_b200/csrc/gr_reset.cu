@@ -203,6 +203,13 @@ template <bool EXT>
 __global__ void __launch_bounds__(128) k_install_pool(DS S, InstallArgs a) {
   constexpr int F = EXT ? 9 : 1, HW = EXT ? 48 * 48 : 64 * 64, A = EXT ? 67 : 22;
   const int k = a.info->k_local;
+  if (a.dstep_advance && blockIdx.x == 0 && threadIdx.x == 0) {
+    *a.dstep_advance += 1;
+    // next step's speculation: this step's pool size + 25 % + 8 (the done
+    // count moves slowly; a shortfall is generated after the step as before)
+    const int np = a.info->n_pool;
+    *a.spec_k = (int32_t)min((int64_t)(np + (np >> 2) + 8), a.spec_cap);
+  }
   for (int r = blockIdx.x; r < k; r += gridDim.x) {
     const int64_t env = a.done_list[r];
     const int64_t p = r % a.M;                   // pool entry

@@ -52,10 +52,11 @@ __device__ __forceinline__ int32_t cta_scan_blocks(const int32_t* block_done, in
 // the pool serving this step is WorldPool(pool_key, step + 1, M)
 // (batch.py:217), and the counter advances here, once per step.
 __device__ __forceinline__ void combine_info(const int32_t* ex_all, int rank, int world, int64_t M, uint64_t pool_key,
-                                             unsigned long long* dstep, StepInfo* info, uint32_t* flags_out) {
+                                             unsigned long long* dstep, StepInfo* info, uint32_t* flags_out,
+                                             bool advance = true) {
   const unsigned long long step = *dstep;
   const uint64_t step_key = hash2(pool_key, (uint64_t)(step + 1));
-  *dstep = step + 1;
+  if (advance) *dstep = step + 1;   // else k_install_pool advances it (speculative pool)
   int off = 0;
   uint32_t fl = 0;
   for (int r = 0; r < world; ++r) {

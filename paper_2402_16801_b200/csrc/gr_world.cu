@@ -792,7 +792,18 @@ template <bool EXT>
 __global__ void __launch_bounds__(WT<EXT>::THREADS, WT<EXT>::MINB) k_worldgen(WorldJob job) {
   using T = WT<EXT>;
   __shared__ WSmem<EXT> sm;
-  const int64_t nworlds = job.mode == 1 ? (int64_t)job.info->n_pool : job.count;
+  // mode 1: pool worlds [w0, n_pool) (w0 > 0: the speculative pass made the
+  // rest); mode 3: the speculative pass, worlds [0, spec_k)
+  int64_t w0 = 0, nworlds = job.count;
+  uint64_t spec_key = 0;
+  if (job.mode == 1) {
+    const int64_t np = (int64_t)job.info->n_pool;
+    w0 = job.spec_k ? (int64_t)min(*job.spec_k, (int32_t)np) : 0;
+    nworlds = np - w0;
+  } else if (job.mode == 3) {
+    nworlds = *job.spec_k;
+    spec_key = hash2(job.pool_key, (uint64_t)(*job.dstep + 1));   // = this step's StepInfo.step_key
+  }
   const int64_t items = nworlds * T::F;
   build_profiles_f32<EXT>(sm);
   if (EXT) build_profiles_f64<EXT>(sm);
@@ -802,7 +813,7 @@ __global__ void __launch_bounds__(WT<EXT>::THREADS, WT<EXT>::MINB) k_worldgen(Wo
     // generator, which keeps the instruction cache warm (no_instructions
     // stalls dominated a world-major order)
     const int f = (int)(it / nworlds);
-    const int64_t w = (it % nworlds) + (job.mode == 2 ? job.first : 0);   // output slot
+    const int64_t w = (it % nworlds) + (job.mode == 2 ? job.first : w0);   // output slot
     uint64_t seed, key;
     if (job.mode == 0) {
       seed = hash2(job.env_key, hash2((uint64_t)(job.env_offset + w), 0));
@@ -811,6 +822,9 @@ __global__ void __launch_bounds__(WT<EXT>::THREADS, WT<EXT>::MINB) k_worldgen(Wo
       const int64_t slot = ((int64_t)job.info->offset + w) % job.M;
       seed = hash2(job.info->step_key, (uint64_t)slot);
       key = hash2(job.info->step_key, (1ull << 32) + (uint64_t)slot);
+    } else if (job.mode == 3) {   // one shard: offset 0, w < cap <= M
+      seed = hash2(spec_key, (uint64_t)w);
+      key = hash2(spec_key, (1ull << 32) + (uint64_t)w);
     } else {
       seed = job.params.seed[w];
       key = 0;   // levels get their install key when installed
@@ -920,7 +934,7 @@ void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t max_items = (j.mode == 1 ? j.out.cap : j.count) * (ext ? 9 : 1);
+  int64_t max_items = (j.mode == 1 || j.mode == 3 ? j.out.cap : j.count) * (ext ? 9 : 1);
   int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * (j.ctas_per_sm > 0 ? j.ctas_per_sm
                                                                 : ext ? WT<true>::MINB : WT<false>::MINB));
   if (grid <= 0) return;
