@@ -295,11 +295,17 @@ __global__ void __launch_bounds__(128) k_pixprep(DS S, ObsArgs a) {
 // threads per frame CTA: large frames stream faster with more (extended 10 px:
 // 128 -> 384 took the writer from 0.95 to 0.84 ms; 512+ slower), small
 // frames prefer 128 (classic 7 px: 384 was 10 % slower)
+#ifndef GR_PIX_MINB
+#define GR_PIX_MINB 4   // resident frame CTAs per SM the registers are fitted to (ext px10: 40 registers, 4 CTAs/SM)
+#endif
+#ifndef GR_PIX_STREAM_INC
+#define GR_PIX_STREAM_INC 1   // incremental (row, offset) walk in the chunk stream (0: divide per chunk)
+#endif
 template <bool EXT, int PX>
 __host__ __device__ constexpr int pix_threads() { return PG<EXT, PX>::FB >= 32768 ? 384 : 128; }
 
 template <bool EXT, int PX>
-__global__ void __launch_bounds__(pix_threads<EXT, PX>()) k_pixels(DS S, ObsArgs a) {
+__global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(DS S, ObsArgs a) {
   using O = OT<EXT>;
   using G = PG<EXT, PX>;
   constexpr int PW = pix_words<EXT>();
@@ -470,6 +476,37 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>()) k_pixels(DS S, ObsArgs
     // store covers 512 contiguous bytes; a chunk at row offset o is the
     // funnel shift of the 5 pattern words from o & ~3 (padded layout: the
     // lanes' loads hit distinct banks)
+#if GR_PIX_STREAM_INC
+    {
+      // (row, offset) of each thread's chunk advance by a constant per pass
+      // (NT * 16 bytes = DY rows + DO bytes), so no division per chunk; the
+      // pattern is addressed in words with the pad word per 32 folded in
+      constexpr int NT = pix_threads<EXT, PX>();
+      constexpr int DY = NT * 16 / G::RB, DO = NT * 16 - DY * G::RB;
+      const uint32_t* patw = reinterpret_cast<const uint32_t*>(pat);
+      int b = (int)(c0 - f0) + 16 * (int)threadIdx.x;
+      int y = b / G::RB, o = b - y * G::RB;
+      uint4* dst = reinterpret_cast<uint4*>(out + c0) + threadIdx.x;
+      for (int q = threadIdx.x; q < nchunk; q += NT) {
+        if (o + 16 <= G::RB) {
+          const uint32_t* w = patw + rowcls[y] * (G::PS / 4);
+          const int L = o >> 2, sh = (o & 3) * 8, r = L & 31;
+          const uint32_t* wl = w + L + (L >> 5);
+          const uint32_t x0 = wl[0];
+          const uint32_t x1 = wl[1 + (r >= 31)];
+          const uint32_t x2 = wl[2 + (r >= 30)];
+          const uint32_t x3 = wl[3 + (r >= 29)];
+          const uint32_t x4 = wl[4 + (r >= 28)];
+          *dst = make_uint4(__funnelshift_r(x0, x1, sh), __funnelshift_r(x1, x2, sh), __funnelshift_r(x2, x3, sh),
+                            __funnelshift_r(x3, x4, sh));
+        }
+        dst += NT;
+        y += DY;
+        o += DO;
+        if (o >= G::RB) { o -= G::RB; ++y; }
+      }
+    }
+#else
     for (int q = threadIdx.x; q < nchunk; q += blockDim.x) {
       const int b = (int)(c0 - f0) + 16 * q;
       const int y = b / G::RB, o = b - y * G::RB;
@@ -484,6 +521,7 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>()) k_pixels(DS S, ObsArgs
         *reinterpret_cast<uint4*>(out + c0 + 16 * (int64_t)q) = val;
       }
     }
+#endif
     if (warp == 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     j = jn;
