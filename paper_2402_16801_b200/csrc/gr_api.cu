@@ -178,6 +178,7 @@ struct gr_env {
   // spec_k worlds of this step's pool beside k_step, before the done count
   // is known; on by default while k_step's grid leaves SMs free (GR_SPEC=0/1)
   bool spec_on = false;
+  bool wg_wide = false;       // pool worldgen with 256-thread extended CTAs (small batches; GR_WG_WIDE=0/1)
   bool spec_pending = false;
   int32_t* spec_k = nullptr;
   cudaEvent_t ev_spec = nullptr;
@@ -323,6 +324,8 @@ int gr_create(const gr_config* cfg, gr_env** out) {
     // the writer, and the extra worlds cost more than the hidden latency)
     e->spec_on = e->nb <= 32 && ng == cfg->n_envs;
     if (const char* sp = getenv("GR_SPEC")) e->spec_on = atoi(sp) != 0 && ng == cfg->n_envs;
+    e->wg_wide = e->nb <= 32;
+    if (const char* ww = getenv("GR_WG_WIDE")) e->wg_wide = atoi(ww) != 0;
   }
   int rc = GR_OK;
   e->S.ns = e->n;
@@ -555,6 +558,7 @@ static int step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, 
     sj.spec_k = e->spec_k;
     sj.pool_key = e->pool_key;
     sj.dstep = e->dstep;
+    sj.wide = e->wg_wide;
     {
       PTimer t(e, PK_WORLDGEN, e->side);
       launch_worldgen(e->ext, sj, e->side);
@@ -613,6 +617,7 @@ static int step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank,
   j.counters = e->counters;
   j.ctas_per_sm = e->wg_ctas;
   j.spec_k = spec ? e->spec_k : nullptr;   // only the slots the speculative pass did not make
+  j.wide = e->wg_wide;
   {
     PTimer t(e, PK_WORLDGEN, rs);
     launch_worldgen(e->ext, j, rs);

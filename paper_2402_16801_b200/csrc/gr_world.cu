@@ -25,7 +25,20 @@
 #include "gr_state.cuh"
 #include "gr_kernels.cuh"
 
+#ifndef GR_WG_EXT_THREADS
+#define GR_WG_EXT_THREADS 128
+#endif
 namespace gr {
+#if GR_WG_WIDE
+// gr_world_wide.cu: this file again with 256-thread extended-tier CTAs, for
+// small batches where the reset chain's latency (one floor per CTA) is the
+// step's critical path
+namespace wide {
+#else
+namespace wide {
+void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st);
+}
+#endif
 
 constexpr double PI_D = 3.141592653589793;
 
@@ -36,8 +49,8 @@ struct WT {
   // and few worlds per step, so its single floor gets more threads (classic
   // 65,536 envs: 128 / 256 / 512 / 1024 threads -> 0.090 / 0.083 / 0.087 /
   // 0.102 ms of worldgen per step)
-  static constexpr int THREADS = EXT ? 128 : 256, WARPS = THREADS / 32;
-  static constexpr int MINB = EXT ? 8 : 1024 / THREADS;   // resident CTAs the registers are fitted to
+  static constexpr int THREADS = EXT ? GR_WG_EXT_THREADS : 256, WARPS = THREADS / 32;
+  static constexpr int MINB = 1024 / THREADS;   // resident CTAs the registers are fitted to (64 registers)
 };
 
 template <bool EXT>
@@ -930,6 +943,12 @@ void launch_level_params(const LevelParamsBuf& p, int64_t first, int64_t count, 
 }
 
 void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st) {
+#if !GR_WG_WIDE
+  if (ext && j.wide) {
+    wide::launch_worldgen(ext, j, st);
+    return;
+  }
+#endif
   // persistent grid: CTAs walk the (world, floor) items
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -942,4 +961,7 @@ void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st) {
   else k_worldgen<false><<<grid, WT<false>::THREADS, 0, st>>>(j);
 }
 
+#if GR_WG_WIDE
+}  // namespace wide
+#endif
 }  // namespace gr
