@@ -34,9 +34,27 @@ __device__ void install_one(const DS& S, int64_t i, const WMeta& m, const uint8_
     uint4* di = reinterpret_cast<uint4*>((uint8_t*)S.f[GR_F_ITEMS] + (size_t)i * F * HW);
     const uint4* sb = reinterpret_cast<const uint4*>(src_blk);
     const uint4* si = reinterpret_cast<const uint4*>(src_itm);
-    for (int q = threadIdx.x; q < F * HW / 16; q += blockDim.x) {
-      db[q] = sb[q];
-      di[q] = si[q];
+    // 2 x U vector loads in flight per thread before their stores: the copy
+    // is a chain of round trips otherwise (small batches wait on it)
+    constexpr int NV = F * HW / 16, U = 4;
+    for (int q0 = threadIdx.x; q0 < NV; q0 += U * blockDim.x) {
+      uint4 vb[U], vi[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + u * blockDim.x;
+        if (q < NV) {
+          vb[u] = sb[q];
+          vi[u] = si[q];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + u * blockDim.x;
+        if (q < NV) {
+          db[q] = vb[u];
+          di[q] = vi[u];
+        }
+      }
     }
   }
   // per-floor lanes and chests: spread over threads
