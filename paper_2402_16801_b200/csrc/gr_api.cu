@@ -178,7 +178,7 @@ struct gr_env {
   // spec_k worlds of this step's pool beside k_step, before the done count
   // is known; on by default while k_step's grid leaves SMs free (GR_SPEC=0/1)
   bool spec_on = false;
-  bool wg_wide = false;       // pool worldgen with 256-thread extended CTAs (small batches; GR_WG_WIDE=0/1)
+  bool wg_wide = false;       // pool worldgen with 512-thread extended CTAs (small batches; GR_WG_WIDE=0/1)
   bool spec_pending = false;
   int32_t* spec_k = nullptr;
   cudaEvent_t ev_spec = nullptr;

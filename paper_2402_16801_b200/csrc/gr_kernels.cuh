@@ -73,7 +73,7 @@ struct WorldJob {
   const int32_t* spec_k;
   uint64_t pool_key;
   const unsigned long long* dstep;
-  int wide;                      // extended tier: 256-thread CTAs (gr_world_wide.cu)
+  int wide;                      // extended tier: 512-thread CTAs (gr_world_wide.cu)
 };
 
 struct InstallArgs {

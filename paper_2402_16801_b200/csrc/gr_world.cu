@@ -30,7 +30,7 @@
 #endif
 namespace gr {
 #if GR_WG_WIDE
-// gr_world_wide.cu: this file again with 256-thread extended-tier CTAs, for
+// gr_world_wide.cu: this file again with 512-thread extended-tier CTAs, for
 // small batches where the reset chain's latency (one floor per CTA) is the
 // step's critical path
 namespace wide {
