@@ -326,7 +326,8 @@ int gr_create(const gr_config* cfg, gr_env** out) {
     // env-steps/s, extended 4,096 28.7 -> 31.8 M; extended 16,384 88 ->
     // 81 M and 65,536 139 -> 110 M (the speculative CTAs crowd k_step and
     // the writer, and the extra worlds cost more than the hidden latency)
-    e->spec_on = e->nb <= 32 && ng == cfg->n_envs;
+    // (classic 4,096 envs with pixels: 59.7 -> 57.1 M, so classic stops at 1,024)
+    e->spec_on = e->nb <= (e->ext ? 32 : 8) && ng == cfg->n_envs;
     if (const char* sp = getenv("GR_SPEC")) e->spec_on = atoi(sp) != 0 && ng == cfg->n_envs;
     e->wg_wide = e->nb <= 32;
     if (const char* ww = getenv("GR_WG_WIDE")) e->wg_wide = atoi(ww) != 0;
