@@ -7,7 +7,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
-        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio"]
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "smsp__branch_targets_threads_divergent.sum", "launch__occupancy_limit_registers",
+        "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_warps",
+        "sm__warps_active.avg.per_cycle_active"]
 
 
 def summary(path):
@@ -22,6 +25,12 @@ def summary(path):
         for k in KEYS:
             if k in d:
                 item[k] = f"{d[k]} {u[k]}".strip()
+        try:   # SIMT efficiency: active threads per executed warp instruction
+            ti = float(d.get("sass__thread_inst_executed_per_opcode_category", "nan").replace(",", ""))
+            wi = float(d.get("smsp__inst_executed.sum", "nan").replace(",", ""))
+            item["threads_per_warp_instruction"] = f"{ti / wi:.1f} of 32 ({100 * ti / wi / 32:.0f} % SIMT efficiency)"
+        except (ValueError, ZeroDivisionError):
+            pass
         stalls = {h.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(d[h] or 0) for h in hdr
                   if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued")}
         tot = sum(stalls.values()) or 1
