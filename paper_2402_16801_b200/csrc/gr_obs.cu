@@ -600,6 +600,9 @@ struct TileSmem {
   uint32_t desc[DESC_WORDS];
 };
 
+#ifndef GR_OBS_WIN_EARLY
+#define GR_OBS_WIN_EARLY 1   // symbolic writer: next env's window loads issued before the scatter
+#endif
 template <bool EXT>
 __host__ __device__ constexpr int stage_warps() { return EXT ? 2 : 8; }
 // one stage = one whole row + up to 3 floats of alignment shift
@@ -715,6 +718,15 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
     float* row = (float*)a.out + (size_t)i * O::L;
     const int shift = (int)((reinterpret_cast<uintptr_t>(row) & 15u) >> 2);
     float* sr = stage + shift;
+#if GR_OBS_WIN_EARLY
+    // the next env's window loads are issued before this row's scatter (its
+    // descriptor had the whole build to arrive), so they overlap the
+    // scatter, the drain and the unscatter
+    have = settle(jn, in, dwn, dn);
+    if (have)
+      load_window<EXT>(S, in, __shfl_sync(0xffffffffu, dwn.y, D_POS / 2),
+                       __shfl_sync(0xffffffffu, dwn.x, D_FLAGS / 2), lane, bqn, iqn);
+#endif
     for (int t = lane; t < O::T; t += 32) {
       const uint32_t g = v.tgt[t];
       float* tv = sr + t * O::STRIDE;
@@ -726,7 +738,9 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
       tv[O::STRIDE - 1] = v.light[t];
     }
     for (int k = lane; k < O::NINV; k += 32) sr[O::T * O::STRIDE + k] = __uint_as_float(v.desc[D_INV + k]);
+#if !GR_OBS_WIN_EARLY
     have = settle(jn, in, dwn, dn);
+#endif
     if (tma) {
       // extended rows are 33,072 B = a 16-byte multiple at 16-byte aligned
       // addresses: one TMA bulk store (cp.async.bulk) per row, issued by one
@@ -739,16 +753,20 @@ __global__ void __launch_bounds__(stage_warps<EXT>() * 32) k_symbolic_stage(DS S
                      :: "l"(row), "r"(saddr), "r"((uint32_t)(O::L * 4)) : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
+#if !GR_OBS_WIN_EARLY
       // the next env's window loads overlap the drain of this row
       if (have)
         load_window<EXT>(S, in, __shfl_sync(0xffffffffu, dwn.y, D_POS / 2),
                          __shfl_sync(0xffffffffu, dwn.x, D_FLAGS / 2), lane, bqn, iqn);
+#endif
       if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncwarp();
     } else {
+#if !GR_OBS_WIN_EARLY
       if (have)
         load_window<EXT>(S, in, __shfl_sync(0xffffffffu, dwn.y, D_POS / 2),
                          __shfl_sync(0xffffffffu, dwn.x, D_FLAGS / 2), lane, bqn, iqn);
+#endif
       __syncwarp();
       const int head = (4 - shift) & 3;
       if (lane < head) row[lane] = sr[lane];
