@@ -562,3 +562,36 @@ def test_tiny_and_ragged_batches(torch_cuda, oracle_lib, tier, obs_mode, n):
         assert np.array_equal(rew.cpu().numpy(), r2.astype(np.float32)), f"reward step {k}"
         assert np.array_equal(obs.cpu().numpy(), ref()), f"obs step {k}"
     _cmp_state(O, gb, ob.state, tier, n)
+
+
+@pytest.mark.parametrize("tier,n,max_len", [("extended", 1024, None), ("extended", 2048, 12), ("classic", 1024, 9)])
+def test_small_batch_paths_match_plain_path(torch_cuda, monkeypatch, tier, n, max_len):
+    """The small-batch step (speculative pool worldgen beside k_step, 512-thread
+    extended worldgen) produces exactly what the plain step does: same rewards,
+    dones, observations and final state, including steps where the done count
+    outruns the speculation (max_episode_length: every env resets at once)."""
+    import torch
+    from paper_2402_16801_b200 import GridrogueBatch
+
+    def run(spec, wide):
+        monkeypatch.setenv("GR_SPEC", spec)
+        monkeypatch.setenv("GR_WG_WIDE", wide)
+        gb = GridrogueBatch(n, tier, 5, "symbolic", max_episode_length=max_len)
+        gb.set_validate(False)
+        obs0 = gb.reset().clone()
+        out = [obs0]
+        for t in range(40):
+            gb.random_actions(5, t)
+            obs, rew, done, *_ = gb.step(gb.actions)
+            out += [obs.clone(), rew.clone(), done.clone()]
+        st = gb.export_state()
+        counters = gb.worldgen_counters()
+        return out, st, counters
+
+    a, sa, ca = run("1", "1")
+    b, sb, cb = run("0", "0")
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    for k in sb:
+        assert np.array_equal(sa[k], sb[k]), k
+    assert ca["worlds"] >= cb["worlds"]   # the speculative pass may make a few unused worlds
