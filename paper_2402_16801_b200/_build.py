@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libgridrogue_b200.so")
-SOURCES = ["gr_step.cu", "gr_world.cu", "gr_world_wide.cu", "gr_reset.cu", "gr_obs.cu", "gr_levels.cu", "gr_api.cu"]
+SOURCES = ["gr_step.cu", "gr_world.cu", "gr_world_wide.cu", "gr_reset.cu", "gr_obs.cu", "gr_levels.cu", "gr_api.cu", "gr_ppo.cu"]
 
 # -fmad=false: no contraction of float mul+add (numpy evaluates them separately);
 # IEEE div/sqrt are nvcc's defaults and fast-math is never enabled.
@@ -45,6 +45,7 @@ def _stale() -> bool:
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps.append(os.path.join(HERE, "..", "include", "gridrogue_b200.h"))
+    deps.append(os.path.join(HERE, "..", "include", "gridrogue_ppo.h"))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 

@@ -120,6 +120,9 @@ def lib() -> ctypes.CDLL:
         "gr_worldgen_counters": (I32, [P, ctypes.POINTER(I64)]),
         "gr_set_profiling": (I32, [P, I32]),
         "gr_kernel_times": (I32, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64), I32]),
+        # include/gridrogue_ppo.h (the learner's fused objective)
+        "grp_ppo_loss": (I32, [P, P, P, P, P, P, P, I32, I32, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                               P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -55,6 +55,7 @@ class PPOConfig:
     seed: int = 0
     bf16: bool = True             # autocast the MLPs to bf16 (tensor cores)
     graphs: bool = True           # one GPU: rollout step, GAE and minibatch update as CUDA graphs
+    fused_loss: bool = True       # graphed learner: PPO objective + gradient in one CUDA kernel (gr_ppo.cu)
 
 
 def gae(rewards, values, dones, last_value, gamma: float, lam: float):
@@ -256,6 +257,57 @@ def train(cfg: PPOConfig, log=print, max_updates: int | None = None) -> dict:
     return result
 
 
+_OBJECTIVE = None
+
+
+def _objective_fn():
+    """torch.autograd.Function over the fused kernel (built once)."""
+    global _OBJECTIVE
+    if _OBJECTIVE is not None:
+        return _OBJECTIVE
+    import torch
+    from ._lib import lib
+
+    class _Objective(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, z, v, actions, logp_old, adv, values_old, returns, clip_eps, vf_coef, ent_coef):
+            B, NA = z.shape
+            dz = torch.empty_like(z)
+            dv = torch.empty_like(v)
+            out = torch.zeros(4, dtype=torch.float32, device=z.device)
+            stream = torch.cuda.current_stream(z.device).cuda_stream
+            rc = lib().grp_ppo_loss(z.data_ptr(), v.data_ptr(), actions.data_ptr(), logp_old.data_ptr(),
+                                    adv.data_ptr(), values_old.data_ptr(), returns.data_ptr(), B, NA,
+                                    clip_eps, vf_coef, ent_coef, dz.data_ptr(), dv.data_ptr(), out.data_ptr(),
+                                    stream)
+            if rc != 0:
+                raise RuntimeError(f"grp_ppo_loss failed ({rc}): n_actions {NA}, batch {B}")
+            ctx.save_for_backward(dz, dv)
+            loss = out[0].clone()
+            ctx.mark_non_differentiable(out)
+            return loss, out
+
+        @staticmethod
+        def backward(ctx, g_loss, g_out):
+            dz, dv = ctx.saved_tensors
+            return dz * g_loss, dv * g_loss, None, None, None, None, None, None, None, None
+
+    _OBJECTIVE = _Objective
+    return _OBJECTIVE
+
+
+def ppo_objective(logits, values, actions, logp_old, adv, values_old, returns, clip_eps: float,
+                  vf_coef: float, ent_coef: float):
+    """The PPO minibatch objective through the fused kernel
+    (include/gridrogue_ppo.h): returns (loss, stats = [loss, pg, vl,
+    entropy]); d loss / d logits and d loss / d values come from the same
+    launch.  The advantages are normalised over the minibatch inside."""
+    z = logits.float().contiguous()
+    v = values.float().contiguous()
+    args = [t.contiguous() for t in (actions, logp_old, adv, values_old, returns)]
+    return _objective_fn().apply(z, v, *args, float(clip_eps), float(vf_coef), float(ent_coef))
+
+
 def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
     """Single-GPU PPO with every per-step launch sequence replayed as a CUDA graph.
 
@@ -378,6 +430,15 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
     def mb_step():
         idx = idx_s
         logits, v = policy(b_obs.index_select(0, idx))
+        if cfg.fused_loss:
+            loss, st = ppo_objective(logits, v, b_act.index_select(0, idx), b_logp.index_select(0, idx),
+                                     b_adv.index_select(0, idx), b_val.index_select(0, idx),
+                                     b_ret.index_select(0, idx), cfg.clip_eps, cfg.vf_coef, cfg.ent_coef)
+            loss.backward()
+            torch.nn.utils.clip_grad_norm_(params, cfg.max_grad_norm, foreach=True)
+            opt.step()
+            stats_s.copy_(st)
+            return
         logp_all = torch.log_softmax(logits, -1)
         logp = logp_all.gather(-1, b_act.index_select(0, idx)[:, None]).squeeze(-1)
         ratio = torch.exp(logp - b_logp.index_select(0, idx))

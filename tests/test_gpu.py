@@ -595,3 +595,45 @@ def test_small_batch_paths_match_plain_path(torch_cuda, monkeypatch, tier, n, ma
     for k in sb:
         assert np.array_equal(sa[k], sb[k]), k
     assert ca["worlds"] >= cb["worlds"]   # the speculative pass may make a few unused worlds
+
+
+@pytest.mark.parametrize("n_actions", [17, 43])
+def test_fused_ppo_objective_matches_torch(torch_cuda, n_actions):
+    """The fused PPO objective kernel (gr_ppo.cu) against a plain PyTorch fp32
+    statement of the same loss: value and gradients (tolerance 1e-5 relative
+    on the loss terms, 1e-6 absolute on the gradients)."""
+    import torch
+    from paper_2402_16801_b200.ppo import ppo_objective
+    g = torch.Generator(device="cuda").manual_seed(n_actions)
+    B = 8192
+    z = torch.randn(B, n_actions, device="cuda", generator=g) * 2
+    v = torch.randn(B, device="cuda", generator=g)
+    act = torch.randint(0, n_actions, (B,), device="cuda", generator=g)
+    logp_old = torch.log_softmax(z + 0.3 * torch.randn(B, n_actions, device="cuda", generator=g), -1).gather(
+        -1, act[:, None]).squeeze(-1)
+    adv = torch.randn(B, device="cuda", generator=g) * 3 + 0.5
+    v_old = v + 0.3 * torch.randn(B, device="cuda", generator=g)
+    ret = v + torch.randn(B, device="cuda", generator=g)
+    eps, cv, ce = 0.2, 0.5, 0.01
+
+    z1, v1 = z.clone().requires_grad_(), v.clone().requires_grad_()
+    loss1, st = ppo_objective(z1, v1, act, logp_old, adv, v_old, ret, eps, cv, ce)
+    loss1.backward()
+
+    z2, v2 = z.clone().requires_grad_(), v.clone().requires_grad_()
+    lp_all = torch.log_softmax(z2, -1)
+    lp = lp_all.gather(-1, act[:, None]).squeeze(-1)
+    ratio = torch.exp(lp - logp_old)
+    a_ = (adv - adv.mean()) / (adv.std() + 1e-8)
+    pg = -torch.min(ratio * a_, ratio.clamp(1 - eps, 1 + eps) * a_).mean()
+    vc = v_old + (v2 - v_old).clamp(-eps, eps)
+    vl = 0.5 * torch.max((v2 - ret) ** 2, (vc - ret) ** 2).mean()
+    ent = -(lp_all.exp() * lp_all).sum(-1).mean()
+    loss2 = pg + cv * vl - ce * ent
+    loss2.backward()
+
+    ref = torch.stack([loss2, pg, vl, ent]).detach()
+    assert torch.allclose(st, ref, rtol=1e-5, atol=1e-6), (st, ref)
+    assert torch.allclose(loss1.detach(), loss2.detach(), rtol=1e-5, atol=1e-6)
+    assert torch.allclose(z1.grad, z2.grad, rtol=1e-4, atol=1e-6), (z1.grad - z2.grad).abs().max()
+    assert torch.allclose(v1.grad, v2.grad, rtol=1e-4, atol=1e-6), (v1.grad - v2.grad).abs().max()
