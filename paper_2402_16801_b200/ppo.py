@@ -319,8 +319,10 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
         value, the previous step's reward / done), then the env step (the
         library's own captured step graph);
       * GAE over the rollout = one graph;
-      * each minibatch = one graph (gather, forward, clipped losses,
-        backward, global-norm clip, Adam with a device-side learning rate).
+      * the whole update = one graph: per epoch a device permutation, then
+        per minibatch the gather, forward, the fused PPO objective
+        (gr_ppo.cu: loss and its logits / value gradients in one kernel),
+        backward, global-norm clip and Adam with a device-side learning rate.
     Same algorithm and hyper-parameters as the eager loop; the sampling
     noise comes from torch's graph-safe generator (Gumbel-max instead of
     multinomial), so runs are not bitwise equal to eager ones.
@@ -455,7 +457,17 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
         opt.step()
         stats_s.copy_(torch.stack([loss.detach(), pg.detach(), vl.detach(), ent.detach()]))
 
-    g_roll, g_gae, g_mb = None, None, None
+    def update_epochs(eager: bool):
+        stats_acc.zero_()
+        for _ in range(cfg.update_epochs):
+            perm = torch.rand(batch_size, device=dev).argsort()   # on the device (randperm builds it on the host)
+            for k in range(cfg.n_minibatches):
+                idx_s.copy_(perm[k * mb:(k + 1) * mb])
+                opt.zero_grad(set_to_none=eager)
+                mb_step()
+                stats_acc.add_(stats_s)
+
+    g_roll, g_gae, g_upd = None, None, None
     pool = None
 
     def capture(fn, *args):
@@ -491,27 +503,13 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
                 g_gae.replay()
         ev[1].record()
         # --- update ----------------------------------------------------------
-        stats_acc.zero_()
-        for ep in range(cfg.update_epochs):
-            perm = torch.rand(batch_size, device=dev).argsort()   # on the device (randperm builds it on the host)
-            for k in range(cfg.n_minibatches):
-                idx_s.copy_(perm[k * mb:(k + 1) * mb])
-                if g_mb is not None:
-                    g_mb.replay()
-                elif upd == 0 and ep == 0 and k == 3:
-                    # three eager minibatches above warmed autograd / cuBLAS
-                    # up; capture (captures do not execute) and replay
-                    torch.cuda.synchronize()
-                    opt.zero_grad(set_to_none=True)
-                    g_mb = capture(mb_step)
-                    g_mb.replay()
-                else:
-                    side.wait_stream(torch.cuda.current_stream())
-                    with torch.cuda.stream(side):
-                        opt.zero_grad(set_to_none=True)
-                        mb_step()
-                    torch.cuda.current_stream().wait_stream(side)
-                stats_acc.add_(stats_s)
+        if g_upd is not None:
+            g_upd.replay()
+        else:   # update 0 runs eagerly (warming autograd / cuBLAS / Adam state up)
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                update_epochs(eager=True)
+            torch.cuda.current_stream().wait_stream(side)
         if g_roll is None:   # after the eager warm-up update: capture the rollout and GAE
             torch.cuda.synchronize()
             with torch.no_grad():
@@ -524,6 +522,10 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
                 pool = torch.cuda.graph_pool_handle() if pool is None else pool
                 g_roll = [capture(roll_step, t) for t in range(T + 1)]
                 g_gae = capture(gae_step)
+            # the whole update (4 epochs x 8 minibatches: permutation, gather,
+            # objective, backward, clip, Adam) as one graph; the gradients stay
+            # the tensors the eager update allocated, zeroed in the graph
+            g_upd = capture(update_epochs, False)
         ev[2].record()
         steps_done += batch_size
         if upd % 10 == 0 or upd == n_updates - 1:
