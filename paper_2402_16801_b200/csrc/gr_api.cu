@@ -326,8 +326,14 @@ int gr_create(const gr_config* cfg, gr_env** out) {
     // env-steps/s, extended 4,096 28.7 -> 31.8 M; extended 16,384 88 ->
     // 81 M and 65,536 139 -> 110 M (the speculative CTAs crowd k_step and
     // the writer, and the extra worlds cost more than the hidden latency)
-    // (classic 4,096 envs with pixels: 59.7 -> 57.1 M, so classic stops at 1,024)
-    e->spec_on = e->nb <= (e->ext ? 32 : 8) && ng == cfg->n_envs;
+    // classic (one 64x64 floor per world, 256-thread worldgen CTAs) without
+    // pixels gains at every size: symbolic 65,536 envs 414 -> 423 M, 16,384
+    // 178 -> 204 M; obs off 65,536 749 -> 829 M, 4,096 74 -> 92 M.  Classic
+    // pixels lose beyond 1,024 envs (4,096: 59.7 -> 57.1 M, 65,536: 171 -> 166 M)
+    // Extended without observations (the reset chain follows k_step with no
+    // writer to hide behind) gains too: 65,536 envs 288 -> 299 M.
+    const bool any_size = cfg->obs_mode == GR_OBS_NONE || (!e->ext && cfg->obs_mode != GR_OBS_PIXELS);
+    e->spec_on = (any_size || e->nb <= (e->ext ? 32 : 8)) && ng == cfg->n_envs;
     if (const char* sp = getenv("GR_SPEC")) e->spec_on = atoi(sp) != 0 && ng == cfg->n_envs;
     e->wg_wide = e->nb <= 32;
     if (const char* ww = getenv("GR_WG_WIDE")) e->wg_wide = atoi(ww) != 0;
