@@ -73,6 +73,7 @@ struct WSmem {
   int spawn;
   int cr[8], cc[8];
   int room[8][4];
+  uint64_t rowmask[WT<EXT>::H];            // dungeon: room columns per row
 };
 
 // ------------------------------------------------------- block reductions
@@ -195,7 +196,16 @@ __device__ __noinline__ int block_excl_scan(SM& sm, int v, int* total) {
 template <bool EXT>
 __device__ __noinline__ unsigned long long census(WSmem<EXT>& sm) {
   unsigned long long m = 0;
-  for (int t = threadIdx.x; t < WT<EXT>::HW; t += WT<EXT>::THREADS) m |= 1ull << sm.blk[t];
+  // 16 tiles per shared-memory load (block ids < 64)
+  const uint4* b4 = reinterpret_cast<const uint4*>(sm.blk);
+  for (int q = threadIdx.x; q < WT<EXT>::HW / 16; q += WT<EXT>::THREADS) {
+    const uint4 x = b4[q];
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) m |= 1ull << ((w[k] >> (8 * j)) & 63u);
+  }
   return block_or_u64(sm, m);
 }
 
@@ -487,11 +497,18 @@ __device__ __noinline__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floo
     sm.room[k][0] = r0; sm.room[k][1] = r0 + rh; sm.room[k][2] = c0; sm.room[k][3] = c0 + rw;
   }
   __syncthreads();
+  // the rooms as one column bitmask per row, then one lookup per tile
+  for (int r = threadIdx.x; r < T::H; r += WT<EXT>::THREADS) {
+    uint64_t m = 0;
+    for (int k = 0; k < n; ++k)
+      if (r >= sm.room[k][0] && r < sm.room[k][1])
+        m |= ((1ull << (sm.room[k][3] - sm.room[k][2])) - 1ull) << sm.room[k][2];
+    sm.rowmask[r] = m;
+  }
+  __syncthreads();
   for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS) {
     const int r = t / T::W, c = t % T::W;
-    bool in = false;
-    for (int k = 0; k < n; ++k)
-      in |= r >= sm.room[k][0] && r < sm.room[k][1] && c >= sm.room[k][2] && c < sm.room[k][3];
+    const bool in = (sm.rowmask[r] >> c) & 1ull;
     sm.blk[t] = in ? B_PATH : B_WALL;
     sm.itm[t] = 0;
   }
