@@ -25,6 +25,21 @@ int grp_ppo_loss(const float* logits, const float* values, const int64_t* action
                  int32_t n_actions, float clip_eps, float vf_coef, float ent_coef, float* dlogits,
                  float* dvalues, float* out, void* stream);
 
+/* One rollout step's action sampling, one launch on `stream`: actions ~
+ * Categorical(softmax(logits[n, n_actions])) by Gumbel-max with
+ * counter-based uniforms keyed by (seed, *counter, t, env, action) -- no
+ * generator state, so the call replays inside a CUDA graph; writes the
+ * actions to actions_a (and actions_b if not null), log p(action) to logp
+ * and values[env * ld_values] to value; when reward_out is not null also
+ * copies prev_reward -> reward_out and prev_done (uint8) -> done_out (float).
+ * logits / values are bf16 (bf16 != 0) or float32, row strides ld_*.
+ * Returns 0, -1 (unsupported n_actions / n <= 0), -2 (launch error). */
+int grp_sample_actions(const void* logits, const void* values, int32_t bf16, int32_t n, int32_t n_actions,
+                       int64_t ld_logits, int64_t ld_values, uint64_t seed, const unsigned long long* counter,
+                       uint32_t t, int64_t* actions_a, int64_t* actions_b, float* logp, float* value,
+                       const float* prev_reward, const uint8_t* prev_done, float* reward_out, float* done_out,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

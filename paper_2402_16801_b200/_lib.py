@@ -123,6 +123,8 @@ def lib() -> ctypes.CDLL:
         # include/gridrogue_ppo.h (the learner's fused objective)
         "grp_ppo_loss": (I32, [P, P, P, P, P, P, P, I32, I32, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                P, P, P, P]),
+        "grp_sample_actions": (I32, [P, P, I32, I32, I32, I64, I64, U64, P, ctypes.c_uint32, P, P, P, P, P, P,
+                                     P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "../../include/gridrogue_ppo.h"
@@ -179,6 +180,82 @@ __global__ void __launch_bounds__(THREADS) k_ppo_loss(const float* __restrict__ 
   }
 }
 
+
+// ---------------------------------------------------------------- sampling
+// One rollout step's action sampling: a ~ Categorical(softmax(logits)) by
+// Gumbel-max with counter-based uniforms (splitmix64 / lowbias32 of (seed,
+// *counter, t, env, action) -- no generator state, so the step replays as a
+// CUDA graph), log p(a), the value, and the previous step's reward / done
+// into the rollout buffers.  One warp per env.
+__device__ __forceinline__ uint64_t smix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
+  x ^= x >> 16; x *= 0x7FEB352Du; x ^= x >> 15; x *= 0x846CA68Bu; x ^= x >> 16;
+  return x;
+}
+
+template <int NA, typename TI>
+__global__ void __launch_bounds__(THREADS) k_sample(const TI* __restrict__ logits, const TI* __restrict__ values,
+                                                    int n, int64_t ldl, int64_t ldv, uint64_t seed,
+                                                    const unsigned long long* __restrict__ counter, uint32_t t,
+                                                    int64_t* __restrict__ act_a, int64_t* __restrict__ act_b,
+                                                    float* __restrict__ logp_out, float* __restrict__ v_out,
+                                                    const float* __restrict__ prev_rew, const uint8_t* __restrict__ prev_done,
+                                                    float* __restrict__ rew_out, float* __restrict__ done_out) {
+  constexpr int PER = (NA + 31) / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int env = blockIdx.x * (THREADS / 32) + warp;
+  if (env >= n) return;
+  const uint64_t key = smix64(seed ^ smix64((uint64_t)*counter * 0x100000001B3ull + t));
+  const uint32_t k32 = (uint32_t)key ^ (uint32_t)(key >> 32);
+  float zl[PER];
+  float m = -INFINITY, best = -INFINITY;
+  int arg = 0x7fffffff;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int j = lane + 32 * k;
+    zl[k] = j < NA ? (float)logits[(size_t)env * ldl + j] : -INFINITY;
+    m = fmaxf(m, zl[k]);
+    if (j < NA) {
+      const uint32_t h = lowbias32(k32 ^ ((uint32_t)(env * NA + j) * 0x9E3779B9u + 0x9E3779B9u));
+      const float u = fmaxf(((float)(h >> 8) + 0.5f) * 5.9604644775390625e-08f, 1e-20f);   // (0, 1)
+      const float g = zl[k] - logf(-logf(u));
+      if (g > best) { best = g; arg = j; }
+    }
+  }
+  // argmax over lanes (first index on ties)
+  for (int o = 16; o; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+  }
+  m = warp_max(m);
+  float se = 0.f;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) se += lane + 32 * k < NA ? expf(zl[k] - m) : 0.f;
+  se = warp_sum(se);
+  float za = 0.f;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const float zk = __shfl_sync(0xffffffffu, zl[k], arg & 31);
+    if (k == arg / 32) za = zk;
+  }
+  if (lane == 0) {
+    act_a[env] = arg;
+    if (act_b) act_b[env] = arg;
+    logp_out[env] = za - (m + logf(se));
+    v_out[env] = (float)values[(size_t)env * ldv];
+    if (rew_out) {
+      rew_out[env] = prev_rew[env];
+      done_out[env] = (float)prev_done[env];
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" int grp_ppo_loss(const float* logits, const float* v, const int64_t* actions, const float* logp_old,
@@ -204,5 +281,34 @@ extern "C" int grp_ppo_loss(const float* logits, const float* v, const int64_t* 
       return -1;
   }
 #undef GRP_CASE
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+extern "C" int grp_sample_actions(const void* logits, const void* values, int32_t bf16, int32_t n, int32_t n_actions,
+                                  int64_t ld_logits, int64_t ld_values, uint64_t seed,
+                                  const unsigned long long* counter, uint32_t t, int64_t* actions_a,
+                                  int64_t* actions_b, float* logp, float* value, const float* prev_reward,
+                                  const uint8_t* prev_done, float* reward_out, float* done_out, void* stream) {
+  if (n <= 0) return -1;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = (n + THREADS / 32 - 1) / (THREADS / 32);
+#define GRS_CASE(N)                                                                                             \
+  case N:                                                                                                       \
+    if (bf16)                                                                                                   \
+      k_sample<N, __nv_bfloat16><<<grid, THREADS, 0, st>>>(                                                     \
+          (const __nv_bfloat16*)logits, (const __nv_bfloat16*)values, n, ld_logits, ld_values, seed, counter, t, \
+          actions_a, actions_b, logp, value, prev_reward, prev_done, reward_out, done_out);                     \
+    else                                                                                                        \
+      k_sample<N, float><<<grid, THREADS, 0, st>>>((const float*)logits, (const float*)values, n, ld_logits,   \
+                                                   ld_values, seed, counter, t, actions_a, actions_b, logp,    \
+                                                   value, prev_reward, prev_done, reward_out, done_out);       \
+    break;
+  switch (n_actions) {
+    GRS_CASE(17)
+    GRS_CASE(43)
+    default:
+      return -1;
+  }
+#undef GRS_CASE
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

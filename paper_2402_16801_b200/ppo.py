@@ -56,6 +56,7 @@ class PPOConfig:
     bf16: bool = True             # autocast the MLPs to bf16 (tensor cores)
     graphs: bool = True           # one GPU: rollout step, GAE and minibatch update as CUDA graphs
     fused_loss: bool = True       # graphed learner: PPO objective + gradient in one CUDA kernel (gr_ppo.cu)
+    fused_sampler: bool = True    # graphed learner: action sampling + rollout-buffer writes in one kernel
 
 
 def gae(rewards, values, dones, last_value, gamma: float, lam: float):
@@ -379,8 +380,13 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
     lin_ix = [(k, k + 1) for k in range(0, len(params), 2)]   # (weight, bias) per Linear, module order
 
     def roll_policy(x):
+        ha, hc = roll_policy_raw(x)
+        return ha.float(), hc.float().squeeze(-1)
+
+    def roll_policy_raw(x):
         """Rollout forward on the pre-cast weights (module order: first,
-        actor 2 + head, critic 2 + head)."""
+        actor 2 + head, critic 2 + head); logits [N, A] and values [N, 1] in
+        the rollout dtype."""
         F = torch.nn.functional
         (w0, b0), rest = lin_ix[0], lin_ix[1:]
         h = torch.tanh(F.linear(x, roll_w[w0], roll_w[b0]))
@@ -395,14 +401,17 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
             hc = F.linear(hc, roll_w[w], roll_w[b])
             if j < na - 1:
                 hc = torch.tanh(hc)
-        return ha.float(), hc.float().squeeze(-1)
+        return ha, hc
+
+    rng_ctr = torch.zeros(1, dtype=torch.int64, device=dev)   # sampler counter, one per rollout
 
     def refresh_roll_w():
         for dst, src in zip(roll_w, params):
             dst.copy_(src.detach())
+        rng_ctr.add_(1)
 
     def roll_step(t):
-        if t > 0:
+        if t > 0 and (t == T or not cfg.fused_sampler):
             buf_rew[t - 1].copy_(gb.reward)
             buf_done[t - 1].copy_(gb.done)
         if t == T:   # closing step: the bootstrap value
@@ -411,6 +420,22 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
             last_v.copy_(v)
             return
         buf_obs[t, :, :obs_dim].copy_(gb.obs)
+        if cfg.fused_sampler:
+            # sampling, log-prob, value and the previous reward / done in one
+            # launch (gr_ppo.cu): the step's other ~15 small kernels
+            from ._lib import lib
+            za, zv = roll_policy_raw(buf_obs[t])
+            prev = t > 0
+            rc = lib().grp_sample_actions(
+                za.data_ptr(), zv.data_ptr(), 1 if za.dtype == torch.bfloat16 else 0, n, n_actions, za.stride(0),
+                zv.stride(0), (cfg.seed * 0x9E3779B97F4A7C15 + 1) & 0xFFFFFFFFFFFFFFFF, rng_ctr.data_ptr(), t,
+                gb.actions.data_ptr(), buf_act[t].data_ptr(), buf_logp[t].data_ptr(), buf_val[t].data_ptr(),
+                gb.reward.data_ptr() if prev else None, gb.done.data_ptr() if prev else None,
+                buf_rew[t - 1].data_ptr() if prev else None, buf_done[t - 1].data_ptr() if prev else None,
+                torch.cuda.current_stream(dev).cuda_stream)
+            if rc != 0:
+                raise RuntimeError(f"grp_sample_actions failed ({rc})")
+            return
         logits, v = roll_policy(buf_obs[t])
         u = torch.rand_like(logits).clamp_(min=1e-20)
         a = (logits - torch.log(-torch.log(u))).argmax(-1)

@@ -637,3 +637,41 @@ def test_fused_ppo_objective_matches_torch(torch_cuda, n_actions):
     assert torch.allclose(loss1.detach(), loss2.detach(), rtol=1e-5, atol=1e-6)
     assert torch.allclose(z1.grad, z2.grad, rtol=1e-4, atol=1e-6), (z1.grad - z2.grad).abs().max()
     assert torch.allclose(v1.grad, v2.grad, rtol=1e-4, atol=1e-6), (v1.grad - v2.grad).abs().max()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_fused_sampler_distribution(torch_cuda, dtype):
+    """grp_sample_actions: actions follow softmax(logits) (empirical
+    frequencies within 5 sigma over 65,536 draws), log p(a) equals the torch
+    log-softmax, values and the previous reward / done are copied."""
+    import torch
+    from paper_2402_16801_b200._lib import lib
+    n, A = 65536, 43
+    g = torch.Generator(device="cuda").manual_seed(3)
+    row = torch.randn(A, device="cuda", generator=g) * 1.5
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    z = row.to(dt).expand(n, A).contiguous()
+    v = torch.randn(n, 1, device="cuda", generator=g).to(dt)
+    ctr = torch.tensor([7], dtype=torch.int64, device="cuda")
+    a1 = torch.empty(n, dtype=torch.int64, device="cuda")
+    a2 = torch.empty_like(a1)
+    lp = torch.empty(n, device="cuda")
+    vo = torch.empty(n, device="cuda")
+    pr = torch.randn(n, device="cuda", generator=g)
+    pd = (torch.rand(n, device="cuda", generator=g) < 0.3).to(torch.uint8)
+    ro, do = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
+    rc = lib().grp_sample_actions(z.data_ptr(), v.data_ptr(), 1 if dtype == "bf16" else 0, n, A, A, 1, 12345,
+                                  ctr.data_ptr(), 5, a1.data_ptr(), a2.data_ptr(), lp.data_ptr(), vo.data_ptr(),
+                                  pr.data_ptr(), pd.data_ptr(), ro.data_ptr(), do.data_ptr(),
+                                  torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert rc == 0
+    assert torch.equal(a1, a2) and int(a1.min()) >= 0 and int(a1.max()) < A
+    p = torch.softmax(z[0].float(), -1)
+    freq = torch.bincount(a1, minlength=A).float() / n
+    sigma = torch.sqrt(p * (1 - p) / n)
+    assert bool(((freq - p).abs() <= 5 * sigma + 1e-4).all()), (freq - p).abs().max()
+    ref_lp = torch.log_softmax(z.float(), -1).gather(-1, a1[:, None]).squeeze(-1)
+    assert torch.allclose(lp, ref_lp, rtol=1e-5, atol=1e-6)
+    assert torch.equal(vo, v.float().squeeze(-1))
+    assert torch.equal(ro, pr) and torch.equal(do, pd.float())
