@@ -143,11 +143,11 @@ def train(cfg: PPOConfig, log=print, max_updates: int | None = None) -> dict:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if cfg.graphs and world == 1:
-        return _train_graphed(cfg, log, max_updates)
     dev = torch.device("cuda", local)
     if world > 1 and not dist.is_initialized():
         dist.init_process_group("nccl", device_id=dev)
+    if cfg.graphs:
+        return _train_graphed(cfg, log, max_updates)
     torch.manual_seed(cfg.seed + rank)
 
     n, T = cfg.n_envs, cfg.n_steps
@@ -324,17 +324,29 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
         per minibatch the gather, forward, the fused PPO objective
         (gr_ppo.cu: loss and its logits / value gradients in one kernel),
         backward, global-norm clip and Adam with a device-side learning rate.
+    Several GPUs (torchrun, one process each): every rank owns a shard of
+    the global batch (parallel.ShardedBatch); each minibatch is then two
+    graphs around one all-reduce of a flat gradient buffer (the parameters'
+    .grad tensors are views into it), the average taken in the second graph.
     Same algorithm and hyper-parameters as the eager loop; the sampling
-    noise comes from torch's graph-safe generator (Gumbel-max instead of
-    multinomial), so runs are not bitwise equal to eager ones.
+    noise comes from counter-based hashes (Gumbel-max), so runs are not
+    bitwise equal to eager ones.
     """
     import torch
     from .env import TIERS, GridrogueBatch
 
+    import torch.distributed as dist
     dev = torch.device("cuda", torch.cuda.current_device())
-    torch.manual_seed(cfg.seed)
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    torch.manual_seed(cfg.seed)   # the same initial weights on every rank
     n, T = cfg.n_envs, cfg.n_steps
-    gb = GridrogueBatch(n, cfg.tier, cfg.seed, "symbolic", newly=False, info=False)
+    if world > 1:
+        from .parallel import ShardedBatch
+        env = ShardedBatch(n * world, cfg.tier, cfg.seed, "symbolic")
+        gb = env.batch
+    else:
+        env = gb = GridrogueBatch(n, cfg.tier, cfg.seed, "symbolic", newly=False, info=False)
     gb.set_validate(False)   # actions are sampled in range
     t_info = TIERS[cfg.tier]
     obs_dim, n_actions = t_info["obs"], t_info["n_actions"]
@@ -345,13 +357,22 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
     obs_pad = (obs_dim + 63) // 64 * 64
     model = make_fused_model(obs_pad, n_actions, cfg.layer_size).to(dev)
     params = list(model.parameters())
+    # gradients as views of one flat buffer: one all-reduce per minibatch
+    flat_grad = torch.zeros(sum(p.numel() for p in params), dtype=torch.float32, device=dev)
+    off = 0
+    for p_ in params:
+        p_.grad = flat_grad[off:off + p_.numel()].view_as(p_)
+        off += p_.numel()
+    if world > 1:
+        for p_ in params:
+            dist.broadcast(p_.data, 0)
     # rollout weights: bf16 copies refreshed once per rollout (the weights do
     # not change within one), so the 64 per-step graphs cast nothing
     roll_w = [p.detach().to(torch.bfloat16 if cfg.bf16 else torch.float32) for p in params]
     lr_t = torch.tensor(cfg.lr, dtype=torch.float32, device=dev)
     opt = torch.optim.Adam(params, lr=lr_t, eps=1e-5, capturable=True, fused=True)
     batch_size = n * T
-    n_updates = max(1, cfg.total_timesteps // batch_size)
+    n_updates = max(1, cfg.total_timesteps // (batch_size * world))
     if max_updates is not None:
         n_updates = min(n_updates, max_updates)
     mb = batch_size // cfg.n_minibatches
@@ -428,7 +449,7 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
             prev = t > 0
             rc = lib().grp_sample_actions(
                 za.data_ptr(), zv.data_ptr(), 1 if za.dtype == torch.bfloat16 else 0, n, n_actions, za.stride(0),
-                zv.stride(0), (cfg.seed * 0x9E3779B97F4A7C15 + 1) & 0xFFFFFFFFFFFFFFFF, rng_ctr.data_ptr(), t,
+                zv.stride(0), (cfg.seed * 0x9E3779B97F4A7C15 + 1 + rank * 0xD1B54A32D192ED03) & 0xFFFFFFFFFFFFFFFF, rng_ctr.data_ptr(), t,
                 gb.actions.data_ptr(), buf_act[t].data_ptr(), buf_logp[t].data_ptr(), buf_val[t].data_ptr(),
                 gb.reward.data_ptr() if prev else None, gb.done.data_ptr() if prev else None,
                 buf_rew[t - 1].data_ptr() if prev else None, buf_done[t - 1].data_ptr() if prev else None,
@@ -462,8 +483,6 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
                                      b_adv.index_select(0, idx), b_val.index_select(0, idx),
                                      b_ret.index_select(0, idx), cfg.clip_eps, cfg.vf_coef, cfg.ent_coef)
             loss.backward()
-            torch.nn.utils.clip_grad_norm_(params, cfg.max_grad_norm, foreach=True)
-            opt.step()
             stats_s.copy_(st)
             return
         logp_all = torch.log_softmax(logits, -1)
@@ -478,21 +497,39 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
         ent = -(logp_all.exp() * logp_all).sum(-1).mean()
         loss = pg + cfg.vf_coef * vl - cfg.ent_coef * ent
         loss.backward()
-        torch.nn.utils.clip_grad_norm_(params, cfg.max_grad_norm, foreach=True)
-        opt.step()
         stats_s.copy_(torch.stack([loss.detach(), pg.detach(), vl.detach(), ent.detach()]))
 
-    def update_epochs(eager: bool):
+    def mb_opt():
+        if world > 1:
+            flat_grad.div_(world)   # the all-reduce summed the ranks' gradients
+        torch.nn.utils.clip_grad_norm_(params, cfg.max_grad_norm, foreach=True)
+        opt.step()
+
+    def mb_grad():
+        opt.zero_grad(set_to_none=False)   # the .grad views of flat_grad stay
+        mb_step()
+
+    def update_epochs(g_grad=None, g_opt=None):
+        """One update; with world > 1 each minibatch is grad graph ->
+        all-reduce -> optimizer graph (or the eager calls before capture)."""
         stats_acc.zero_()
         for _ in range(cfg.update_epochs):
             perm = torch.rand(batch_size, device=dev).argsort()   # on the device (randperm builds it on the host)
             for k in range(cfg.n_minibatches):
                 idx_s.copy_(perm[k * mb:(k + 1) * mb])
-                opt.zero_grad(set_to_none=eager)
-                mb_step()
+                if g_grad is not None:
+                    g_grad.replay()
+                else:
+                    mb_grad()
+                if world > 1:
+                    dist.all_reduce(flat_grad)
+                if g_opt is not None:
+                    g_opt.replay()
+                else:
+                    mb_opt()
                 stats_acc.add_(stats_s)
 
-    g_roll, g_gae, g_upd = None, None, None
+    g_roll, g_gae, g_upd, g_grad, g_opt = None, None, None, None, None
     pool = None
 
     def capture(fn, *args):
@@ -501,7 +538,7 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
             fn(*args)
         return g
 
-    gb.reset()
+    env.reset()
     history = []
     last_ep, last_ret = 0, 0.0
     t0 = time.perf_counter()
@@ -521,7 +558,7 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
                 else:
                     g_roll[t].replay()
                 if t < T:
-                    gb.step(gb.actions)
+                    env.step(gb.actions)
             if g_gae is None:
                 gae_step()
             else:
@@ -530,10 +567,12 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
         # --- update ----------------------------------------------------------
         if g_upd is not None:
             g_upd.replay()
+        elif g_grad is not None:
+            update_epochs(g_grad, g_opt)
         else:   # update 0 runs eagerly (warming autograd / cuBLAS / Adam state up)
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
-                update_epochs(eager=True)
+                update_epochs()
             torch.cuda.current_stream().wait_stream(side)
         if g_roll is None:   # after the eager warm-up update: capture the rollout and GAE
             torch.cuda.synchronize()
@@ -550,14 +589,18 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
             # the whole update (4 epochs x 8 minibatches: permutation, gather,
             # objective, backward, clip, Adam) as one graph; the gradients stay
             # the tensors the eager update allocated, zeroed in the graph
-            g_upd = capture(update_epochs, False)
+            if world == 1:
+                g_upd = capture(update_epochs)
+            else:
+                g_grad = capture(mb_grad)
+                g_opt = capture(mb_opt)
         ev[2].record()
-        steps_done += batch_size
+        steps_done += batch_size * world
         if upd % 10 == 0 or upd == n_updates - 1:
             torch.cuda.synchronize()
             ms_roll, ms_upd = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
             s = (stats_acc / (cfg.update_epochs * cfg.n_minibatches)).tolist()
-            st = gb.stats()
+            st = env.stats()
             mean_ret = st["total_return"] / max(st["episodes"], 1)
             window = (st["total_return"] - last_ret) / max(st["episodes"] - last_ep, 1)
             last_ep, last_ret = st["episodes"], st["total_return"]
@@ -567,13 +610,15 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
                    "recent_episode_return": window,
                    "ms_rollout": round(ms_roll, 3), "ms_update": round(ms_upd, 3)}
             history.append(row)
-            log(json.dumps(row))
+            if rank == 0:
+                log(json.dumps(row))
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    st = gb.stats()
-    return {"config": asdict(cfg), "n_gpus": 1, "updates": n_updates, "env_steps": steps_done,
+    st = env.stats()
+    return {"config": asdict(cfg), "n_gpus": world, "updates": n_updates, "env_steps": steps_done,
             "seconds": round(dt, 3), "sps": round(steps_done / dt, 1), "episodes_rank0": st["episodes"],
-            "mean_episode_return_rank0": st["total_return"] / max(st["episodes"], 1), "history": history}
+            "mean_episode_return_rank0": st["total_return"] / max(st["episodes"], 1), "history": history,
+            "param_checksum": float(sum(float(p_.detach().double().sum()) for p_ in params))}
 
 
 def main(argv=None) -> int:

@@ -675,3 +675,42 @@ def test_fused_sampler_distribution(torch_cuda, dtype):
     assert torch.allclose(lp, ref_lp, rtol=1e-5, atol=1e-6)
     assert torch.equal(vo, v.float().squeeze(-1))
     assert torch.equal(ro, pr) and torch.equal(do, pd.float())
+
+
+def _ppo_two_rank_worker(rank, world, port, q):
+    import torch.distributed as dist
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world), RANK=str(rank),
+                          LOCAL_RANK="0")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2402_16801_b200.ppo import PPOConfig, train
+        cfg = PPOConfig(tier="classic", n_envs=128, n_steps=16, total_timesteps=128 * 2 * 16 * 4)
+        res = train(cfg, log=lambda s: None)
+        q.put((rank, "ok", res["param_checksum"], res["updates"], res["env_steps"],
+               [r["loss"] for r in res["history"]]))
+        dist.destroy_process_group()
+    except Exception:   # reported to the parent
+        import traceback
+        q.put((rank, traceback.format_exc(), None, None, None, None))
+
+
+def test_graphed_ppo_two_ranks_one_gpu(torch_cuda):
+    """The graphed learner with two ranks (two processes sharing the GPU, gloo
+    all-reduce of the flat gradient): the ranks' shards differ, their
+    averaged updates must leave identical weights on both ranks."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29800 + (os.getpid() % 150)
+    ps = [ctx.Process(target=_ppo_two_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=900) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for rank, msg, *_ in res:
+        assert msg == "ok", f"rank {rank}: {msg}"
+    (_, _, c0, u0, s0, l0), (_, _, c1, u1, s1, l1) = res
+    assert u0 == u1 == 4 and s0 == s1 == 128 * 2 * 16 * 4
+    assert c0 == c1, (c0, c1)
+    assert all(np.isfinite(l0)) and all(np.isfinite(l1))
