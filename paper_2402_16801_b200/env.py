@@ -305,12 +305,19 @@ class BatchEnv:
         t = TIERS[self.tier_name]
         pin = dict(pin_memory=True)
         if obs_mode == "symbolic":
-            self._h_obs = torch.empty((n, t["obs"]), dtype=torch.float32, **pin).numpy()
+            self._obs_alloc = lambda: torch.empty((n, t["obs"]), dtype=torch.float32, **pin).numpy()
         elif obs_mode == "pixels":
-            self._h_obs = torch.empty((n,) + pixel_shape(self.tier_name, self._batch.tile_px),
-                                      dtype=torch.uint8, **pin).numpy()
+            shape = (n,) + pixel_shape(self.tier_name, self._batch.tile_px)
+            self._obs_alloc = lambda: torch.empty(shape, dtype=torch.uint8, **pin).numpy()
         else:
-            self._h_obs = np.zeros((n, 0), np.float32)
+            self._obs_alloc = lambda: np.zeros((n, 0), np.float32)
+        # observations: the reference returns a fresh array per call.  Copying
+        # a 2 GB pinned buffer into a new array per step cost 5x the PCIe
+        # transfer, so the obs land in one of two pinned buffers that is
+        # handed out as is; a buffer is only reused once the caller holds no
+        # reference to it (refcount), else the step falls back to a copy
+        self._h_obs = self._obs_alloc()          # staging buffer of the fallback
+        self._obs_pool = [self._obs_alloc(), self._obs_alloc()] if obs_mode != "none" else []
         self._h_act = torch.empty(n, dtype=torch.int64, **pin).numpy()
         self._h_rew = torch.empty(n, dtype=torch.float32, **pin).numpy()
         self._h_done = torch.empty(n, dtype=torch.bool, **pin).numpy()
@@ -337,11 +344,31 @@ class BatchEnv:
     def _vp(self, a):
         return a.ctypes.data_as(ctypes.c_void_p)
 
+    def _free_obs_buffer(self):
+        """A pool buffer no caller holds (None: all held)."""
+        import sys
+        for k in range(len(self._obs_pool)):
+            if sys.getrefcount(self._obs_pool[k]) <= 2:   # the pool list + getrefcount's argument
+                return k
+        return None
+
+    def _obs_target(self):
+        if self.obs_mode == "none":
+            return None, self._h_obs
+        k = self._free_obs_buffer()
+        return k, (self._obs_pool[k] if k is not None else self._h_obs)
+
+    def _obs_result(self, k, buf):
+        if self.obs_mode == "none":
+            return self._h_obs.copy()
+        return buf if k is not None else buf.copy()
+
     def reset(self) -> np.ndarray:
-        obs_p = self._vp(self._h_obs) if self.obs_mode != "none" else None
+        k, buf = self._obs_target()
+        obs_p = self._vp(buf) if self.obs_mode != "none" else None
         check(lib().gr_reset_host(self._batch.h, obs_p))
         self._ready = True
-        return self._h_obs.copy()
+        return self._obs_result(k, buf)
 
     def step(self, actions):
         if not self._ready:
@@ -357,14 +384,15 @@ class BatchEnv:
                 i = int(np.argmax(bad))
                 raise ValueError(f"invalid action {int(actions[i])} for env {i}")
             np.copyto(self._h_act, actions)
-            obs_p = self._vp(self._h_obs) if self.obs_mode != "none" else None
+            k, buf = self._obs_target()
+            obs_p = self._vp(buf) if self.obs_mode != "none" else None
             check(lib().gr_step_host(self._batch.h, self._vp(self._h_act), obs_p, self._vp(self._h_rew),
                                      self._vp(self._h_done), self._vp(self._h_newly),
                                      self._vp(self._h_time), self._vp(self._h_floor)))
             info = {"time": self._h_time.view(np.uint32).copy(), "floor": self._h_floor.copy(),
                     "newly_unlocked": self._h_newly.copy(),
                     "episodes_completed": self._batch.episodes_completed()}
-            return self._h_obs.copy(), self._h_rew.copy(), self._h_done.copy(), info
+            return self._obs_result(k, buf), self._h_rew.copy(), self._h_done.copy(), info
         finally:
             self._stepping.release()
 

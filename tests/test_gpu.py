@@ -714,3 +714,27 @@ def test_graphed_ppo_two_ranks_one_gpu(torch_cuda):
     assert u0 == u1 == 4 and s0 == s1 == 128 * 2 * 16 * 4
     assert c0 == c1, (c0, c1)
     assert all(np.isfinite(l0)) and all(np.isfinite(l1))
+
+
+def test_batchenv_returned_obs_are_never_overwritten(torch_cuda):
+    """BatchEnv hands out observations without a per-step copy (two pinned
+    buffers, reused only when the caller holds no reference): arrays the
+    caller keeps stay as returned, like the reference's fresh arrays."""
+    from paper_2402_16801_b200 import BatchEnv
+    env = BatchEnv(6, tier="extended", seed=2)
+    kept = [env.reset()]
+    snap = [kept[0].copy()]
+    acts = np.zeros(6, np.int64)
+    for k in range(6):
+        o, *_ = env.step(acts + (k % 5))
+        kept.append(o)
+        snap.append(o.copy())
+    for a, b in zip(kept, snap):
+        assert np.array_equal(a, b)
+    # a loop that drops each observation reuses the two buffers (no copies)
+    ids = set()
+    for k in range(8):
+        o, *_ = env.step(acts)
+        ids.add(o.__array_interface__["data"][0])
+        del o
+    assert len(ids) <= 2
