@@ -86,6 +86,8 @@ struct Ctx {
   uint8_t plal[10];
   uint8_t boss_wave, boss_vuln, boss_timer;
   bool hurt;
+  uint8_t act, pend, lflags;   // k_step's action-sorted phase: action in, pending cooldowns / lane flags out
+  uint8_t pad_[5];
 };
 static_assert(alignof(Ctx) == 4, "Ctx packs at 4-byte alignment");
 static_assert((sizeof(Ctx) / 4) % 2 == 1, "Ctx stride must be an odd number of words (shared-memory banks)");
@@ -1238,6 +1240,9 @@ __device__ __forceinline__ void apply_pending(Ctx& e, uint8_t pend, uint32_t pre
 }
 
 
+#ifndef GR_STEP_SORT
+#define GR_STEP_SORT 1   // game logic on action-sorted envs inside each CTA (needs GR_STEP_SMEM_CTX)
+#endif
 #ifndef GR_STEP_SMEM_CTX
 #define GR_STEP_SMEM_CTX 1   // per-thread working copy in shared memory (0: registers + local memory)
 #endif
@@ -1262,6 +1267,86 @@ __global__ void __launch_bounds__(128, GR_STEP_MINB) k_step(DS S, StepArgs a) {
   Ctx e;
 #endif
   __syncthreads();
+#if GR_STEP_SORT
+  // Phase A (thread t = env t, coalesced): load the state into the working copy.
+  const uint32_t prev_fl = a.prev_flags ? a.prev_flags[0] : 0u;
+  double ep_ret0 = 0.0;
+  int32_t ep_len0 = 0;
+  __shared__ int s_hist[64], s_perm[128];
+  if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
+  int my_act = 63;   // invalid threads sort last
+  if (valid) {
+    e.i = (uint32_t)i;
+    my_act = (int)a.actions[i];
+    ep_ret0 = S.ep_return[i];
+    ep_len0 = S.ep_length[i];
+    e.act = (uint8_t)my_act;
+    e.pend = S.cd_pending[i];
+    load_env<EXT>(e, S);
+    load_lanes<EXT>(e, S, e.pfloor);
+  }
+  __syncthreads();
+  // counting sort of the CTA's envs by action: the game logic below runs
+  // with each warp's lanes on few distinct actions (less branch divergence)
+  const int rank_in = atomicAdd(&s_hist[my_act], 1);
+  __syncthreads();
+  if (threadIdx.x < 32) {   // exclusive scan of the 64 bucket counts
+    const int c0 = s_hist[2 * threadIdx.x], c1 = s_hist[2 * threadIdx.x + 1];
+    int x = c0 + c1;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((int)threadIdx.x >= o) x += y;
+    }
+    const int excl = x - c0 - c1;
+    s_hist[2 * threadIdx.x] = excl;
+    s_hist[2 * threadIdx.x + 1] = excl + c0;
+  }
+  __syncthreads();
+  s_perm[s_hist[my_act] + rank_in] = threadIdx.x;
+  __syncthreads();
+  // Phase B (thread t = the env at sorted position t): the game logic.
+  {
+    const int slot = s_perm[threadIdx.x];
+    const int64_t ii = (int64_t)blockIdx.x * blockDim.x + slot;
+    const bool v2 = ii < a.n && !(a.bad && a.bad[0] >= 0);
+    if (v2) {
+      Ctx& g = reinterpret_cast<Ctx*>(s_ctx_raw)[slot];
+      uint8_t pend = g.pend;
+      apply_pending(g, pend, prev_fl);
+      pend = 0;
+      g.unlock[0] = g.unlock[1] = g.unlock[2] = 0;
+      g.hurt = false;
+      g.health0 = g.health;
+      g.base = mix32(g.key_lo ^ (g.time * 0x9E3779B9u));
+      const int f0 = g.pfloor;
+      player_actions<EXT>(g, S, (int)g.act);
+      if (EXT && g.pfloor != f0) {
+#pragma unroll
+        for (int s_ = 0; s_ < 5; ++s_) {
+          const int cls = s_ < 3 ? 0 : 1, l = s_ < 3 ? s_ : s_ - 3;
+          GR_AT(S, cls == 0 ? GR_F_MEL_CD : GR_F_RAN_CD, uint8_t, f0 * LCAP(cls) + l, ii) = g.lcd[s_];
+        }
+        load_lanes<EXT>(g, S, g.pfloor);
+      }
+      advance_projectiles<EXT>(g);
+      uint8_t lf = 0;
+      lf |= (g.lal[0] | g.lal[1] | g.lal[2]) ? 1u : 0u;
+      lf |= (g.lal[3] | g.lal[4]) ? 2u : 0u;
+      g.lflags = lf;
+      creatures_act<EXT>(g, &pend);
+      survival_tick<EXT>(g);
+      spawn_despawn<EXT>(g, &pend);
+      grow_plants<EXT>(g);
+      g.time += 1;
+      g.pend = pend;
+    }
+  }
+  __syncthreads();
+  // Phase C (thread t = env t again, coalesced): outcome, write-back, outputs.
+  if (valid) {
+    my_flags = e.lflags;
+    const uint8_t pend = e.pend;
+#else
   if (valid) {
     e.i = (uint32_t)i;
     // the per-env words the tail needs are loaded with the state, not after
@@ -1298,6 +1383,7 @@ __global__ void __launch_bounds__(128, GR_STEP_MINB) k_step(DS S, StepArgs a) {
     spawn_despawn<EXT>(e, &pend);
     grow_plants<EXT>(e);
     e.time += 1;
+#endif
     // achievements, reward, done (engine.py:731-745)
     double reward = 0.0;
     uint32_t newly[3];
