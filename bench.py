@@ -377,17 +377,39 @@ def run_e2e(args, gb, env, world, rank, dist, t):
     if dist:
         dist.barrier()
     if world == 1:
-        # one warm-up call allocates the library's host-path scratch
-        h_act.numpy()[:] = acts[0]
-        _lib.check(_lib.lib().gr_step_host(gb.h, P(h_act), obs_p, P(h_rew), P(h_done), P(h_newly),
-                                           P(h_time), P(h_floor)))
-        t0 = time.perf_counter()
-        for k in range(1, args.e2e_steps):
-            h_act.numpy()[:] = acts[k]
+        def host_steps():
+            # one warm-up call allocates the library's host-path scratch
+            h_act.numpy()[:] = acts[0]
             _lib.check(_lib.lib().gr_step_host(gb.h, P(h_act), obs_p, P(h_rew), P(h_done), P(h_newly),
                                                P(h_time), P(h_floor)))
-        dt = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            for k in range(1, args.e2e_steps):
+                h_act.numpy()[:] = acts[k]
+                _lib.check(_lib.lib().gr_step_host(gb.h, P(h_act), obs_p, P(h_rew), P(h_done), P(h_newly),
+                                                   P(h_time), P(h_floor)))
+            return time.perf_counter() - t0
+
+        dt = host_steps()
         steps = args.e2e_steps - 1
+        if args.obs == "symbolic" and n * h_obs.shape[1] < 2 ** 32:
+            # the same calls into an attached buffer (BatchEnv(obs_transfer="delta")):
+            # only the obs words that changed since the buffer's last step cross PCIe
+            dense = {"value": round(n * steps / dt, 1), "unit": UNIT, "h2d_bytes_per_step": n * 8,
+                     "d2h_bytes_per_step": int(d2h), "steps": steps, "path": "gr_step_host, dense obs copy"}
+            _lib.check(_lib.lib().gr_host_obs_attach(gb.h, obs_p))
+            dt = host_steps()
+            prev = h_obs.numpy().view(np.uint32).copy()
+            h_act.numpy()[:] = acts[0]
+            _lib.check(_lib.lib().gr_step_host(gb.h, P(h_act), obs_p, P(h_rew), P(h_done), P(h_newly),
+                                               P(h_time), P(h_floor)))
+            changed = int(np.count_nonzero(h_obs.numpy().view(np.uint32) != prev))   # one step's list length
+            _lib.check(_lib.lib().gr_host_obs_detach(gb.h, obs_p))
+            d2h_delta = 2 * 8 + changed * 8 + n * (4 + 1 + gb.n_achievements + 4 + 1)
+            return {"value": round(n * steps / dt, 1), "unit": UNIT, "h2d_bytes_per_step": n * 8,
+                    "d2h_bytes_per_step": int(d2h_delta), "steps": steps,
+                    "path": "gr_step_host into a gr_host_obs_attach'ed pinned buffer (BatchEnv obs_transfer='delta'): "
+                            "(index, value) of the obs words changed since the buffer's last step, host scatter",
+                    "dense": dense}
     else:
         d_act = torch.empty(n, dtype=torch.int64, device=gb.device)
         t0 = time.perf_counter()

@@ -155,6 +155,20 @@ int gr_step_host(gr_env *env, const int64_t *actions_host, void *obs_host, float
                  uint8_t *floor_host);
 int gr_reset_host(gr_env *env, void *obs_host);
 
+/* Delta observation transfer (symbolic observations only).  Attaching a host
+ * buffer of n_envs x obs_width float32 hands its contents to the handle: it
+ * is zero-filled now, the handle keeps a device copy of it, and every later
+ * gr_step_host / gr_reset_host into it moves only the words that changed
+ * since the observation last written into that buffer ((word index, value
+ * bits), 8 B each; ~1.3 % of the words two steps apart) and rewrites only
+ * those on the host, instead of copying 4 B x n x width.  The buffer then
+ * equals a dense copy bit for bit, as long as the caller never writes into
+ * it.  Needs n x width < 2^32.  The transfer behind BatchEnv.step's obs
+ * (bindings/src/gridrogue_gym/__init__.py:63-84), BatchEnv(obs_transfer=
+ * "delta") in the Python mirror. */
+int gr_host_obs_attach(gr_env *env, void *obs_host);
+int gr_host_obs_detach(gr_env *env, void *obs_host);
+
 /* ---- state channel (parity / checkpoint) -------------------------------- *
  * Copy one SimState field to / from host memory in the reference layout
  * (env-major, state._SHAPES).  Synchronous.  Importing clears any deferred

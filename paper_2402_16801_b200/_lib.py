@@ -97,6 +97,8 @@ def lib() -> ctypes.CDLL:
         "gr_step_finish": (I32, [P, P, I32, I32, P, P]),
         "gr_step_host": (I32, [P, P, P, P, P, P, P, P]),
         "gr_reset_host": (I32, [P, P]),
+        "gr_host_obs_attach": (I32, [P, P]),
+        "gr_host_obs_detach": (I32, [P, P]),
         "gr_export_field": (I32, [P, I32, P]),
         "gr_import_field": (I32, [P, I32, P]),
         "gr_observe": (I32, [P, P, P]),

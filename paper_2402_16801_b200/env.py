@@ -289,9 +289,14 @@ class BatchEnv:
 
     def __init__(self, n_envs: int, tier: str = "extended", seed: int = 0,
                  obs_mode: str = "symbolic", max_episode_length: int | None = None,
-                 tile_px: int | None = None, device: int = 0):
+                 tile_px: int | None = None, device: int = 0, obs_transfer: str = "dense"):
         if obs_mode not in self.metadata["obs_modes"]:
             raise ValueError(f"unknown obs_mode {obs_mode!r}")
+        if obs_transfer not in ("dense", "delta"):
+            raise ValueError(f"unknown obs_transfer {obs_transfer!r}")
+        if obs_transfer == "delta" and obs_mode != "symbolic":
+            raise ValueError("obs_transfer='delta' needs obs_mode='symbolic'")
+        self.obs_transfer = obs_transfer
         self.tier_name = _tier_name(tier)
         self.n_envs = int(n_envs)
         self.obs_mode = obs_mode
@@ -318,6 +323,14 @@ class BatchEnv:
         # reference to it (refcount), else the step falls back to a copy
         self._h_obs = self._obs_alloc()          # staging buffer of the fallback
         self._obs_pool = [self._obs_alloc(), self._obs_alloc()] if obs_mode != "none" else []
+        # obs_transfer "delta": the handle owns the buffers' contents
+        # (gr_host_obs_attach) and moves only the words that changed since the
+        # buffer's last observation; arrays are handed out read-only so a
+        # caller cannot make the buffer and the handle's copy of it disagree
+        if obs_transfer == "delta":
+            for b in [self._h_obs, *self._obs_pool]:
+                check(lib().gr_host_obs_attach(self._batch.h, b.ctypes.data_as(ctypes.c_void_p)))
+                b.flags.writeable = False   # views handed out cannot be made writable again
         self._h_act = torch.empty(n, dtype=torch.int64, **pin).numpy()
         self._h_rew = torch.empty(n, dtype=torch.float32, **pin).numpy()
         self._h_done = torch.empty(n, dtype=torch.bool, **pin).numpy()
@@ -361,7 +374,9 @@ class BatchEnv:
     def _obs_result(self, k, buf):
         if self.obs_mode == "none":
             return self._h_obs.copy()
-        return buf if k is not None else buf.copy()
+        if k is None:
+            return buf.copy()
+        return buf.view() if self.obs_transfer == "delta" else buf
 
     def reset(self) -> np.ndarray:
         k, buf = self._obs_target()

@@ -738,3 +738,63 @@ def test_batchenv_returned_obs_are_never_overwritten(torch_cuda):
         ids.add(o.__array_interface__["data"][0])
         del o
     assert len(ids) <= 2
+
+
+@pytest.mark.parametrize("tier,n_act", [("extended", 43), ("classic", 17)])
+def test_batchenv_delta_obs_transfer_matches_oracle(torch_cuda, tier, n_act):
+    """BatchEnv(obs_transfer="delta") -- gr_host_obs_attach'ed pinned buffers
+    that receive only the words changed since their last observation --
+    returns the same arrays as the oracle (bindings/src/gridrogue_gym/
+    __init__.py:63-95) under reset stress, while the caller holds some
+    returned arrays (buffer rotation and the copy fallback) and drops others
+    (buffer reuse)."""
+    import oracle as O
+    from paper_2402_16801_b200 import BatchEnv
+    n, seed, max_len = 48, 11, 12
+    env = BatchEnv(n, tier=tier, seed=seed, max_episode_length=max_len, obs_transfer="delta")
+    ob = O.OracleBatch(tier, n, seed, max_episode_length=max_len)
+    obs = env.reset()
+    assert not obs.flags.writeable
+    with pytest.raises(ValueError):
+        obs.flags.writeable = True
+    assert np.array_equal(obs, ob.state.encode_symbolic())
+    held = []
+    rng = np.random.default_rng(4)
+    for k in range(60):
+        a = rng.integers(0, n_act, size=n)
+        obs, rew, done, _ = env.step(a)
+        r2, d2, _, _ = ob.step(a)
+        want = ob.state.encode_symbolic()
+        assert np.array_equal(obs.view(np.uint32), want.view(np.uint32)), f"obs differs at step {k}"
+        assert np.array_equal(rew, r2.astype(np.float32)) and np.array_equal(done, d2)
+        if k % 7 == 3:
+            held.append((obs, want))     # keep this buffer out of the rotation for a while
+        if k % 7 == 6:
+            held.clear()
+    for o, w in held:                     # held arrays were never overwritten
+        assert np.array_equal(o, w)
+    obs = env.reset()                     # a reset through an attached buffer
+    ob = O.OracleBatch(tier, n, seed, max_episode_length=max_len)
+    assert np.array_equal(obs, ob.state.encode_symbolic())
+    with pytest.raises(ValueError):
+        BatchEnv(2, tier=tier, obs_mode="pixels", obs_transfer="delta")
+
+
+def test_host_obs_delta_list_growth(torch_cuda):
+    """The changed-word list outgrows its first capacity (every word of a
+    fresh reset differs from a zeroed buffer when the capacity is tiny
+    relative to the row): several passes, same result as a dense copy."""
+    import ctypes
+    from paper_2402_16801_b200 import _lib, GridrogueBatch
+    import oracle as O
+    n = 64
+    gb = GridrogueBatch(n, "extended", 2, "symbolic", device=0)
+    h = torch_cuda.zeros((n, 8268), dtype=torch_cuda.float32, pin_memory=True)
+    p = ctypes.c_void_p(h.data_ptr())
+    _lib.check(_lib.lib().gr_host_obs_attach(gb.h, p))
+    _lib.check(_lib.lib().gr_reset_host(gb.h, p))
+    ob = O.OracleBatch("extended", n, 2)
+    assert np.array_equal(h.numpy(), ob.state.encode_symbolic())
+    with pytest.raises(ValueError, match="not attached"):
+        _lib.check(_lib.lib().gr_host_obs_detach(gb.h, ctypes.c_void_p(12345)))
+    _lib.check(_lib.lib().gr_host_obs_detach(gb.h, p))
