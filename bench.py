@@ -19,7 +19,9 @@ with a CUDA event pair around every launch (kernel-by-kernel, no graph;
 `roofline.profiled_ms_per_step`);
 `e2e` is the same metric through the host-buffer C-ABI call (gr_step_host):
 H2D of the step's actions and D2H of obs/reward/done/info inside the timed
-region.  State (~2.8 GB) and the per-step obs (2.17 GB) exceed the 126 MB L2,
+region.  Symbolic obs go into a gr_host_obs_attach'ed pinned buffer (the
+delta transfer: only the words changed since the buffer's last step cross
+PCIe and are rewritten on the host); `e2e.dense` is the plain 2.17 GB copy.  State (~2.8 GB) and the per-step obs (2.17 GB) exceed the 126 MB L2,
 so no explicit flush is needed between steps.
 
 --impl reference times the reference algorithm on the host CPU cores (the
