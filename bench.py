@@ -205,7 +205,7 @@ def main():
     ap.add_argument("--tile-px", type=int, default=None, help="pixels: tile size (default 7 classic, 10 extended)")
     ap.add_argument("--max-episode-length", type=int, default=None,
                     help="BatchConfig.max_episode_length (reset stress: 16 or 32, SURVEY.md 8(d) config 4)")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
