@@ -1,0 +1,149 @@
+"""Mint the north-star parity goldens from the unmodified numpy reference.
+
+    python tests/golden/make_long_golden.py [long|north_star|all]
+
+Run HERE (where /root/reference exists); the GPU box has no reference, so
+the fixtures are committed and both the C oracle (tests/test_oracle_golden.py)
+and the CUDA product (tests/test_gpu.py) are checked against them directly.
+
+* ``long_<tier>_<obs>.npz`` -- BASELINE.json north star: "bit-exact ... parity
+  with the CPU reference on 10^4-step random rollouts for all four variants".
+  The configs of ``tests/test_gpu.py::test_long_rollout_parity_10k``:
+  seed 31, ``max_episode_length`` 700, n = 32 (symbolic) / 16 classic pixels /
+  12 extended pixels, BatchEnv semantics (``batch_step`` then the post-reset
+  observation, ``bindings/src/gridrogue_gym/__init__.py:63-84``), actions from
+  ``RandomPolicy(seed, n_actions)`` (``policies.py:22-37``).  Per step: blake2b
+  digests of reward (the BatchEnv float32 cast, ``__init__.py:80``), done and
+  the observation (``encode_symbolic_batch``, ``obs.py:343``, or the stacked
+  per-env ``render_tiles`` frames, ``tiles.py:85``).  Every 2,500 steps: the
+  full SimState digest (every field of ``state.FIELD_NAMES``, maps included)
+  plus the f64 episode accumulators (``batch.py:200-201``), which pin the f64
+  reward sums.
+* ``north_star_ext_n65536.npz`` -- the bench workload (Craftax-Symbolic,
+  65,536 envs, seed 0): the reset state and observation, then 12 steps with
+  reward / done / newly / info / observation / full-state digests per step
+  and per-field digests at the end (maps included).
+
+Digests: tests/_digest.py (blake2b-64 over dtype name + bytes).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+from tests._digest import digest, state_digest  # noqa: E402
+
+LONG = {   # name: (tier, obs, n)
+    "classic_symbolic": ("classic", "symbolic", 32),
+    "extended_symbolic": ("extended", "symbolic", 32),
+    "classic_pixels": ("classic", "pixels", 16),
+    "extended_pixels": ("extended", "pixels", 12),
+}
+LONG_STEPS, LONG_SEED, LONG_MAXLEN, LONG_EVERY = 10_000, 31, 700, 2500
+
+
+def _ref():
+    sys.path.insert(0, REF)
+    import gridrogue
+    return gridrogue
+
+
+def long_rollout(name):
+    _ref()
+    from gridrogue import CLASSIC, EXTENDED
+    from gridrogue.batch import BatchConfig, batch_reset, batch_step
+    from gridrogue.obs import encode_symbolic_batch
+    from gridrogue.policies import RandomPolicy
+    from gridrogue.state import FIELD_NAMES, GameState
+    from gridrogue.tiles import render_tiles
+
+    tier, obs_mode, n = LONG[name]
+    t = {"classic": CLASSIC, "extended": EXTENDED}[tier]
+    px = 7 if tier == "classic" else 10
+    bs = batch_reset(BatchConfig(n_envs=n, tier=t, max_episode_length=LONG_MAXLEN), LONG_SEED)
+    pol = RandomPolicy(LONG_SEED, t.n_actions)
+
+    def observe():
+        if obs_mode == "symbolic":
+            return encode_symbolic_batch(bs.sim)
+        return np.stack([render_tiles(GameState(bs.sim.view(slice(i, i + 1))), px) for i in range(n)])
+
+    def full_state():
+        return state_digest({f: getattr(bs.sim, f) for f in FIELD_NAMES}, FIELD_NAMES)
+
+    reset = np.array([full_state(), digest(observe())], np.uint64)
+    rew, done, obs, ckpt = [], [], [], []
+    t0 = time.time()
+    for k in range(LONG_STEPS):
+        bs, out = batch_step(bs, pol.actions(bs.sim))
+        rew.append(digest(out.reward.astype(np.float32)))
+        done.append(digest(out.done))
+        obs.append(digest(observe()))
+        if (k + 1) % LONG_EVERY == 0:
+            ckpt.append([full_state(), digest(bs.ep_return, bs.ep_length)])
+            print(f"  {name}: step {k + 1} ({time.time() - t0:.0f} s)", flush=True)
+    st = bs.stats
+    np.savez_compressed(
+        os.path.join(OUT, f"long_{name}.npz"), tier=tier, obs_mode=obs_mode, n=n, steps=LONG_STEPS,
+        seed=LONG_SEED, max_len=LONG_MAXLEN, every=LONG_EVERY, tile_px=px, reset=reset,
+        reward=np.array(rew, np.uint64), done=np.array(done, np.uint64), obs=np.array(obs, np.uint64),
+        ckpt=np.array(ckpt, np.uint64),
+        final_fields=np.array([digest(getattr(bs.sim, f)) for f in FIELD_NAMES], np.uint64),
+        episodes=np.int64(st.episodes), total_steps=np.int64(st.total_steps),
+        ach_episodes=np.asarray(st.ach_episodes, np.int64), level_seeds=bs.level_seeds())
+
+
+NS_N, NS_SEED, NS_STEPS = 65536, 0, 12
+
+
+def north_star():
+    _ref()
+    from gridrogue import EXTENDED
+    from gridrogue.batch import BatchConfig, batch_reset, batch_step
+    from gridrogue.obs import encode_symbolic_batch
+    from gridrogue.policies import RandomPolicy
+    from gridrogue.state import FIELD_NAMES
+
+    t0 = time.time()
+    bs = batch_reset(BatchConfig(n_envs=NS_N, tier=EXTENDED), NS_SEED)
+    print(f"  north_star: reset {time.time() - t0:.0f} s", flush=True)
+    pol = RandomPolicy(NS_SEED, EXTENDED.n_actions)
+
+    def full_state():
+        return state_digest({f: getattr(bs.sim, f) for f in FIELD_NAMES}, FIELD_NAMES)
+
+    reset = np.array([full_state(), digest(encode_symbolic_batch(bs.sim))], np.uint64)
+    rec = {k: [] for k in ("reward", "done", "newly", "info", "obs", "state")}
+    for k in range(NS_STEPS):
+        bs, out = batch_step(bs, pol.actions(bs.sim))
+        rec["reward"].append(digest(out.reward.astype(np.float32)))
+        rec["done"].append(digest(out.done))
+        rec["newly"].append(digest(out.newly))
+        rec["info"].append(digest(out.info["time"], out.info["floor"]))
+        rec["obs"].append(digest(encode_symbolic_batch(bs.sim)))
+        rec["state"].append(full_state())
+        print(f"  north_star: step {k + 1} ({time.time() - t0:.0f} s, {int(out.done.sum())} done)", flush=True)
+    st = bs.stats
+    np.savez_compressed(
+        os.path.join(OUT, f"north_star_ext_n{NS_N}.npz"), tier="extended", n=NS_N, steps=NS_STEPS,
+        seed=NS_SEED, reset=reset, **{k: np.array(v, np.uint64) for k, v in rec.items()},
+        final_fields=np.array([digest(getattr(bs.sim, f)) for f in FIELD_NAMES], np.uint64),
+        episode_acc=np.uint64(digest(bs.ep_return, bs.ep_length)),
+        episodes=np.int64(st.episodes), level_seeds_digest=np.uint64(digest(bs.level_seeds())))
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("long", "all"):
+        for nm in (sys.argv[2:] or LONG):
+            long_rollout(nm)
+    if what in ("north_star", "all"):
+        north_star()
+    print("written to", OUT)

@@ -125,22 +125,37 @@ def test_scrambled_state_parity(torch_cuda, oracle_lib, tier):
         _cmp_state(O, gb, ob.state, tier, n)
 
 
-def test_full_size_north_star_parity(torch_cuda, oracle_lib):
-    """65,536 extended envs (the bench workload): rewards, dones, obs digests
-    and non-map state against the oracle for 12 steps."""
+def test_full_size_north_star_parity(torch_cuda):
+    """The bench workload (65,536 extended envs, seed 0) against digests minted
+    from the unmodified numpy reference (tests/golden/make_long_golden.py):
+    the reset state (maps included) and observation, then 12 steps of reward /
+    done / newly / info / observation / full state, the final per-field digests,
+    the f64 episode accumulators and the level seeds."""
     from paper_2402_16801_b200 import GridrogueBatch
-    from tests._digest import digest
-    O = oracle_lib
+    from paper_2402_16801_b200.layout import field_shapes, FIELD_NAMES
+    from tests._digest import digest, state_digest
     torch = torch_cuda
-    n, seed = 65536, 0
+    g = np.load(os.path.join(GOLD, "north_star_ext_n65536.npz"))
+    n, seed, steps = int(g["n"]), int(g["seed"]), int(g["steps"])
+    shapes = field_shapes("extended", n)
     gb = GridrogueBatch(n, "extended", seed, "symbolic")
-    gb.reset()
-    ob = O.OracleBatch("extended", n, seed, threads=os.cpu_count() or 8)
-    for k in range(12):
-        a = O.random_actions(seed, k, n, 43)
-        obs = _step_both(torch, gb, ob, a)
-        assert digest(obs.cpu().numpy()) == digest(ob.state.encode_symbolic()), f"obs step {k}"
-    _cmp_state(O, gb, ob.state, "extended", n, skip=("blocks", "items"))
+    obs = gb.reset()
+    assert state_digest(gb.export_state(shapes), FIELD_NAMES) == int(g["reset"][0]), "reset state"
+    assert digest(obs.cpu().numpy()) == int(g["reset"][1]), "reset obs"
+    for k in range(steps):
+        obs, rew, done, newly, tm, fl = gb.step(gb.random_actions(seed, k))
+        assert digest(rew.cpu().numpy()) == int(g["reward"][k]), f"reward step {k}"
+        assert digest(done.cpu().numpy().astype(bool)) == int(g["done"][k]), f"done step {k}"
+        assert digest(newly.cpu().numpy().astype(bool)) == int(g["newly"][k]), f"newly step {k}"
+        assert digest(tm.cpu().numpy().view(np.uint32), fl.cpu().numpy()) == int(g["info"][k]), f"info step {k}"
+        assert digest(obs.cpu().numpy()) == int(g["obs"][k]), f"obs step {k}"
+        assert state_digest(gb.export_state(shapes), FIELD_NAMES) == int(g["state"][k]), f"state step {k}"
+    ex = gb.export_state(shapes)
+    bad = [f for f, dg in zip(FIELD_NAMES, g["final_fields"]) if digest(ex[f]) != int(dg)]
+    assert not bad, f"fields differ from the reference: {bad}"
+    assert digest(*gb.episode_progress()) == int(g["episode_acc"])
+    assert digest(gb.level_seeds()) == int(g["level_seeds_digest"])
+    assert gb.stats()["episodes"] == int(g["episodes"])
 
 
 def test_batchenv_contract(torch_cuda, oracle_lib):
@@ -477,35 +492,49 @@ def test_sharded_batch_two_ranks_one_gpu(torch_cuda):
         assert msg == "ok", f"rank {rank}: {msg}"
 
 
-@pytest.mark.parametrize("tier,obs_mode,n", [("classic", "symbolic", 32), ("extended", "symbolic", 32),
-                                             ("classic", "pixels", 16), ("extended", "pixels", 12)])
-def test_long_rollout_parity_10k(torch_cuda, oracle_lib, tier, obs_mode, n):
-    """10^4-step rollouts, every step's reward / done / observation
-    equal to the oracle's, the full SimState every 2,500 steps (episodes capped at
-    700 steps, so every env lives through many resets)."""
+LONG = sorted(f[len("long_"):-4] for f in os.listdir(GOLD) if f.startswith("long_"))
+
+
+@pytest.mark.parametrize("name", LONG)
+def test_long_rollout_parity_10k(torch_cuda, name):
+    """BASELINE.json north star, pinned to the reference itself: 10^4-step random
+    rollouts of all four variants (Classic/Full x Symbolic/Pixels) against digests
+    minted from the unmodified numpy reference (tests/golden/make_long_golden.py):
+    every step's reward / done / observation, the full SimState (maps included)
+    and the f64 episode accumulators every 2,500 steps, final fields and
+    EpisodeStats.  Episodes are capped at 700 steps, so every env lives through
+    many auto-resets."""
     from paper_2402_16801_b200 import GridrogueBatch
-    O = oracle_lib
+    from paper_2402_16801_b200.layout import field_shapes, FIELD_NAMES
+    from tests._digest import digest, state_digest
     torch = torch_cuda
-    steps, seed, max_len = 10_000, 31, 700
-    gb = GridrogueBatch(n, tier, seed, obs_mode, max_len, newly=False, info=False)
-    gb.reset()
+    g = np.load(os.path.join(GOLD, f"long_{name}.npz"))
+    tier, obs_mode, n = str(g["tier"]), str(g["obs_mode"]), int(g["n"])
+    steps, seed, ml, every, px = (int(g[k]) for k in ("steps", "seed", "max_len", "every", "tile_px"))
+    shapes = field_shapes(tier, n)
+    gb = GridrogueBatch(n, tier, seed, obs_mode, ml, tile_px=px, newly=False, info=False)
+    obs = gb.reset()
+    assert state_digest(gb.export_state(shapes), FIELD_NAMES) == int(g["reset"][0]), "reset state"
+    assert digest(obs.cpu().numpy()) == int(g["reset"][1]), "reset obs"
     gb.set_validate(False)
-    ob = O.OracleBatch(tier, n, seed, max_episode_length=max_len, threads=8)
-    na = O.TIERS[tier]["NA"]
-    px = gb.tile_px
+    c = 0
     for k in range(steps):
-        a = O.random_actions(seed, k, n, na)
-        obs, rew, done, *_ = gb.step(torch.from_numpy(a).cuda())
-        r2, d2, _, _ = ob.step(a)
-        ref_obs = ob.state.encode_symbolic() if obs_mode == "symbolic" else ob.state.render_pixels(px)
-        assert torch.equal(rew.cpu(), torch.from_numpy(r2.astype(np.float32))), f"reward step {k}"
-        assert np.array_equal(done.cpu().numpy().astype(bool), d2), f"done step {k}"
-        assert torch.equal(obs, torch.from_numpy(ref_obs).cuda()), f"obs step {k}"
-        if (k + 1) % 2500 == 0:
-            _cmp_state(O, gb, ob.state, tier, n)
-    s1, s2 = gb.stats(), ob.stats()
-    assert s1["episodes"] == s2["episodes"] >= n * (steps // max_len)
-    assert np.array_equal(s1["ach_episodes"], s2["ach_episodes"])
+        obs, rew, done, *_ = gb.step(gb.random_actions(seed, k))
+        assert digest(rew.cpu().numpy()) == int(g["reward"][k]), f"reward step {k}"
+        assert digest(done.cpu().numpy().astype(bool)) == int(g["done"][k]), f"done step {k}"
+        assert digest(obs.cpu().numpy()) == int(g["obs"][k]), f"obs step {k}"
+        if (k + 1) % every == 0:
+            assert state_digest(gb.export_state(shapes), FIELD_NAMES) == int(g["ckpt"][c][0]), f"state step {k}"
+            assert digest(*gb.episode_progress()) == int(g["ckpt"][c][1]), f"episode acc step {k}"
+            c += 1
+    ex = gb.export_state(shapes)
+    bad = [f for f, dg in zip(FIELD_NAMES, g["final_fields"]) if digest(ex[f]) != int(dg)]
+    assert not bad, f"fields differ from the reference: {bad}"
+    s = gb.stats()
+    assert s["episodes"] == int(g["episodes"]) >= n * (steps // ml)
+    assert s["total_steps"] == int(g["total_steps"])
+    assert np.array_equal(s["ach_episodes"], g["ach_episodes"])
+    assert np.array_equal(gb.level_seeds(), g["level_seeds"])
 
 
 def test_batchenv_determinism_and_no_allocation_growth(torch_cuda):

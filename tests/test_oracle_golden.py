@@ -150,3 +150,68 @@ def test_recorded_session_replay(oracle_lib):
         assert bool(d[0]) == e["done"]
         assert state_digest(st.export_fields(), O.FIELD_NAMES) == e["state"]
     assert used == set(range(43))
+
+
+LONG = sorted(f[len("long_"):-4] for f in os.listdir(GOLD) if f.startswith("long_"))
+
+
+@pytest.mark.parametrize("name", LONG)
+def test_long_rollout_matches_reference(oracle_lib, name):
+    """BASELINE.json north star: 10^4-step random rollouts of all four variants
+    (tests/golden/make_long_golden.py, minted from the unmodified reference):
+    every step's reward / done / observation, the full SimState + f64 episode
+    accumulators every 2,500 steps, the final fields and EpisodeStats."""
+    O = oracle_lib
+    g = np.load(os.path.join(GOLD, f"long_{name}.npz"))
+    tier, obs_mode, n = str(g["tier"]), str(g["obs_mode"]), int(g["n"])
+    steps, seed, ml, every, px = (int(g[k]) for k in ("steps", "seed", "max_len", "every", "tile_px"))
+    b = O.OracleBatch(tier, n, seed, max_episode_length=ml)
+    st = b.state
+
+    def observe():
+        return st.encode_symbolic() if obs_mode == "symbolic" else st.render_pixels(px)
+
+    assert state_digest(st.export_fields(), O.FIELD_NAMES) == int(g["reset"][0])
+    assert digest(observe()) == int(g["reset"][1])
+    na = O.TIERS[tier]["NA"]
+    c = 0
+    for k in range(steps):
+        r, d, _, _ = b.step(O.random_actions(seed, k, n, na))
+        assert digest(r.astype(np.float32)) == int(g["reward"][k]), f"reward step {k}"
+        assert digest(d) == int(g["done"][k]), f"done step {k}"
+        assert digest(observe()) == int(g["obs"][k]), f"obs step {k}"
+        if (k + 1) % every == 0:
+            assert state_digest(st.export_fields(), O.FIELD_NAMES) == int(g["ckpt"][c][0]), f"state step {k}"
+            assert digest(*b.episode_progress()) == int(g["ckpt"][c][1]), f"episode acc step {k}"
+            c += 1
+    ex = st.export_fields()
+    for f, dg in zip(O.FIELD_NAMES, g["final_fields"]):
+        assert digest(ex[f]) == int(dg), f
+    s = b.stats()
+    assert s["episodes"] == int(g["episodes"]) and s["total_steps"] == int(g["total_steps"])
+    assert np.array_equal(s["ach_episodes"], g["ach_episodes"])
+    assert np.array_equal(ex["params_seed"], g["level_seeds"])
+
+
+@pytest.mark.skipif(not os.environ.get("GR_SLOW"), reason="65,536-env oracle run: set GR_SLOW=1 (~2 min, 8 cores)")
+def test_north_star_size_matches_reference(oracle_lib):
+    """The bench workload (65,536 extended envs) on the oracle against the
+    reference's digests -- the same fixture tests/test_gpu.py checks the CUDA
+    path against."""
+    O = oracle_lib
+    g = np.load(os.path.join(GOLD, "north_star_ext_n65536.npz"))
+    n, seed, steps = int(g["n"]), int(g["seed"]), int(g["steps"])
+    b = O.OracleBatch("extended", n, seed, threads=os.cpu_count() or 8)
+    st = b.state
+    assert state_digest(st.export_fields(), O.FIELD_NAMES) == int(g["reset"][0])
+    assert digest(st.encode_symbolic()) == int(g["reset"][1])
+    for k in range(steps):
+        r, d, nw, info = b.step(O.random_actions(seed, k, n, 43))
+        assert digest(r.astype(np.float32)) == int(g["reward"][k]), f"reward step {k}"
+        assert digest(d) == int(g["done"][k]), f"done step {k}"
+        assert digest(nw) == int(g["newly"][k]), f"newly step {k}"
+        assert digest(info["time"], info["floor"]) == int(g["info"][k]), f"info step {k}"
+        assert digest(st.encode_symbolic()) == int(g["obs"][k]), f"obs step {k}"
+        assert state_digest(st.export_fields(), O.FIELD_NAMES) == int(g["state"][k]), f"state step {k}"
+    assert digest(*b.episode_progress()) == int(g["episode_acc"])
+    assert digest(st.export_fields()["params_seed"]) == int(g["level_seeds_digest"])
