@@ -168,6 +168,13 @@ int gr_reset_host(gr_env *env, void *obs_host);
  * "delta") in the Python mirror. */
 int gr_host_obs_attach(gr_env *env, void *obs_host);
 int gr_host_obs_detach(gr_env *env, void *obs_host);
+/* Host-measured phases of gr_step_host / gr_reset_host since the last read
+ * (then reset), milliseconds summed over calls: [0] enqueue (H2D of actions,
+ * step launch, delta kernels), [1] waiting on the device (step + change
+ * detection; with a dense copy, included in [3]), [2] host scatter of the
+ * changed words, [3] final synchronisation (small outputs, dense obs copy);
+ * calls / words: host-path calls and changed words delivered. */
+int gr_host_phase_times(gr_env *env, double out[4], int64_t *calls, int64_t *words);
 
 /* ---- state channel (parity / checkpoint) -------------------------------- *
  * Copy one SimState field to / from host memory in the reference layout
@@ -231,8 +238,23 @@ int64_t gr_kernel_launches(const gr_env *env);
 int gr_set_profiling(gr_env *env, int32_t on);
 int gr_kernel_times(gr_env *env, double *ms, int64_t *counts, int32_t n_classes);
 /* worldgen diagnostics: [worlds generated, floors retried, template floors,
- * potion argsort ties, numerically fragile cave floors] */
+ * potion draws with ties (reproduced in numpy's order), 0 (reserved)] */
 int gr_worldgen_counters(gr_env *env, int64_t out[5]);
+/* worldgen.MAX_GEN_RETRIES (worldgen.py:36, default 16) for every later
+ * world this handle generates (pool, reset, level buffers); 0 sends every
+ * floor to the _template_floor fallback (worldgen.py:549-595) -- the hook the
+ * parity tests use to reach that branch */
+int gr_set_worldgen_attempts(gr_env *env, int32_t max_attempts);
+
+/* ---- numerics self-test -------------------------------------------------- *
+ * The exact device routines the kernels use where the reference's results
+ * depend on its host libraries, exposed so tests can compare them with
+ * numpy directly over large input sets (device pointers, async on stream):
+ * float64 sin / cos of float32 angles as glibc computes them (the cave noise,
+ * perlin.py:71-72 + worldgen.py:424), and np.argsort of six float32 keys in
+ * numpy's AVX-512 tie order (the potion permutation, worldgen.py:647-649). */
+int gr_selftest_sincos64(const float *x_dev, double *sin_dev, double *cos_dev, int64_t n, void *stream);
+int gr_selftest_argsort6(const float *keys_dev, uint8_t *idx_dev, int64_t n, void *stream);
 
 #ifdef __cplusplus
 }

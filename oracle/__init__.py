@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import shutil
 import subprocess
 
 import numpy as np
@@ -93,8 +94,11 @@ def pixel_shape(tier: str, px: int) -> tuple:
 
 def build(force: bool = False) -> str:
     """Compile the oracle library (gcc, plain C, -ffp-contract=off)."""
-    if force or not os.path.exists(_LIB_PATH):
-        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    if shutil.which("make") is None:
+        if not os.path.exists(_LIB_PATH):
+            raise RuntimeError("make not found and the oracle library is not built")
+        return _LIB_PATH
+    subprocess.run(["make", "-s", "-C", _HERE] + (["-B"] if force else []), check=True)   # incremental
     return _LIB_PATH
 
 
@@ -119,6 +123,8 @@ def lib():
         L.go_np_sinf.argtypes = [c.c_float]
         L.go_np_cosf.restype = c.c_float
         L.go_np_cosf.argtypes = [c.c_float]
+        L.go_np_argsort6.argtypes = [P, P]
+        L.go_set_max_gen_retries.argtypes = [c.c_int]
         L.go_generate_world.argtypes = [c.c_uint64, c.c_int, P]
         L.go_state_new.restype = P
         L.go_state_new.argtypes = [c.c_int, c.c_int64, c.c_int64]

@@ -127,13 +127,13 @@ int64_t go_state_step(go_state_t *s, const int64_t *actions, double *reward, uin
 void go_state_encode(const go_state_t *s, float *out) {
   int L = s->classic ? 1345 : 8268;
   int dark = gs_any_dark(s);
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if (s->n >= 512)
   for (int64_t i = 0; i < s->n; ++i) gs_encode_symbolic(s, i, dark, out + (size_t)i * L);
 }
 
 void go_state_pixels(const go_state_t *s, int px, uint8_t *out) {
   size_t fr = (size_t)(s->VR + 2) * px * (s->VC + (s->classic ? 0 : 2)) * px * 3;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if (s->n >= 128)
   for (int64_t i = 0; i < s->n; ++i) gs_render_pixels(s, i, px, out + i * fr);
 }
 
@@ -304,7 +304,7 @@ int go_state_any_dark(const go_state_t *s) { return gs_any_dark(s); }
 
 void go_state_encode_flag(const go_state_t *s, int dark, float *out) {
   int L = s->classic ? 1345 : 8268;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if (s->n >= 512)
   for (int64_t i = 0; i < s->n; ++i) gs_encode_symbolic(s, i, dark, out + (size_t)i * L);
 }
 

@@ -107,6 +107,25 @@ static float np_sincosf(float x, int is_cos) {
 float go_np_sinf(float x) { return np_sincosf(x, 0); }
 float go_np_cosf(float x) { return np_sincosf(x, 1); }
 
+/* np.argsort of 6 float32 (worldgen.py:647-649) as numpy >= 2 runs it on
+   AVX-512 hosts: x86-simd-sort's key/index bitonic network over one 8-lane
+   register (lanes 6-7 = +inf, inert), compare-exchange on a strict '>' with
+   each lane keeping its index on ties -- 15 comparators on the live lanes.
+   Not stable; pinned against np.argsort on all 6^6 value patterns. */
+void go_np_argsort6(const float *v, uint8_t *idx) {
+  static const int P[15][2] = {{0, 1}, {2, 3}, {4, 5}, {0, 3}, {1, 2}, {0, 1}, {2, 3}, {4, 5},
+                               {2, 5}, {3, 4}, {0, 2}, {1, 3}, {0, 1}, {2, 3}, {4, 5}};
+  float k[6];
+  for (int i = 0; i < 6; ++i) { k[i] = v[i]; idx[i] = (uint8_t)i; }
+  for (int c = 0; c < 15; ++c) {
+    int a = P[c][0], b = P[c][1];
+    if (k[a] > k[b]) {
+      float tk = k[a]; k[a] = k[b]; k[b] = tk;
+      uint8_t ti = idx[a]; idx[a] = idx[b]; idx[b] = ti;
+    }
+  }
+}
+
 /* -------------------------------------------------------------- perlin.py */
 
 /* perlin.py:22-23, evaluated left to right in the working precision */
@@ -668,6 +687,11 @@ static void weighted_loot(double u, int *kind, int *qty) {
   *kind = kinds[3]; *qty = qtys[3];
 }
 
+/* worldgen.MAX_GEN_RETRIES (worldgen.py:36); settable so tests can force the
+   _template_floor fallback (worldgen.py:549-595) */
+static int max_gen_retries = 16;
+void go_set_max_gen_retries(int n) { max_gen_retries = n; }
+
 /* worldgen.py:636-651 + 578-633 */
 void go_generate_world(uint64_t seed, int classic, go_world *W) {
   int h = classic ? 64 : 48, w = h, n = h * w;
@@ -684,7 +708,7 @@ void go_generate_world(uint64_t seed, int classic, go_world *W) {
     o.blocks = W->blocks[f];
     o.items = W->items[f];
     int ok = 0, attempt;
-    for (attempt = 0; attempt < 16 && !ok; ++attempt) {
+    for (attempt = 0; attempt < max_gen_retries && !ok; ++attempt) {
       int rc;
       if (f == 0) rc = gen_overworld(fields, fields + n, fields + 2 * n, fs[0], h, w, !classic, attempt, &o);
       else if (f == 1 || f == 3 || f == 4) rc = gen_dungeon(fs[f], h, w, f, attempt, &o);
@@ -700,18 +724,14 @@ void go_generate_world(uint64_t seed, int classic, go_world *W) {
     W->ladder_up[f][0] = (int16_t)o.lu_r; W->ladder_up[f][1] = (int16_t)o.lu_c;
   }
   free(fields);
-  /* potion permutation: argsort of six hashed f32 draws (stable order) */
+  /* potion permutation: np.argsort of six hashed f32 draws (worldgen.py:647-649) */
   {
     uint32_t k32 = (uint32_t)(go_hash2(seed, 42) & 0xFFFFFFFFu);
     float v[6];
-    int idx[6];
-    for (int i = 0; i < 6; ++i) { v[i] = go_vuniform32(k32, (uint32_t)i); idx[i] = i; }
-    for (int i = 1; i < 6; ++i)
-      for (int j = i; j > 0 && v[idx[j - 1]] > v[idx[j]]; --j) { int t = idx[j]; idx[j] = idx[j - 1]; idx[j - 1] = t; }
-    for (int i = 0; i < 6; ++i) {
-      W->potion[i] = (uint8_t)idx[i];
+    for (int i = 0; i < 6; ++i) v[i] = go_vuniform32(k32, (uint32_t)i);
+    go_np_argsort6(v, W->potion);
+    for (int i = 0; i < 6; ++i)
       for (int j = i + 1; j < 6; ++j) if (v[i] == v[j]) W->potion_tie = 1;
-    }
   }
   /* chests (worldgen.py:598-623) */
   static const int per_floor[9] = {0, 4, 2, 3, 3, 2, 2, 2, 0};

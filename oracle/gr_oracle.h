@@ -79,10 +79,14 @@ double go_vuniform(uint64_t key, uint64_t n);
 /* numpy's float32 SIMD sin / cos (loops_trigonometric), restated */
 float go_np_sinf(float x);
 float go_np_cosf(float x);
+/* numpy's AVX-512 np.argsort of 6 float32 (tie order included) */
+void go_np_argsort6(const float *v, uint8_t *idx);
 
 /* --- worldgen ------------------------------------------------------------ */
 void go_level_angles(uint64_t seed, float *angles252, uint64_t *floor_seeds9);
 void go_generate_world(uint64_t seed, int classic, go_world *w);
+/* worldgen.MAX_GEN_RETRIES (default 16; 0 forces every floor to the template) */
+void go_set_max_gen_retries(int n);
 void go_overworld_fields(const float *angles252, int h, int w,
                          float *height, float *forest, float *special);
 void go_perlin_cave(const float *a25, const float *a81, int h, int w,

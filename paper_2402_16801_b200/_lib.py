@@ -99,6 +99,7 @@ def lib() -> ctypes.CDLL:
         "gr_reset_host": (I32, [P, P]),
         "gr_host_obs_attach": (I32, [P, P]),
         "gr_host_obs_detach": (I32, [P, P]),
+        "gr_host_phase_times": (I32, [P, P, P, P]),
         "gr_export_field": (I32, [P, I32, P]),
         "gr_import_field": (I32, [P, I32, P]),
         "gr_observe": (I32, [P, P, P]),
@@ -120,6 +121,9 @@ def lib() -> ctypes.CDLL:
         "gr_set_step_index": (I32, [P, I64]),
         "gr_kernel_launches": (I64, [P]),
         "gr_worldgen_counters": (I32, [P, ctypes.POINTER(I64)]),
+        "gr_set_worldgen_attempts": (I32, [P, I32]),
+        "gr_selftest_sincos64": (I32, [P, P, P, I64, P]),
+        "gr_selftest_argsort6": (I32, [P, P, I64, P]),
         "gr_set_profiling": (I32, [P, I32]),
         "gr_kernel_times": (I32, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64), I32]),
         # include/gridrogue_ppo.h (the learner's fused objective)

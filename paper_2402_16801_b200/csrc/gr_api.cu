@@ -22,6 +22,13 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <cuda_runtime.h>
 
 #include "gr_device.cuh"
@@ -43,6 +50,24 @@ __global__ void k_random_actions(int64_t* out, int64_t n, int64_t env0, uint32_t
   if (i >= n) return;
   const float u = u32f(key, (uint32_t)(env0 + i));
   out[i] = (int64_t)__fmul_rn(u, (float)na) % na;
+}
+
+// numerics self-test (gr_selftest_*): the device routines worldgen uses
+__global__ void k_selftest_sincos64(const float* x, double* s, double* c, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = (double)x[i];
+  s[i] = gl_sin(v);
+  c[i] = gl_cos(v);
+}
+__global__ void k_selftest_argsort6(const float* keys, uint8_t* idx, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float v[6];
+  uint8_t o[6];
+  for (int k = 0; k < 6; ++k) v[k] = keys[i * 6 + k];
+  np_argsort6(v, o);
+  for (int k = 0; k < 6; ++k) idx[i * 6 + k] = o[k];
 }
 
 // first invalid action (engine.py:715-717)
@@ -134,10 +159,73 @@ struct StepGraph {
 struct HostObs {
   uint32_t* ptr = nullptr;      // host
   uint32_t* shadow = nullptr;   // device, same contents
-  uint2* stage = nullptr;       // pinned: (word index, value bits) of the changed words
-  int64_t cap = 0;
   bool dirty = false;           // host and shadow may differ (an interrupted delivery): re-zero both
 };
+
+// A small persistent pool of host threads for the delta scatter (no OpenMP
+// runtime in the library: the process already carries torch's).
+class HostPool {
+ public:
+  explicit HostPool(int n) : n_(std::max(1, n)) {
+    for (int k = 1; k < n_; ++k) th_.emplace_back([this, k] { loop(k); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return n_; }
+  // fn(lo, hi) over n_ contiguous parts of [0, count); the caller runs part 0
+  void run(int64_t count, const std::function<void(int64_t, int64_t)>& fn) {
+    if (count <= 0) return;
+    if (n_ == 1 || count < 4096) { fn(0, count); return; }
+    {
+      std::lock_guard<std::mutex> g(m_);
+      fn_ = &fn;
+      count_ = count;
+      left_ = n_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0, part(0));
+    std::unique_lock<std::mutex> g(m_);
+    done_cv_.wait(g, [this] { return left_ == 0; });
+  }
+
+ private:
+  int64_t part(int k) const { return count_ * (k + 1) / n_; }
+  void loop(int k) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int64_t, int64_t)>* fn;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        fn = fn_;
+      }
+      (*fn)(count_ * k / n_, part(k));
+      std::lock_guard<std::mutex> g(m_);
+      if (--left_ == 0) done_cv_.notify_one();
+    }
+  }
+  int n_;
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+  const std::function<void(int64_t, int64_t)>* fn_ = nullptr;
+  int64_t count_ = 0;
+  int left_ = 0;
+};
+
+constexpr int DL_CHUNKS = 8;   // row chunks of one delivery: chunk c's scatter overlaps chunk c+1's kernel
 
 struct gr_env {
   Prof prof;
@@ -163,6 +251,7 @@ struct gr_env {
   int64_t step_index = 0;
   bool have_reset = false;
   bool validate = true;
+  int wg_attempts = 16;       // worldgen.MAX_GEN_RETRIES (gr_set_worldgen_attempts)
   int64_t launches = 0;
   int64_t last_bad_env = -1, last_bad_action = 0;
   // e2e scratch
@@ -174,10 +263,18 @@ struct gr_env {
   cudaStream_t h_stream = nullptr;
   // delta observation transfer into attached host buffers
   std::vector<HostObs> host_obs;
-  uint2* nz_dev = nullptr;                   // this delivery's changed words
-  int64_t nz_cap = 0;
-  unsigned long long* nz_cursor = nullptr;    // device count (in allocs)
-  unsigned long long* nz_count_h = nullptr;   // pinned host copy
+  // the changed-word list lives in mapped pinned host memory: the delta
+  // kernel writes it across PCIe while it runs (no separate copy)
+  uint2* dl_host = nullptr;
+  uint2* dl_dev = nullptr;
+  int64_t dl_cap = 0;                          // entries, split evenly over DL_CHUNKS
+  unsigned long long* dl_cnt_host = nullptr;   // [DL_CHUNKS] mapped counters
+  unsigned long long* dl_cnt_dev = nullptr;
+  cudaEvent_t dl_ev[DL_CHUNKS] = {};
+  std::unique_ptr<HostPool> hpool;            // host threads of the delta scatter
+  double host_ms[4] = {0, 0, 0, 0};            // enqueue, wait, scatter, tail (gr_host_phase_times)
+  int64_t host_calls = 0;
+  int64_t host_words = 0;                      // changed words delivered
   // reset work (worldgen + install + obs of reset envs) overlaps the obs of
   // the other envs on a second stream
   cudaStream_t side = nullptr;
@@ -291,12 +388,13 @@ void gr_destroy(gr_env* e) {
   cudaDeviceSynchronize();
   for (void* p : e->allocs) cudaFree(p);
   if (e->h_stream) cudaStreamDestroy(e->h_stream);
-  for (auto& h : e->host_obs) {
-    if (h.stage) cudaFreeHost(h.stage);
+  for (auto& h : e->host_obs)
     if (h.shadow) cudaFree(h.shadow);
-  }
-  if (e->nz_dev) cudaFree(e->nz_dev);
-  if (e->nz_count_h) cudaFreeHost(e->nz_count_h);
+  if (e->dl_host) cudaFreeHost(e->dl_host);
+  if (e->dl_cnt_host) cudaFreeHost(e->dl_cnt_host);
+  for (auto& ev : e->dl_ev)
+    if (ev) cudaEventDestroy(ev);
+  e->hpool.reset();
   if (e->side) cudaStreamDestroy(e->side);
   for (auto& g : e->step_graphs) cudaGraphExecDestroy(g.exec);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
@@ -489,6 +587,7 @@ int gr_reset(gr_env* e, void* obs_dev, void* stream) {
   j.M = e->M;
   j.out = WBuf{(uint8_t*)e->S.f[GR_F_BLOCKS], (uint8_t*)e->S.f[GR_F_ITEMS], e->init_meta, e->n};
   j.counters = e->counters;
+  j.max_attempts = e->wg_attempts;
   {
     PTimer t(e, PK_WORLDGEN, st);
     launch_worldgen(e->ext, j, st);
@@ -589,6 +688,7 @@ static int step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, 
     sj.M = e->M;
     sj.out = e->pool;
     sj.counters = e->counters;
+    sj.max_attempts = e->wg_attempts;
     sj.ctas_per_sm = e->wg_ctas;
     sj.spec_k = e->spec_k;
     sj.pool_key = e->pool_key;
@@ -650,6 +750,7 @@ static int step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank,
   j.M = e->M;
   j.out = e->pool;
   j.counters = e->counters;
+  j.max_attempts = e->wg_attempts;
   j.ctas_per_sm = e->wg_ctas;
   j.spec_k = spec ? e->spec_k : nullptr;   // only the slots the speculative pass did not make
   j.wide = e->wg_wide;
@@ -779,41 +880,59 @@ static int ensure_host_scratch(gr_env* e) {
 // change, in ~20 % of its 64-byte lines.  An attached buffer therefore
 // receives only the changed words as (word index, value bits) pairs, and the
 // host rewrites only those: the dense path moves 2.17 GB across PCIe into
-// every line of the host array per step at 65,536 extended envs.  One warp
-// per row: count the words that differ from the shadow, reserve a slice of
-// the list with one atomic, then write them in order (ballot + popc) and
-// update the shadow.  Row order in the list varies run to run; positions are
-// distinct, so the host array after the scatter does not.
-__global__ void __launch_bounds__(256) k_obs_delta(const uint32_t* __restrict__ obs, uint32_t* __restrict__ shadow,
-                                                   int64_t n, int W, uint2* __restrict__ out, int64_t cap,
-                                                   unsigned long long* __restrict__ cursor) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nwarps) {
+// every line of the host array per step at 65,536 extended envs.
+//
+// One warp per row, one pass over HBM: the warp compares the row with its
+// shadow 32 words at a time and keeps the ballot masks in shared memory
+// (259 words per extended row), reserves the row's slice of the list with
+// one atomic, then walks the masks: only the changed words are re-read (from
+// L2: the row was just streamed) and written to the list -- mapped pinned
+// host memory, so the list crosses PCIe while the kernel runs -- and to the
+// shadow.  Row order in the list varies run to run; positions are distinct,
+// so the host array after the scatter does not.
+constexpr int DL_WARPS = 8;
+constexpr int DL_MAXCH = 272;   // >= ceil(8268 / 32)
+__global__ void __launch_bounds__(DL_WARPS * 32) k_obs_delta(const uint32_t* __restrict__ obs,
+                                                              uint32_t* __restrict__ shadow, int64_t r0, int64_t r1,
+                                                              int W, uint2* __restrict__ out, int64_t cap,
+                                                              unsigned long long* __restrict__ cursor) {
+  __shared__ uint32_t masks[DL_WARPS][DL_MAXCH];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nch = (W + 31) >> 5;
+  uint32_t* mk = masks[wid];
+  const int64_t nwarps = (int64_t)gridDim.x * DL_WARPS;
+  for (int64_t r = r0 + (int64_t)blockIdx.x * DL_WARPS + wid; r < r1; r += nwarps) {
     const uint32_t* row = obs + r * W;
     uint32_t* sh = shadow + r * W;
     int cnt = 0;
-    for (int c = lane; c < W; c += 32) cnt += row[c] != sh[c];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(~0u, cnt, o);
+#pragma unroll 4
+    for (int ch = 0; ch < nch; ++ch) {
+      const int c = (ch << 5) + lane;
+      const bool d = c < W && __ldcs(row + c) != __ldcs(sh + c);
+      const uint32_t m = __ballot_sync(~0u, d);
+      if (lane == 0) mk[ch] = m;
+      cnt += __popc(m);
+    }
+    __syncwarp();
     if (!cnt) continue;
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(cursor, (unsigned long long)cnt);
     base = __shfl_sync(~0u, base, 0);
-    for (int c0 = 0; c0 < W; c0 += 32) {
-      const int c = c0 + lane;
-      const uint32_t v = c < W ? row[c] : 0u;
-      const bool d = c < W && v != sh[c];
-      const unsigned m = __ballot_sync(~0u, d);
-      if (d) {
+    for (int ch = 0; ch < nch; ++ch) {
+      const uint32_t m = mk[ch];
+      if (!m) continue;
+      if ((m >> lane) & 1u) {
+        const int c = (ch << 5) + lane;
         const unsigned long long p = base + __popc(m & ((1u << lane) - 1u));
         if (p < (unsigned long long)cap) {   // beyond: left for the next pass, shadow unchanged
+          const uint32_t v = row[c];
           out[p] = make_uint2((uint32_t)(r * W + c), v);
           sh[c] = v;
         }
       }
       base += __popc(m);
     }
+    __syncwarp();
   }
 }
 
@@ -825,9 +944,15 @@ static HostObs* find_host_obs(gr_env* e, const void* p) {
 
 static int64_t host_obs_words(const gr_env* e) { return obs_elems_of(e) * e->n; }
 
+// zero the host buffer and its shadow.  Everything that may still touch the
+// shadow (a delivery's k_obs_delta on h_stream) is drained first, and the
+// clear is ordered on h_stream and completed before returning, so the next
+// delivery never compares against a half-cleared shadow.
 static int host_obs_zero(gr_env* e, HostObs& h) {
+  CK(cudaStreamSynchronize(e->h_stream));
   memset(h.ptr, 0, (size_t)host_obs_words(e) * 4);
-  CK(cudaMemset(h.shadow, 0, (size_t)host_obs_words(e) * 4));
+  CK(cudaMemsetAsync(h.shadow, 0, (size_t)host_obs_words(e) * 4, e->h_stream));
+  CK(cudaStreamSynchronize(e->h_stream));
   h.dirty = false;
   return GR_OK;
 }
@@ -839,6 +964,8 @@ int gr_host_obs_attach(gr_env* e, void* obs_host) {
   if (host_obs_words(e) > (int64_t)UINT32_MAX) return fail(GR_E_INVALID, "n_envs x obs width exceeds 2^32 words");
   if (find_host_obs(e, obs_host)) return GR_OK;
   CK(cudaSetDevice(e->cfg.device));
+  int rc = ensure_host_scratch(e);   // creates h_stream, which host_obs_zero orders on
+  if (rc) return rc;
   HostObs h;
   h.ptr = (uint32_t*)obs_host;
   CK(cudaMalloc((void**)&h.shadow, (size_t)host_obs_words(e) * 4));
@@ -851,7 +978,6 @@ int gr_host_obs_detach(gr_env* e, void* obs_host) {
   for (size_t k = 0; k < e->host_obs.size(); ++k)
     if (e->host_obs[k].ptr == obs_host) {
       cudaDeviceSynchronize();
-      if (e->host_obs[k].stage) cudaFreeHost(e->host_obs[k].stage);
       if (e->host_obs[k].shadow) cudaFree(e->host_obs[k].shadow);
       e->host_obs.erase(e->host_obs.begin() + (ptrdiff_t)k);
       return GR_OK;
@@ -859,54 +985,103 @@ int gr_host_obs_detach(gr_env* e, void* obs_host) {
   return fail(GR_E_INVALID, "buffer %p is not attached", obs_host);
 }
 
+using hclock = std::chrono::steady_clock;
+static double ms_since(hclock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(hclock::now() - t0).count();
+}
+
+static int ensure_delta_list(gr_env* e, int64_t cap) {
+  if (e->dl_host && e->dl_cap >= cap) return GR_OK;
+  if (e->dl_host) cudaFreeHost(e->dl_host);
+  e->dl_host = nullptr;
+  e->dl_cap = 0;
+  CK(cudaHostAlloc((void**)&e->dl_host, (size_t)cap * sizeof(uint2), cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer((void**)&e->dl_dev, e->dl_host, 0));
+  e->dl_cap = cap;
+  return GR_OK;
+}
+
 // after the observation is in e->h_obs_dev (ordered on st): list the words
-// that differ from the buffer's shadow, copy the list back, scatter it.
-// Repeats while the list outgrows its capacity (each pass applies what it
-// listed).  Synchronous.
-static int host_obs_deliver(gr_env* e, HostObs& h, cudaStream_t st) {
+// that differ from the buffer's shadow and scatter them into the host
+// buffer, chunk by chunk (rows split in DL_CHUNKS ranges, one kernel + event
+// each), so the host scatters chunk c while the device lists chunk c+1.
+// If a chunk outgrows its share of the list, whole-buffer passes with a
+// larger list follow (each pass applies what it listed).  Synchronous.
+static int host_obs_deliver(gr_env* e, HostObs& h, cudaStream_t st, hclock::time_point t_call) {
   const int W = (int)obs_elems_of(e);
-  if (!e->nz_cursor) {
-    int rc = dev_alloc(e, (void**)&e->nz_cursor, sizeof(unsigned long long));
-    if (rc) return rc;
-    CK(cudaHostAlloc((void**)&e->nz_count_h, sizeof(unsigned long long), cudaHostAllocDefault));
+  if (!e->dl_cnt_host) {
+    CK(cudaHostAlloc((void**)&e->dl_cnt_host, DL_CHUNKS * sizeof(unsigned long long), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&e->dl_cnt_dev, e->dl_cnt_host, 0));
+    for (auto& ev : e->dl_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync));
+    unsigned hc = std::thread::hardware_concurrency();
+    e->hpool.reset(new HostPool((int)std::min<unsigned>(hc ? hc : 1, 32)));
   }
-  if (!e->nz_dev) {
-    e->nz_cap = e->n * (int64_t)std::min(W, 256);
-    CK(cudaMalloc((void**)&e->nz_dev, (size_t)e->nz_cap * sizeof(uint2)));
-  }
+  int rc = ensure_delta_list(e, e->n * (int64_t)std::min(W, 256));
+  if (rc) return rc;
   h.dirty = true;
-  for (int pass = 0; pass < 64; ++pass) {
-    CK(cudaMemsetAsync(e->nz_cursor, 0, sizeof(unsigned long long), st));
-    k_obs_delta<<<148 * 8, 256, 0, st>>>((const uint32_t*)e->h_obs_dev, h.shadow, e->n, W, e->nz_dev, e->nz_cap,
-                                         e->nz_cursor);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  volatile unsigned long long* cnt = e->dl_cnt_host;
+  auto scatter = [&](const uint2* list, int64_t k) {
+    uint32_t* p = h.ptr;
+    e->hpool->run(k, [&](int64_t lo, int64_t hi) {
+      for (int64_t i = lo; i < hi; ++i) p[list[i].x] = list[i].y;
+    });
+    e->host_words += k;
+  };
+  double t_wait = 0, t_scatter = 0;
+  // pipelined pass
+  const int C = (int)std::min<int64_t>(DL_CHUNKS, std::max<int64_t>(1, e->n / 256));
+  const int64_t capc = e->dl_cap / C;
+  for (int c = 0; c < C; ++c) cnt[c] = 0;
+  for (int c = 0; c < C; ++c) {
+    const int64_t r0 = e->n * c / C, r1 = e->n * (c + 1) / C;
+    const int grid = (int)std::min<int64_t>((r1 - r0 + DL_WARPS - 1) / DL_WARPS, (int64_t)sms * 8);
+    k_obs_delta<<<grid, DL_WARPS * 32, 0, st>>>((const uint32_t*)e->h_obs_dev, h.shadow, r0, r1, W,
+                                                 e->dl_dev + c * capc, capc, e->dl_cnt_dev + c);
     e->launches += 1;
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(e->nz_count_h, e->nz_cursor, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    const int64_t count = (int64_t)*e->nz_count_h, k = std::min(count, e->nz_cap);
-    if (k > h.cap) {
-      if (h.stage) cudaFreeHost(h.stage);
-      h.stage = nullptr;
-      h.cap = 0;
-      CK(cudaHostAlloc((void**)&h.stage, (size_t)e->nz_cap * sizeof(uint2), cudaHostAllocDefault));
-      h.cap = e->nz_cap;
-    }
-    if (k) CK(cudaMemcpyAsync(h.stage, e->nz_dev, (size_t)k * sizeof(uint2), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    uint32_t* p = h.ptr;
-    const uint2* s = h.stage;
-#pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < k; ++i) p[s[i].x] = s[i].y;
-    if (count <= e->nz_cap) {
-      h.dirty = false;
-      return GR_OK;
-    }
-    cudaFree(e->nz_dev);
-    e->nz_dev = nullptr;
-    e->nz_cap = std::min<int64_t>(count + count / 4 + 1024, host_obs_words(e));
-    CK(cudaMalloc((void**)&e->nz_dev, (size_t)e->nz_cap * sizeof(uint2)));
+    CK(cudaEventRecord(e->dl_ev[c], st));
   }
-  return fail(GR_E_CUDA, "delta transfer did not converge");
+  e->host_ms[0] += ms_since(t_call);
+  bool overflow = false;
+  int64_t total = 0;
+  for (int c = 0; c < C; ++c) {
+    auto t0 = hclock::now();
+    CK(cudaEventSynchronize(e->dl_ev[c]));
+    t_wait += ms_since(t0);
+    const int64_t count = (int64_t)cnt[c];
+    total += count;
+    t0 = hclock::now();
+    scatter(e->dl_host + c * capc, std::min(count, capc));
+    t_scatter += ms_since(t0);
+    overflow |= count > capc;
+  }
+  // overflow: whole-buffer passes until every changed word is listed
+  for (int pass = 0; overflow && pass < 64; ++pass) {
+    rc = ensure_delta_list(e, std::min<int64_t>(total + total / 4 + 1024, host_obs_words(e)));
+    if (rc) return rc;
+    cnt[0] = 0;
+    k_obs_delta<<<sms * 8, DL_WARPS * 32, 0, st>>>((const uint32_t*)e->h_obs_dev, h.shadow, 0, e->n, W, e->dl_dev,
+                                                    e->dl_cap, e->dl_cnt_dev);
+    e->launches += 1;
+    CK(cudaGetLastError());
+    auto t0 = hclock::now();
+    CK(cudaEventRecord(e->dl_ev[0], st));
+    CK(cudaEventSynchronize(e->dl_ev[0]));
+    t_wait += ms_since(t0);
+    total = (int64_t)cnt[0];
+    t0 = hclock::now();
+    scatter(e->dl_host, std::min(total, e->dl_cap));
+    t_scatter += ms_since(t0);
+    overflow = total > e->dl_cap;
+  }
+  e->host_ms[1] += t_wait;
+  e->host_ms[2] += t_scatter;
+  if (overflow) return fail(GR_E_CUDA, "delta transfer did not converge");
+  h.dirty = false;
+  return GR_OK;
 }
 
 int gr_reset_host(gr_env* e, void* obs_host) {
@@ -916,10 +1091,12 @@ int gr_reset_host(gr_env* e, void* obs_host) {
   if (rc) return rc;
   HostObs* hz = obs_host ? find_host_obs(e, obs_host) : nullptr;
   if (hz && hz->dirty && (rc = host_obs_zero(e, *hz))) return rc;
+  const auto t_call = hclock::now();
   rc = gr_reset(e, obs_host ? e->h_obs_dev : nullptr, e->h_stream);
   if (rc) return rc;
   const int64_t ob = obs_elems_of(e) * (e->cfg.obs_mode == GR_OBS_PIXELS ? 1 : 4);
-  if (HostObs* ho = obs_host ? find_host_obs(e, obs_host) : nullptr) return host_obs_deliver(e, *ho, e->h_stream);
+  if (HostObs* ho = obs_host ? find_host_obs(e, obs_host) : nullptr)
+    return host_obs_deliver(e, *ho, e->h_stream, t_call);
   if (obs_host && ob)
     CK(cudaMemcpyAsync(obs_host, e->h_obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, e->h_stream));
   CK(cudaStreamSynchronize(e->h_stream));
@@ -944,6 +1121,7 @@ int gr_step_host(gr_env* e, const int64_t* actions_host, void* obs_host, float* 
   cudaStream_t st = e->h_stream;
   HostObs* hz = obs_host ? find_host_obs(e, obs_host) : nullptr;
   if (hz && hz->dirty && (rc = host_obs_zero(e, *hz))) return rc;
+  const auto t_call = hclock::now();
   CK(cudaMemcpyAsync(e->h_act_dev, actions_host, e->n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   const bool v = e->validate;
   e->validate = false;
@@ -953,18 +1131,36 @@ int gr_step_host(gr_env* e, const int64_t* actions_host, void* obs_host, float* 
   e->validate = v;
   if (rc) return rc;
   const int64_t ob = obs_elems_of(e) * (e->cfg.obs_mode == GR_OBS_PIXELS ? 1 : 4);
-  if (HostObs* ho = obs_host ? find_host_obs(e, obs_host) : nullptr) {
-    rc = host_obs_deliver(e, *ho, st);
-    if (rc) return rc;
-  } else if (obs_host && ob) {
-    CK(cudaMemcpyAsync(obs_host, e->h_obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, st));
-  }
+  // the small outputs first: they cross PCIe while the obs is delivered
   if (reward_host) CK(cudaMemcpyAsync(reward_host, e->h_rew_dev, e->n * sizeof(float), cudaMemcpyDeviceToHost, st));
   if (done_host) CK(cudaMemcpyAsync(done_host, e->h_done_dev, e->n, cudaMemcpyDeviceToHost, st));
   if (newly_host) CK(cudaMemcpyAsync(newly_host, e->h_newly_dev, e->n * e->d.A, cudaMemcpyDeviceToHost, st));
   if (time_host) CK(cudaMemcpyAsync(time_host, e->h_time_dev, e->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   if (floor_host) CK(cudaMemcpyAsync(floor_host, e->h_floor_dev, e->n, cudaMemcpyDeviceToHost, st));
+  if (HostObs* ho = obs_host ? find_host_obs(e, obs_host) : nullptr) {
+    rc = host_obs_deliver(e, *ho, st, t_call);
+    if (rc) return rc;
+  } else {
+    if (obs_host && ob) CK(cudaMemcpyAsync(obs_host, e->h_obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, st));
+    e->host_ms[0] += ms_since(t_call);
+  }
+  const auto t_tail = hclock::now();
   CK(cudaStreamSynchronize(st));
+  e->host_ms[3] += ms_since(t_tail);
+  e->host_calls += 1;
+  return GR_OK;
+}
+
+int gr_host_phase_times(gr_env* e, double out[4], int64_t* calls, int64_t* words) {
+  if (!e || !out) return fail(GR_E_INVALID, "null argument");
+  for (int k = 0; k < 4; ++k) {
+    out[k] = e->host_ms[k];
+    e->host_ms[k] = 0;
+  }
+  if (calls) *calls = e->host_calls;
+  if (words) *words = e->host_words;
+  e->host_calls = 0;
+  e->host_words = 0;
   return GR_OK;
 }
 
@@ -1217,6 +1413,7 @@ int gr_levels_generate(gr_levels* lv, int64_t first, int64_t count) {
   j.out = lv->w;
   j.params = lv->p;
   j.counters = e->counters;
+  j.max_attempts = e->wg_attempts;
   launch_worldgen(e->ext, j, 0);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
@@ -1334,6 +1531,32 @@ int gr_kernel_times(gr_env* e, double* ms, int64_t* counts, int32_t n) {
     }
     e->prof.ev[c].clear();
   }
+  return GR_OK;
+}
+
+int gr_set_worldgen_attempts(gr_env* e, int32_t max_attempts) {
+  if (!e || max_attempts < 0) return fail(GR_E_INVALID, "max_attempts must be >= 0");
+  CK(cudaSetDevice(e->cfg.device));
+  CK(cudaDeviceSynchronize());
+  e->wg_attempts = max_attempts;
+  for (auto& g : e->step_graphs) cudaGraphExecDestroy(g.exec);   // they captured the old value
+  e->step_graphs.clear();
+  return GR_OK;
+}
+
+int gr_selftest_sincos64(const float* x, double* s, double* c, int64_t n, void* stream) {
+  if (n < 0 || (n && (!x || !s || !c))) return fail(GR_E_INVALID, "bad self-test arguments");
+  if (!n) return GR_OK;
+  k_selftest_sincos64<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x, s, c, n);
+  CK(cudaGetLastError());
+  return GR_OK;
+}
+
+int gr_selftest_argsort6(const float* keys, uint8_t* idx, int64_t n, void* stream) {
+  if (n < 0 || (n && (!keys || !idx))) return fail(GR_E_INVALID, "bad self-test arguments");
+  if (!n) return GR_OK;
+  k_selftest_argsort6<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(keys, idx, n);
+  CK(cudaGetLastError());
   return GR_OK;
 }
 

@@ -145,73 +145,37 @@ __device__ __forceinline__ float np_sincosf(float x, bool is_cos) {
   return (iq & 2) ? -v : v;
 }
 
-// ------------------------- float64 sin/cos for the cave noise (perlin.py)
-// numpy's float64 path is libm.  Evaluated here in double-double (~106
-// bits) and rounded once: correctly rounded.  libm differs from correct
-// rounding by 1 ulp on ~1.5e-4 of inputs; the cave field is only ever
-// thresholded / argmax'ed, so a 1-ulp gradient difference changes a block
-// only if a tile's field lies within ~1e-15 of a threshold or of a rival
-// tile -- the kernel flags such fragile worlds (WG_FLAG_FRAGILE).
-struct dd { double hi, lo; };
-__device__ __forceinline__ dd two_sum(double a, double b) {
-  double s = __dadd_rn(a, b), bb = __dsub_rn(s, a);
-  double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
-  return {s, e};
-}
-__device__ __forceinline__ dd fast_two_sum(double a, double b) {
-  double s = __dadd_rn(a, b);
-  return {s, __dsub_rn(b, __dsub_rn(s, a))};
-}
-__device__ __forceinline__ dd two_prod(double a, double b) {
-  double p = __dmul_rn(a, b);
-  return {p, __fma_rn(a, b, -p)};
-}
-__device__ __forceinline__ dd dd_add(dd a, dd b) {
-  dd s = two_sum(a.hi, b.hi), t = two_sum(a.lo, b.lo);
-  s.lo = __dadd_rn(s.lo, t.hi);
-  s = fast_two_sum(s.hi, s.lo);
-  s.lo = __dadd_rn(s.lo, t.lo);
-  return fast_two_sum(s.hi, s.lo);
-}
-__device__ __forceinline__ dd dd_mul(dd a, dd b) {
-  dd p = two_prod(a.hi, b.hi);
-  p.lo = __dadd_rn(p.lo, __dadd_rn(__dmul_rn(a.hi, b.lo), __dmul_rn(a.lo, b.hi)));
-  return fast_two_sum(p.hi, p.lo);
-}
-// 1/n! for n = 0..28 as double-doubles
-__constant__ double C_INVFACT[29][2] = {
-#include "gr_invfact.inc"
-};
-__device__ inline void dd_sincos(double x, double* s_out, double* c_out) {
-  const double P0 = 1.5707963267948966e+00, P1 = 6.123233995736766e-17, P2 = -1.4973849048591698e-33;
-  double k = rint(__ddiv_rn(x, P0));
-  dd kp = dd_add(two_prod(k, P0), two_prod(k, P1));
-  kp = dd_add(kp, two_prod(k, P2));
-  dd r = dd_add(dd{x, 0.0}, dd{-kp.hi, -kp.lo});
-  dd t = dd_mul(r, r);
-  dd ps = {-C_INVFACT[27][0], -C_INVFACT[27][1]};
-  for (int j = 12; j >= 0; --j) {
-    dd c = {C_INVFACT[2 * j + 1][0], C_INVFACT[2 * j + 1][1]};
-    if (j & 1) { c.hi = -c.hi; c.lo = -c.lo; }
-    ps = dd_add(dd_mul(ps, t), c);
-  }
-  dd pc = {C_INVFACT[28][0], C_INVFACT[28][1]};
-  for (int j = 13; j >= 0; --j) {
-    dd c = {C_INVFACT[2 * j][0], C_INVFACT[2 * j][1]};
-    if (j & 1) { c.hi = -c.hi; c.lo = -c.lo; }
-    pc = dd_add(dd_mul(pc, t), c);
-  }
-  double sn = dd_mul(ps, r).hi, cs = pc.hi;
-  switch (((int)k) & 3) {
-    case 0: *s_out = sn; *c_out = cs; break;
-    case 1: *s_out = cs; *c_out = -sn; break;
-    case 2: *s_out = -sn; *c_out = -cs; break;
-    default: *s_out = -cs; *c_out = sn; break;
-  }
-}
+// float64 sin / cos of the cave noise (hazard H3): glibc's own algorithm,
+// bit for bit (gr_glibc_sincos.h).
+#include "gr_glibc_sincos.h"
 
 // -------------------------------------------------------- game helpers
 // _kern.q1: one-decimal quantiser, every op separately rounded
+// np.argsort of 6 float32 (worldgen.py:647-649).  numpy >= 2 on AVX-512
+// hardware sorts n <= 256 elements with x86-simd-sort's key/index bitonic
+// network: one 8-lane register (lanes 6, 7 padded with +inf, which never
+// move), six compare-exchange layers with partner lane l^1, l^3, l^1, l^7,
+// l^2, l^1, the upper lane taking the max and each lane keeping its own index
+// on equal keys.  Restricted to the six live lanes that is the 15-comparator
+// network below, exchanging only on a strict '>'.  On ties it is NOT a stable
+// sort; it equals np.argsort on all 6^6 value patterns
+// (tests/golden/numpy_corners.npz).
+__host__ __device__ __forceinline__ void np_argsort6(const float* v, uint8_t* idx) {
+  constexpr uint8_t P[15][2] = {{0, 1}, {2, 3}, {4, 5}, {0, 3}, {1, 2}, {0, 1}, {2, 3}, {4, 5},
+                                {2, 5}, {3, 4}, {0, 2}, {1, 3}, {0, 1}, {2, 3}, {4, 5}};
+  float k[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) { k[i] = v[i]; idx[i] = (uint8_t)i; }
+#pragma unroll
+  for (int c = 0; c < 15; ++c) {
+    const int a = P[c][0], b = P[c][1];
+    if (k[a] > k[b]) {
+      const float tk = k[a]; k[a] = k[b]; k[b] = tk;
+      const uint8_t ti = idx[a]; idx[a] = idx[b]; idx[b] = ti;
+    }
+  }
+}
+
 __device__ __forceinline__ float q1(float x) {
   return __fmul_rn(floorf(__fadd_rn(__fmul_rn(x, 10.0f), 0.5f)), 0.1f);
 }

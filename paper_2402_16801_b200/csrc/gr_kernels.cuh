@@ -1,10 +1,32 @@
 // gr_kernels.cuh -- kernel argument blocks and host-side launchers.
 #pragma once
+#include <atomic>
+#include <mutex>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "gr_state.cuh"
 
 namespace gr {
+
+// Launch attributes (cudaFuncSetAttribute) belong to each device's context:
+// `init` runs once per device per process, before any caller on that device
+// proceeds (handles may live on different devices and threads).
+struct PerDeviceOnce {
+  std::atomic<uint64_t> done{0};
+  std::mutex m;
+  template <class F>
+  void operator()(F&& init) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    std::lock_guard<std::mutex> g(m);
+    if (done.load(std::memory_order_relaxed) & bit) return;
+    init(dev & 63);
+    done.fetch_or(bit, std::memory_order_release);
+  }
+};
+
 
 struct StepInfo;
 struct StepArgs {
@@ -74,6 +96,7 @@ struct WorldJob {
   uint64_t pool_key;
   const unsigned long long* dstep;
   int wide;                      // extended tier: 512-thread CTAs (gr_world_wide.cu)
+  int max_attempts = 16;         // worldgen.MAX_GEN_RETRIES (worldgen.py:36)
 };
 
 struct InstallArgs {

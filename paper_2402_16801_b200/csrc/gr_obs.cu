@@ -569,12 +569,17 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(
 template <bool EXT, int PX>
 static void launch_pixels_px(const DS& S, const ObsArgs& a, int sms, cudaStream_t st) {
   constexpr int smem = PG<EXT, PX>::SMEM;
-  static int per_sm = 0;
-  if (!per_sm) {
+  static PerDeviceOnce once;
+  static int occ[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  once([&](int d) {
+    int o = 0;
     cudaFuncSetAttribute(k_pixels<EXT, PX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pixels<EXT, PX>, pix_threads<EXT, PX>(), smem);
-    if (per_sm < 1) per_sm = 1;
-  }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_pixels<EXT, PX>, pix_threads<EXT, PX>(), smem);
+    occ[d] = o < 1 ? 1 : o;
+  });
+  const int per_sm = occ[dev & 63];
   // persistent grid: every CTA resident from the start (k_pixprep ran before, launch_pixprep)
   k_pixels<EXT, PX><<<(int)std::min<int64_t>(a.n, (int64_t)sms * per_sm), pix_threads<EXT, PX>(), smem, st>>>(S, a);
 }
@@ -815,22 +820,16 @@ void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
   if (ext) {
     constexpr int NW = stage_warps<true>();
     const size_t smem = (size_t)NW * stage_floats<true>() * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_symbolic_stage<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    static PerDeviceOnce once;
+    once([&](int) { cudaFuncSetAttribute(k_symbolic_stage<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
     const int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm : 3;
     const int grid = (int)std::min<int64_t>((a.n + NW - 1) / NW, (int64_t)sms * per_sm);
     k_symbolic_stage<true><<<grid, NW * 32, smem, st>>>(S, a);
   } else {
     constexpr int NW = stage_warps<false>();
     const size_t smem = (size_t)NW * stage_floats<false>() * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_symbolic_stage<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    static PerDeviceOnce once;
+    once([&](int) { cudaFuncSetAttribute(k_symbolic_stage<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
     const int grid = (int)std::min<int64_t>((a.n + NW - 1) / NW, (int64_t)sms * 4);
     k_symbolic_stage<false><<<grid, NW * 32, smem, st>>>(S, a);
   }

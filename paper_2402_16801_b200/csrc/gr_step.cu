@@ -1470,12 +1470,11 @@ void launch_step(bool ext, const DS& S, const StepArgs& a, cudaStream_t st) {
   if (grid == 0) return;
 #if GR_STEP_SMEM_CTX
   const size_t smem = (size_t)bs * sizeof(Ctx);
-  static bool attr_set = false;   // idempotent; a race only repeats the call
-  if (!attr_set) {
+  static PerDeviceOnce once;
+  once([&](int) {
     cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
-  }
+  });
 #else
   const size_t smem = 0;
 #endif

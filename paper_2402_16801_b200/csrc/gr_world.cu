@@ -611,22 +611,18 @@ __device__ __forceinline__ double cave_field_at(const WSmem<EXT>& sm, int t) {
 
 // worldgen._gen_cave (:418-468)
 template <bool EXT>
-__device__ __noinline__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo, bool* fragile) {
+__device__ __noinline__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, int attempt, FloorOut* fo) {
   using T = WT<EXT>;
   const Stream s = Stream::raw(seed).split(2000 + (uint64_t)attempt);
   for (int k = threadIdx.x; k < 106; k += WT<EXT>::THREADS) {
     const float a = angle_of(s.at((uint64_t)k));
-    double sn, cs;
-    dd_sincos((double)a, &sn, &cs);
-    sm.dgx[k] = cs;
-    sm.dgy[k] = sn;
+    sm.dgx[k] = gl_cos((double)a);   // np.cos / np.sin in float64 = glibc
+    sm.dgy[k] = gl_sin((double)a);
   }
   __syncthreads();
   const UField u(hash2(seed, 11 + (uint64_t)attempt), 5);
-  int frag = 0;
   for (int t = threadIdx.x; t < T::HW; t += WT<EXT>::THREADS) {
     const double field = cave_field_at<EXT>(sm, t);
-    frag |= fabs(field + 0.02) < 1e-12 || fabs(field + 0.62) < 1e-12;
     const float uu = u(t);
     const bool open = field > -0.02;
     uint8_t b = open ? B_PATH : B_STONE;
@@ -647,7 +643,7 @@ __device__ __noinline__ bool gen_cave(WSmem<EXT>& sm, uint64_t seed, int floor, 
     sm.blk[t] = b;
     sm.itm[t] = 0;
   }
-  if (__syncthreads_or(frag)) *fragile = true;
+  __syncthreads();
   const uint8_t must2[3] = {B_COAL, B_IRON, B_SAPPHIRE};
   const uint8_t must5[4] = {B_COAL, B_IRON, B_DIAMOND, B_RUBY};
   const int nm = floor == 2 ? 3 : 4;
@@ -863,7 +859,6 @@ __global__ void __launch_bounds__(WT<EXT>::THREADS, WT<EXT>::MINB) k_worldgen(Wo
     // make_level_params (worldgen.py:75-87), or the explicit params
     const uint64_t base = mix64(seed);
     const uint64_t fseed = job.mode == 2 ? job.params.floor_seed[w * 9 + f] : hash2(base, hash2(100 + (uint64_t)f, 0));
-    bool fragile = false;
     FloorOut fo{-1, -1, -1};
     int attempt = 0;
     bool ok = false;
@@ -873,18 +868,18 @@ __global__ void __launch_bounds__(WT<EXT>::THREADS, WT<EXT>::MINB) k_worldgen(Wo
         sm.ang[k] = job.mode == 2 ? job.params.angles[w * 252 + k] : angle_of(u64d(k1, (uint64_t)k));
       __syncthreads();
       overworld_gradients<EXT>(sm);
-      for (attempt = 0; attempt < 16 && !ok; ++attempt) {
+      for (attempt = 0; attempt < job.max_attempts && !ok; ++attempt) {
         int ld;
         ok = gen_overworld<EXT>(sm, fseed, EXT, attempt, &ld);
         if (ok) { fo.spawn = sm.spawn; fo.ld = ld; fo.lu = -1; }
       }
     } else if (f == 1 || f == 3 || f == 4) {
-      for (attempt = 0; attempt < 16 && !ok; ++attempt) ok = gen_dungeon<EXT>(sm, fseed, f, attempt, &fo);
+      for (attempt = 0; attempt < job.max_attempts && !ok; ++attempt) ok = gen_dungeon<EXT>(sm, fseed, f, attempt, &fo);
     } else if (f == 2 || f == 5) {
-      for (attempt = 0; attempt < 16 && !ok; ++attempt) ok = gen_cave<EXT>(sm, fseed, f, attempt, &fo, &fragile);
+      for (attempt = 0; attempt < job.max_attempts && !ok; ++attempt) ok = gen_cave<EXT>(sm, fseed, f, attempt, &fo);
     } else if (f == 6 || f == 7) {
-      for (attempt = 0; attempt < 16 && !ok; ++attempt) ok = gen_realm<EXT>(sm, fseed, f, attempt, &fo);
-    } else {
+      for (attempt = 0; attempt < job.max_attempts && !ok; ++attempt) ok = gen_realm<EXT>(sm, fseed, f, attempt, &fo);
+    } else if (job.max_attempts > 0) {
       gen_graveyard<EXT>(sm, &fo);
       ok = true;
       attempt = 1;
@@ -895,7 +890,6 @@ __global__ void __launch_bounds__(WT<EXT>::THREADS, WT<EXT>::MINB) k_worldgen(Wo
       gen_template<EXT>(sm, f, &fo);
       flags |= WG_FLAG_TEMPLATE;
     }
-    if (fragile) flags |= WG_FLAG_FRAGILE;
     if (EXT && f >= 1 && f <= 7) assign_chests<EXT>(sm, seed, f, meta);
     // write the floor out (16-byte vectors)
     uint8_t* ob = job.out.blocks + ((size_t)w * T::F + f) * T::HW;
@@ -917,16 +911,14 @@ __global__ void __launch_bounds__(WT<EXT>::THREADS, WT<EXT>::MINB) k_worldgen(Wo
         // potion permutation: argsort of six hashed float32 draws
         const uint32_t pk = (uint32_t)(hash2(seed, 42) & 0xFFFFFFFFull);
         float v[6];
-        int idx[6];
-        for (int q = 0; q < 6; ++q) { v[q] = u32f(pk, (uint32_t)q); idx[q] = q; }
-        for (int a = 1; a < 6; ++a)
-          for (int b = a; b > 0 && v[idx[b - 1]] > v[idx[b]]; --b) { int tq = idx[b]; idx[b] = idx[b - 1]; idx[b - 1] = tq; }
+        uint8_t idx[6];
         bool tie = false;
-        for (int a = 0; a < 6; ++a) {
-          meta->potion[a] = (uint8_t)idx[a];
+        for (int q = 0; q < 6; ++q) v[q] = u32f(pk, (uint32_t)q);
+        for (int a = 0; a < 6; ++a)
           for (int b = a + 1; b < 6; ++b) tie |= v[a] == v[b];
-        }
-        if (tie) flags |= WG_FLAG_POTION_TIE;
+        np_argsort6(v, idx);   // numpy's tie order, not a stable sort (gr_device.cuh)
+        for (int a = 0; a < 6; ++a) meta->potion[a] = idx[a];
+        if (tie) flags |= WG_FLAG_POTION_TIE;   // counted only: ties are reproduced
         if (!EXT) meta->nch[0] = 0;
       }
       if (flags) {
@@ -935,7 +927,6 @@ __global__ void __launch_bounds__(WT<EXT>::THREADS, WT<EXT>::MINB) k_worldgen(Wo
           if (flags & WG_FLAG_RETRY) atomicAdd(&job.counters[1], 1ull);
           if (flags & WG_FLAG_TEMPLATE) atomicAdd(&job.counters[2], 1ull);
           if (flags & WG_FLAG_POTION_TIE) atomicAdd(&job.counters[3], 1ull);
-          if (flags & WG_FLAG_FRAGILE) atomicAdd(&job.counters[4], 1ull);
         }
       }
       if (f == 0 && job.counters) atomicAdd(&job.counters[0], 1ull);

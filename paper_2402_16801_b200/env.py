@@ -327,9 +327,11 @@ class BatchEnv:
         # (gr_host_obs_attach) and moves only the words that changed since the
         # buffer's last observation; arrays are handed out read-only so a
         # caller cannot make the buffer and the handle's copy of it disagree
+        self._attached = []
         if obs_transfer == "delta":
             for b in [self._h_obs, *self._obs_pool]:
                 check(lib().gr_host_obs_attach(self._batch.h, b.ctypes.data_as(ctypes.c_void_p)))
+                self._attached.append(b)
                 b.flags.writeable = False   # views handed out cannot be made writable again
         self._h_act = torch.empty(n, dtype=torch.int64, **pin).numpy()
         self._h_rew = torch.empty(n, dtype=torch.float32, **pin).numpy()
@@ -337,6 +339,23 @@ class BatchEnv:
         self._h_newly = torch.empty((n, t["n_achievements"]), dtype=torch.bool, **pin).numpy()
         self._h_time = torch.empty(n, dtype=torch.int32, **pin).numpy()
         self._h_floor = torch.empty(n, dtype=torch.uint8, **pin).numpy()
+
+    def close(self) -> None:
+        """Detach the delta-transfer buffers from the handle (idempotent): the
+        handle may outlive this object (``env.batch``), and its attachments
+        are keyed by host address."""
+        att = getattr(self, "_attached", None)
+        b = getattr(self, "_batch", None)
+        while att:
+            buf = att.pop()
+            if b is not None and getattr(b, "h", None) is not None and b.h.value:
+                try:
+                    lib().gr_host_obs_detach(b.h, buf.ctypes.data_as(ctypes.c_void_p))
+                except Exception:   # interpreter shutdown
+                    pass
+
+    def __del__(self):
+        self.close()
 
     @property
     def n_actions(self) -> int:

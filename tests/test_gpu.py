@@ -827,3 +827,89 @@ def test_host_obs_delta_list_growth(torch_cuda):
     with pytest.raises(ValueError, match="not attached"):
         _lib.check(_lib.lib().gr_host_obs_detach(gb.h, ctypes.c_void_p(12345)))
     _lib.check(_lib.lib().gr_host_obs_detach(gb.h, p))
+
+
+def test_potion_ties_match_reference(torch_cuda):
+    """worldgen.py:647-649 on the device: worlds whose six potion draws tie get
+    numpy's (unstable) argsort order, as the reference produced it
+    (tests/golden/numpy_corners.npz)."""
+    from paper_2402_16801_b200 import GridrogueBatch
+    from paper_2402_16801_b200.levels import LevelBuffer
+    g = np.load(os.path.join(GOLD, "numpy_corners.npz"))
+    seeds = g["tie_seeds"]
+    gb = GridrogueBatch(4, "extended", 0, "symbolic")
+    gb.reset()
+    lv = LevelBuffer(gb, len(seeds))
+    lv.set_params(0, seeds)
+    lv.generate(0, len(seeds))
+    for k, s in enumerate(seeds):
+        assert np.array_equal(lv.world(k)["potion"], g["tie_potion"][k]), f"seed {s}"
+    assert gb.worldgen_counters()["potion_ties"] >= len(seeds)
+
+
+def test_device_argsort6_all_tie_patterns(torch_cuda):
+    """np.argsort of six float32 in numpy's tie order, on the device, over all
+    6^6 value patterns (tests/golden/numpy_corners.npz)."""
+    import itertools
+    from paper_2402_16801_b200._lib import check, lib
+    from tests._digest import digest
+    torch = torch_cuda
+    g = np.load(os.path.join(GOLD, "numpy_corners.npz"))
+    pats = torch.tensor(list(itertools.product(range(6), repeat=6)), dtype=torch.float32, device="cuda")
+    out = torch.empty(pats.shape, dtype=torch.uint8, device="cuda")
+    check(lib().gr_selftest_argsort6(pats.data_ptr(), out.data_ptr(), pats.shape[0], None))
+    o = out.cpu().numpy().astype(np.int64)
+    assert np.array_equal(o[::97], g["argsort6_sample"])
+    assert digest(o) == int(g["argsort6_digest"])
+
+
+def test_device_glibc_sincos_equals_numpy(torch_cuda):
+    """Hazard H3: the device's float64 sin / cos (the cave gradients) equal
+    numpy's -- glibc's -- bit for bit: on the golden's hard cases (angles where
+    glibc is not correctly rounded, minted here) and on EVERY float32 angle in
+    [0, 2*pi] against numpy evaluated on this box's host."""
+    from paper_2402_16801_b200._lib import check, lib
+    from tests._digest import digest
+    torch = torch_cuda
+    g = np.load(os.path.join(GOLD, "numpy_corners.npz"))
+
+    def dev(x_np):
+        x = torch.from_numpy(x_np).cuda()
+        s = torch.empty(x.shape, dtype=torch.float64, device="cuda")
+        c = torch.empty_like(s)
+        check(lib().gr_selftest_sincos64(x.data_ptr(), s.data_ptr(), c.data_ptr(), x.numel(), None))
+        return s.cpu().numpy(), c.cpu().numpy()
+
+    s, c = dev(g["trig_x"])
+    assert digest(s) == int(g["trig_digest"][0]) and digest(c) == int(g["trig_digest"][1])
+    lo, hi = int(np.float32(0).view(np.uint32)), int(np.float32(2 * np.pi).view(np.uint32))
+    bad = 0
+    for a in range(lo, hi + 1, 1 << 26):
+        x = np.arange(a, min(a + (1 << 26), hi + 1), dtype=np.uint32).view(np.float32)
+        s, c = dev(x)
+        xd = x.astype(np.float64)
+        bad += int((s.view(np.uint64) != np.sin(xd).view(np.uint64)).sum())
+        bad += int((c.view(np.uint64) != np.cos(xd).view(np.uint64)).sum())
+    assert bad == 0
+
+
+def test_template_floors_match_reference(torch_cuda):
+    """worldgen.py:549-595 on the device: with MAX_GEN_RETRIES = 0
+    (gr_set_worldgen_attempts) every floor is the template; chests / potions
+    over them equal the reference's (tests/golden/template_worlds.npz)."""
+    from paper_2402_16801_b200 import GridrogueBatch
+    from paper_2402_16801_b200._lib import check, lib
+    from paper_2402_16801_b200.levels import LevelBuffer
+    g = np.load(os.path.join(GOLD, "template_worlds.npz"))
+    for tier, seeds in (("classic", [0, 7]), ("extended", [0, 7, 123])):
+        gb = GridrogueBatch(4, tier, 0, "symbolic")
+        gb.reset()
+        check(lib().gr_set_worldgen_attempts(gb.h, 0))
+        lv = LevelBuffer(gb, len(seeds))
+        lv.set_params(0, seeds)
+        lv.generate(0, len(seeds))
+        for k, s in enumerate(seeds):
+            w, tag = lv.world(k), f"{tier}_{s}"
+            for key in ("blocks", "items", "spawn", "ladders", "chests", "potion"):
+                assert np.array_equal(w[key], g[f"{tag}_{key}"]), f"{tag} {key}"
+        assert gb.worldgen_counters()["template_floors"] == len(seeds) * (1 if tier == "classic" else 9)

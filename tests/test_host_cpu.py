@@ -140,3 +140,48 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "libgr_oracle" not in txt, f
+
+
+_GLIBC_CHECK = r"""
+#include "gr_glibc_sincos.h"
+#include <stdio.h>
+int main(void) {
+  float lo = 0.0f, hi = 6.2831853071795864769f;
+  uint32_t a, b; memcpy(&a, &lo, 4); memcpy(&b, &hi, 4);
+  long bad = 0, n = 0;
+  for (uint32_t i = a; i <= b; ++i, ++n) {
+    float f; memcpy(&f, &i, 4);
+    double x = f, s1 = sin(x), s2 = gl_sin(x), c1 = cos(x), c2 = gl_cos(x);
+    bad += memcmp(&s1, &s2, 8) != 0 || memcmp(&c1, &c2, 8) != 0;
+  }
+  uint64_t r = 88172645463325252ull;
+  for (long k = 0; k < 20000000; ++k, ++n) {
+    r ^= r << 13; r ^= r >> 7; r ^= r << 17;
+    double x = ((double)(r >> 11) * 0x1p-53 - 0.5) * ((k & 1) ? 2e-2 : 2e4);
+    double s1 = sin(x), s2 = gl_sin(x), c1 = cos(x), c2 = gl_cos(x);
+    bad += memcmp(&s1, &s2, 8) != 0 || memcmp(&c1, &c2, 8) != 0;
+  }
+  printf("%ld %ld\n", n, bad);
+  return 0;
+}
+"""
+
+
+def test_glibc_sincos_port_equals_libm_exhaustively(tmp_path):
+    """Hazard H3: the device's float64 sin / cos (csrc/gr_glibc_sincos.h, the
+    code worldgen's cave noise runs) compiled for the host with the same
+    operation sequence equals the system libm -- which numpy's float64
+    sin / cos call -- bit for bit on every float32 angle in [0, 2*pi]
+    (1,086,918,620 inputs: the cave gradients' whole domain) and on 2e7
+    random doubles of both signs."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc") or pytest.skip("gcc not available")
+    src = tmp_path / "glibc_check.c"
+    src.write_text(_GLIBC_CHECK)
+    exe = tmp_path / "glibc_check"
+    inc = os.path.join(ROOT, "paper_2402_16801_b200", "csrc")
+    subprocess.run([gcc, "-O2", "-ffp-contract=off", "-I", inc, str(src), "-o", str(exe), "-lm"], check=True)
+    n, bad = map(int, subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split())
+    assert n == 1_086_918_620 + 20_000_000
+    assert bad == 0

@@ -215,3 +215,68 @@ def test_north_star_size_matches_reference(oracle_lib):
         assert state_digest(st.export_fields(), O.FIELD_NAMES) == int(g["state"][k]), f"state step {k}"
     assert digest(*b.episode_progress()) == int(g["episode_acc"])
     assert digest(st.export_fields()["params_seed"]) == int(g["level_seeds_digest"])
+
+
+def _corners():
+    return np.load(os.path.join(GOLD, "numpy_corners.npz"))
+
+
+def test_numpy_argsort6_tie_order(oracle_lib):
+    """worldgen.py:647-649: np.argsort's (unstable, AVX-512 network) order on
+    every tie pattern of six float32 keys (tests/golden/make_corner_golden.py)."""
+    import itertools
+    L = oracle_lib.lib()
+    pats = np.array(list(itertools.product(range(6), repeat=6)), np.float32)
+    out = np.zeros(pats.shape, np.uint8)
+    for i in range(len(pats)):
+        L.go_np_argsort6(pats[i].ctypes.data, out[i].ctypes.data)
+    g = _corners()
+    assert np.array_equal(out[::97].astype(np.int64), g["argsort6_sample"])
+    assert digest(out.astype(np.int64)) == int(g["argsort6_digest"])
+    stable = np.argsort(pats, axis=1, kind="stable")
+    assert (out != stable).any(axis=1).sum() > 1000     # really not a stable sort
+
+
+def test_potion_ties_match_reference(oracle_lib):
+    """Worlds whose potion draws tie: the reference's permutation and world."""
+    O = oracle_lib
+    g = _corners()
+    for s, pot, wd in zip(g["tie_seeds"], g["tie_potion"], g["tie_world"]):
+        w = O.generate_world(int(s), "extended")
+        assert np.array_equal(w["potion"], pot), f"seed {s}"
+        parts = []
+        for f in range(len(w["blocks"])):
+            parts += [w["blocks"][f], w["items"][f],
+                      np.array(w["spawn"] if f == 0 else _floor_spawn(w, f), np.int64),
+                      w["ladder_down"][f].astype(np.int64), w["ladder_up"][f].astype(np.int64)]
+        ch = np.array([c for lanes in w["chests"] for c in lanes] or np.zeros((0, 4)), np.int64)
+        assert digest(digest(*parts), digest(ch.reshape(-1, 4))) == int(wd), f"seed {s} world"
+
+
+def test_template_floors_match_reference(oracle_lib):
+    """worldgen.py:549-595: with MAX_GEN_RETRIES = 0 every floor is the
+    _template_floor fallback; chests and potions are assigned over them
+    (tests/golden/template_worlds.npz, minted with the reference's constant
+    patched at run time)."""
+    O = oracle_lib
+    L = O.lib()
+    g = np.load(os.path.join(GOLD, "template_worlds.npz"))
+    tags = sorted({k.rsplit("_", 1)[0] for k in g.files if k.endswith("_digest")})
+    assert len(tags) == 5
+    L.go_set_max_gen_retries(0)
+    try:
+        for tag in tags:
+            tier, seed = tag.split("_")
+            w = O.generate_world(int(seed), tier)
+            assert np.array_equal(np.stack(w["blocks"]), g[f"{tag}_blocks"]), tag
+            assert np.array_equal(np.stack(w["items"]), g[f"{tag}_items"]), tag
+            assert np.array_equal(w["potion"], g[f"{tag}_potion"]), tag
+            lad = np.concatenate([np.asarray(w["ladder_down"]), np.asarray(w["ladder_up"])], axis=1)
+            assert np.array_equal(lad.astype(np.int16), g[f"{tag}_ladders"]), tag
+            ch = np.full(g[f"{tag}_chests"].shape, -1, np.int64)
+            for f, lanes in enumerate(w["chests"]):
+                for j, c in enumerate(lanes):
+                    ch[f, j] = c
+            assert np.array_equal(ch, g[f"{tag}_chests"]), tag
+    finally:
+        L.go_set_max_gen_retries(16)
