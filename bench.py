@@ -11,21 +11,33 @@ for every env, pool world generation + install for finished envs, post-reset
 observation for every env.  Synthetic: worlds are procedurally generated
 from seed 0; there is no dataset.
 
+Both arms first pre-roll ``--preroll`` (default 400, ~2x the mean episode
+length) untimed steps from batch_reset so the timed window sees the steady
+reset rate (~275 resets/step at 65,536 envs), then W warm-up steps, then K
+timed steps; both print ``resets_per_step``.
+
 `value` is device-timed (CUDA events on the stream, barrier + synchronize
 on both sides, max over ranks) with state and observations resident in HBM;
-one-shard steps replay as a CUDA graph.  The per-kernel breakdown behind
-`roofline` comes from a second timed pass over the same number of steps
-with a CUDA event pair around every launch (kernel-by-kernel, no graph;
-`roofline.profiled_ms_per_step`);
-`e2e` is the same metric through the host-buffer C-ABI call (gr_step_host):
-H2D of the step's actions and D2H of obs/reward/done/info inside the timed
-region.  Symbolic obs go into a gr_host_obs_attach'ed pinned buffer (the
-delta transfer: only the words changed since the buffer's last step cross
-PCIe and are rewritten on the host); `e2e.dense` is the plain 2.17 GB copy.  State (~2.8 GB) and the per-step obs (2.17 GB) exceed the 126 MB L2,
-so no explicit flush is needed between steps.
+steps replay as a CUDA graph (N > 1: local step + NCCL all-gather + finish
+captured in one graph).  The per-kernel breakdown behind `roofline` comes
+from a second timed pass over the same number of steps with a CUDA event
+pair around every launch (kernel-by-kernel, no graph;
+`roofline.profiled_ms_per_step`).
+
+`e2e` is the same metric through the reference-facing numpy API,
+``BatchEnv.step`` (bindings/src/gridrogue_gym/__init__.py:63-84) on host
+arrays: H2D of the actions and D2H of obs / reward / done / info inside the
+timed region.  ``e2e.value`` is the reference's contract (writable
+observation arrays, a dense 2.17 GB copy per step, PCIe-bound);
+``e2e.delta`` is BatchEnv(obs_transfer="delta") (read-only arrays owned by the
+handle; only the words changed since a buffer's last step cross PCIe).  Each
+carries the host-measured phase breakdown (gr_host_phase_times).  State
+(~2.8 GB) and the per-step obs (2.17 GB) exceed the 126 MB L2, so no explicit
+flush is needed between steps.
 
 --impl reference times the reference algorithm on the host CPU cores (the
 C oracle port in oracle/, all threads) on the same workload, time-capped.
+--gpus N without torchrun re-launches itself under torch.distributed.run.
 """
 
 from __future__ import annotations
@@ -51,11 +63,11 @@ STEP_BYTES = {("extended", "symbolic"): 34579, ("classic", "symbolic"): 6281,
               ("extended", "pixels"): 44407, ("classic", "pixels"): 12808,
               ("extended", "none"): 1507, ("classic", "none"): 901}
 # dominant kernel (the observation writer): bytes per env per launch.
-# symbolic: row written + block/item view window read + 64 B of the
-# descriptor; pixels (k_pixels, after k_pixprep): frame written + the 848 /
+# symbolic: row written + block/item view window read + the 256 B
+# descriptor (gr_desc.cuh, read whole); pixels (k_pixels, after k_pixprep): frame written + the 848 /
 # 560 B per-env scratch read
-OBS_KERNEL_BYTES = {("extended", "symbolic"): 33072 + 99 + 255 + 64,
-                    ("classic", "symbolic"): 5380 + 63 + 64,
+OBS_KERNEL_BYTES = {("extended", "symbolic"): 33072 + 99 + 255 + 256,
+                    ("classic", "symbolic"): 5380 + 63 + 256,
                     ("extended", "pixels"): 42900 + 848,
                     ("classic", "pixels"): 11907 + 560}
 
@@ -120,10 +132,9 @@ class ClockSampler:
 def cpu_baseline(tier: str, obs: str, n_envs: int, budget_s: float = 15.0, tile_px=None,
                  max_episode_length=None, steps: int | None = None, warmup: int = 0) -> dict:
     """The oracle port on the host cores (BatchEnv semantics): ``warmup``
-    untimed steps, then ``steps`` timed steps -- or, without ``steps``, as
-    many as fit in ``budget_s`` (a bounded sample); the timed loop also stops
-    at ``budget_s`` so a run always ends in minutes."""
-    import numpy as np
+    untimed steps (pre-roll + warm-up), then ``steps`` timed steps -- or,
+    without ``steps``, as many as fit in ``budget_s`` (a bounded sample); the
+    timed loop also stops at ``budget_s`` so a run always ends in minutes."""
     import oracle as O
     threads = os.cpu_count() or 1
     t0 = time.time()
@@ -140,9 +151,12 @@ def cpu_baseline(tier: str, obs: str, n_envs: int, budget_s: float = 15.0, tile_
             b.state.render_pixels(px)
 
     t = 0
+    t0 = time.time()
     for _ in range(warmup):
         one(t)
         t += 1
+    pre_s = time.time() - t0
+    ep0 = b.stats()["episodes"]
     done = 0
     t0 = time.time()
     while steps is None or done < steps:
@@ -152,25 +166,29 @@ def cpu_baseline(tier: str, obs: str, n_envs: int, budget_s: float = 15.0, tile_
         if time.time() - t0 > budget_s:
             break
     dt = time.time() - t0
+    rps = (b.stats()["episodes"] - ep0) / max(done, 1)
     cap = f"{done} of {steps} steps" if steps is not None else f"{done} steps (time-capped {budget_s:.0f} s)"
     return {"value": done * n_envs / dt, "unit": UNIT, "cores": threads, "kind": "port", "steps": done,
-            "sample": f"{tier}/{obs}, {n_envs} envs x {cap} after {warmup} warm-up steps and a {init_s:.1f} s "
-                      f"batch_reset; oracle/ C port of the reference, OpenMP over envs"}
+            "resets_per_step": round(rps, 1),
+            "sample": f"{tier}/{obs}, {n_envs} envs x {cap} after {warmup} untimed pre-roll + warm-up steps "
+                      f"({pre_s:.1f} s) and a {init_s:.1f} s batch_reset; oracle/ C port of the reference, "
+                      f"one host thread per core over envs"}
 
 
 def run_reference(args, world: int, rank: int):
     if rank != 0:
         return
-    # the requested K steps after W warm-up steps, on all host cores; the
-    # timed loop stops early at GR_REF_BUDGET_S (default 180 s)
+    # the requested K steps after the pre-roll and W warm-up steps, on all
+    # host cores; the timed loop stops early at GR_REF_BUDGET_S (default 180 s)
     budget = float(os.environ.get("GR_REF_BUDGET_S", "180"))
     cb = cpu_baseline(args.tier, args.obs, args.envs, budget, args.tile_px, args.max_episode_length,
-                      steps=args.steps, warmup=args.warmup)
+                      steps=args.steps, warmup=args.preroll + args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
-            "steps": cb["steps"], "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None,
+            "steps": cb["steps"], "warmup": args.warmup, "preroll": args.preroll,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (procedural worlds, seed 0)",
             "config": workload_config(args, world),
+            "resets_per_step": cb["resets_per_step"],
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -188,9 +206,28 @@ def workload_config(args, world):
             "tier": args.tier, "obs": args.obs, "n_envs_per_gpu": args.envs,
             "tile_px": args.tile_px if args.obs == "pixels" else None,
             "max_episode_length": args.max_episode_length,
-            "global_envs": args.envs * world, "seed": SEED,
+            "global_envs": args.envs * world, "seed": SEED, "preroll_steps": args.preroll,
             "l2_policy": "no flush: per-step state+obs (>4.9 GB/GPU) exceed the 126 MB L2",
             "parallelism": f"dp{world} (contiguous env shards, NCCL all-gather of a 16 B record/step)"}
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _relaunch(args) -> int:
+    """--gpus N outside torchrun: run N ranks, one per GPU, under
+    torch.distributed.run (127.0.0.1 rendezvous); rank 0 prints the line."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")   # the communicator's rank count goes to the log
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    log("launching", " ".join(cmd))
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -198,6 +235,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=100)
+    ap.add_argument("--preroll", type=int, default=400,
+                    help="untimed steps from batch_reset before the warm-up (steady-state reset rate)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--envs", type=int, default=65536, help="envs per GPU")
     ap.add_argument("--tier", default="extended", choices=["extended", "classic"])
@@ -207,19 +246,37 @@ def main():
                     help="BatchConfig.max_episode_length (reset stress: 16 or 32, SURVEY.md 8(d) config 4)")
     ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch / rank / config plumbing only (gloo, no GPU work): prints the config line")
     args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
 
+    in_torchrun = "WORLD_SIZE" in os.environ
+    if args.impl == "ours" and args.gpus > 1 and not in_torchrun:
+        if args.dry_run:
+            os.environ.setdefault("GR_BENCH_BACKEND", "gloo")
+        sys.exit(_relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
 
     if args.impl == "reference":
-        run_reference(args, world, rank)
+        run_reference(args, max(world, args.gpus), rank)
+        return
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    if args.dry_run:
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+            assert dist.get_world_size() == args.gpus
+            dist.barrier()
+            dist.destroy_process_group()
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": world, "config": workload_config(args, world)}), flush=True)
         return
 
-    import numpy as np
     import torch
     # GR_BENCH_BACKEND=gloo lets a dev run put several ranks on one GPU to
     # exercise the multi-rank path; the measured configuration is NCCL, one GPU per rank
@@ -231,16 +288,17 @@ def main():
     if world > 1:
         import torch.distributed as dist
         if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        assert dist.get_world_size() == args.gpus
 
     from paper_2402_16801_b200 import GridrogueBatch, ShardedBatch
-    from paper_2402_16801_b200.policies import RandomPolicy
 
     if world > 1:
         env = ShardedBatch(args.envs * world, args.tier, SEED, args.obs, max_episode_length=args.max_episode_length,
-                           tile_px=args.tile_px)
+                           tile_px=args.tile_px, graph=(backend == "nccl"))
         gb = env.batch
     else:
         env = gb = GridrogueBatch(args.envs, args.tier, SEED, args.obs, max_episode_length=args.max_episode_length,
@@ -253,11 +311,13 @@ def main():
     torch.cuda.synchronize()
     log(f"[rank {rank}] reset of {gb.n} envs: {time.time() - t0:.2f} s")
     t = 0
-    for _ in range(args.warmup):
+    t0 = time.time()
+    for _ in range(args.preroll + args.warmup):
         gb.random_actions(SEED, t)
         env.step(gb.actions)
         t += 1
     torch.cuda.synchronize()
+    log(f"[rank {rank}] pre-roll {args.preroll} + warm-up {args.warmup} steps: {time.time() - t0:.2f} s")
     gb.kernel_times()   # drop warm-up events
 
     def timed_steps(k, t):
@@ -277,8 +337,7 @@ def main():
             dist.barrier()
         return ev0.elapsed_time(ev1), t
 
-    # pass 1, the measurement: one-shard steps replay as a CUDA graph, no
-    # per-kernel events
+    # pass 1, the measurement: steps replay as a CUDA graph, no per-kernel events
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -290,46 +349,53 @@ def main():
     clk = clocks.stop()
     # pass 2, the per-kernel breakdown behind the roofline: the same steps
     # again with a CUDA event pair around every launch (kernel-by-kernel
-    # launches, no graph), timed the same way
-    gb.set_profiling(True)
-    ms_prof, t = timed_steps(args.steps, t)
-    gb.set_profiling(False)
-    ktimes = gb.kernel_times()
+    # launches, no graph), timed the same way (one shard only: the sharded
+    # step is graph-captured with its collective)
+    ktimes, ms_prof = None, None
+    if world == 1:
+        gb.set_profiling(True)
+        ms_prof, t = timed_steps(args.steps, t)
+        gb.set_profiling(False)
+        ktimes = gb.kernel_times()
     if dist:
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
+        rr = torch.tensor([resets_per_step], dtype=torch.float64, device="cuda")
+        dist.all_reduce(rr)
+        resets_per_step = float(rr.item())    # whole job
     value = args.envs * world * args.steps / (ms / 1000.0)
 
-    # roofline of the dominant kernel (device-ms share of the step)
-    peak, peak_src = peak_hbm()
-    dom = max(ktimes, key=lambda k: ktimes[k][0])
-    dom_ms, dom_n = ktimes[dom]
     key = (args.tier, args.obs)
-    if dom == "obs" and key in OBS_KERNEL_BYTES:
-        # the main writer renders every env not reset this step; the reset
-        # envs are rendered by a small launch after their install (obs_reset)
-        bytes_per_launch = int(OBS_KERNEL_BYTES[key] * (gb.n - resets_per_step))
-    else:
-        bytes_per_launch = STEP_BYTES[key] * gb.n
-    per_launch_ms = dom_ms / max(dom_n, 1)
-    achieved = bytes_per_launch / (per_launch_ms / 1000.0) / 1e9 if per_launch_ms > 0 else 0.0
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            tr = json.load(fh)
-        traffic = tr.get(f"{args.tier}_{args.obs}_{dom}")
-    except Exception:
-        pass
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
-                "bytes_per_launch": bytes_per_launch, "ms_per_launch": round(per_launch_ms, 5),
-                "share_of_step": round(dom_ms / ms_prof, 3), "peak_source": peak_src,
-                "profiled_ms_per_step": round(ms_prof / args.steps, 5),
-                "resets_per_step": round(resets_per_step, 1),
-                "step_frac": round(value / world * STEP_BYTES[key] / 1e9 / peak, 4)}
+    peak, peak_src = peak_hbm()
+    roofline = None
+    if ktimes:
+        # roofline of the dominant kernel (device-ms share of the step)
+        dom = max(ktimes, key=lambda k: ktimes[k][0])
+        dom_ms, dom_n = ktimes[dom]
+        if dom == "obs" and key in OBS_KERNEL_BYTES:
+            # the main writer renders every env not reset this step; the reset
+            # envs are rendered by a small launch after their install (obs_reset)
+            bytes_per_launch = int(OBS_KERNEL_BYTES[key] * (gb.n - resets_per_step))
+        else:
+            bytes_per_launch = STEP_BYTES[key] * gb.n
+        per_launch_ms = dom_ms / max(dom_n, 1)
+        achieved = bytes_per_launch / (per_launch_ms / 1000.0) / 1e9 if per_launch_ms > 0 else 0.0
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                traffic = json.load(fh).get(f"{args.tier}_{args.obs}_{dom}")
+        except Exception:
+            pass
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
+                    "bytes_per_launch": bytes_per_launch, "ms_per_launch": round(per_launch_ms, 5),
+                    "share_of_step": round(dom_ms / ms_prof, 3), "peak_source": peak_src,
+                    "profiled_ms_per_step": round(ms_prof / args.steps, 5),
+                    "resets_per_step": round(resets_per_step, 1),
+                    "step_frac": round(value / world * STEP_BYTES[key] / 1e9 / peak, 4)}
 
-    # end to end through the host-buffer C ABI (pinned host memory)
+    # end to end through the numpy API (pinned host memory)
     e2e = None
     if args.e2e_steps > 0:
         e2e = run_e2e(args, gb, env, world, rank, dist, t)
@@ -338,103 +404,110 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cb = cpu_baseline(args.tier, args.obs, args.envs, float(os.environ.get("GR_CPU_BUDGET_S", "15")),
-                              args.tile_px, args.max_episode_length)
+                              args.tile_px, args.max_episode_length, warmup=args.preroll)
         except Exception as ex:   # the oracle is only the reported baseline
             cb = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
+                "steps": args.steps, "warmup": args.warmup, "preroll": args.preroll,
+                "ms_per_step": round(ms / args.steps, 5),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (procedural worlds, seed 0; random policy)",
-                "config": workload_config(args, world), "roofline": roofline,
-                "cpu_baseline": cb, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
-                "kernel_ms": {k: round(v[0], 3) for k, v in ktimes.items()},
+                "config": workload_config(args, world), "resets_per_step": round(resets_per_step, 1),
+                "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
+                "kernel_ms": {k: round(v[0], 3) for k, v in ktimes.items()} if ktimes else None,
                 "worldgen": gb.worldgen_counters()}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
 
 
+def _phases(gb) -> dict:
+    import ctypes
+    import numpy as np
+    from paper_2402_16801_b200 import _lib
+    out = np.zeros(4, np.float64)
+    calls, words = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.lib().gr_host_phase_times(gb.h, out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(calls),
+                                              ctypes.byref(words)))
+    c = max(calls.value, 1)
+    return {"ms_per_step": {"enqueue": round(out[0] / c, 3), "device_wait": round(out[1] / c, 3),
+                            "host_scatter": round(out[2] / c, 3), "final_sync": round(out[3] / c, 3)},
+            "changed_words_per_step": int(words.value / c)}
+
+
 def run_e2e(args, gb, env, world, rank, dist, t):
     import numpy as np
     import torch
-    from paper_2402_16801_b200 import _lib
+    from paper_2402_16801_b200 import BatchEnv
     from paper_2402_16801_b200.policies import RandomPolicy
-    import ctypes
     n = gb.n
     pol = RandomPolicy(SEED, gb.n_actions)
-    acts = [pol.actions_at(t + k, n, env0=gb.cfg.env_offset) for k in range(args.e2e_steps)]
-    h_act = torch.empty(n, dtype=torch.int64, pin_memory=True)
-    h_obs = torch.empty(tuple(gb.obs.shape), dtype=gb.obs.dtype, pin_memory=True)
-    h_rew = torch.empty(n, dtype=torch.float32, pin_memory=True)
-    h_done = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-    h_newly = torch.empty((n, gb.n_achievements), dtype=torch.uint8, pin_memory=True)
-    h_time = torch.empty(n, dtype=torch.int32, pin_memory=True)
-    h_floor = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-    P = lambda x: ctypes.c_void_p(x.data_ptr())
-    obs_p = P(h_obs) if args.obs != "none" else None
-    d2h = h_obs.numel() * h_obs.element_size() + n * (4 + 1 + gb.n_achievements + 4 + 1)
+    steps = args.e2e_steps
+    acts = [pol.actions_at(t + k, n, env0=gb.cfg.env_offset) for k in range(steps + 2)]
+    small_d2h = n * (4 + 1 + gb.n_achievements + 4 + 1)   # reward, done, newly, time, floor
+    obs_bytes = int(np.prod(gb.obs.shape[1:])) * gb.obs.element_size() * n
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     if world == 1:
-        def host_steps():
-            # one warm-up call allocates the library's host-path scratch
-            h_act.numpy()[:] = acts[0]
-            _lib.check(_lib.lib().gr_step_host(gb.h, P(h_act), obs_p, P(h_rew), P(h_done), P(h_newly),
-                                               P(h_time), P(h_floor)))
+        def run(be, k0):
+            # BatchEnv.step is the timed call; the caller drops each step's
+            # arrays before the next step, like a training loop would
+            be.step(acts[k0])
+            _phases(gb)
             t0 = time.perf_counter()
-            for k in range(1, args.e2e_steps):
-                h_act.numpy()[:] = acts[k]
-                _lib.check(_lib.lib().gr_step_host(gb.h, P(h_act), obs_p, P(h_rew), P(h_done), P(h_newly),
-                                                   P(h_time), P(h_floor)))
-            return time.perf_counter() - t0
+            for k in range(steps):
+                obs, rew, done, info = be.step(acts[k0 + 1 + k])
+                del obs, rew, done, info
+            dt = time.perf_counter() - t0
+            return n * steps / dt, _phases(gb)
 
-        dt = host_steps()
-        steps = args.e2e_steps - 1
-        if args.obs == "symbolic" and n * h_obs.shape[1] < 2 ** 32:
-            # the same calls into an attached buffer (BatchEnv(obs_transfer="delta")):
-            # only the obs words that changed since the buffer's last step cross PCIe
-            dense = {"value": round(n * steps / dt, 1), "unit": UNIT, "h2d_bytes_per_step": n * 8,
-                     "d2h_bytes_per_step": int(d2h), "steps": steps, "path": "gr_step_host, dense obs copy"}
-            _lib.check(_lib.lib().gr_host_obs_attach(gb.h, obs_p))
-            dt = host_steps()
-            prev = h_obs.numpy().view(np.uint32).copy()
-            h_act.numpy()[:] = acts[0]
-            _lib.check(_lib.lib().gr_step_host(gb.h, P(h_act), obs_p, P(h_rew), P(h_done), P(h_newly),
-                                               P(h_time), P(h_floor)))
-            changed = int(np.count_nonzero(h_obs.numpy().view(np.uint32) != prev))   # one step's list length
-            _lib.check(_lib.lib().gr_host_obs_detach(gb.h, obs_p))
-            d2h_delta = 2 * 8 + changed * 8 + n * (4 + 1 + gb.n_achievements + 4 + 1)
-            return {"value": round(n * steps / dt, 1), "unit": UNIT, "h2d_bytes_per_step": n * 8,
-                    "d2h_bytes_per_step": int(d2h_delta), "steps": steps,
-                    "path": "gr_step_host into a gr_host_obs_attach'ed pinned buffer (BatchEnv obs_transfer='delta'): "
-                            "(index, value) of the obs words changed since the buffer's last step, host scatter",
-                    "dense": dense}
-    else:
-        d_act = torch.empty(n, dtype=torch.int64, device=gb.device)
-        t0 = time.perf_counter()
-        for k in range(args.e2e_steps):
-            h_act.numpy()[:] = acts[k]
-            d_act.copy_(h_act, non_blocking=True)
-            obs, rew, done, newly, tm, fl = env.step(d_act)
-            h_obs.copy_(obs, non_blocking=True)
-            h_rew.copy_(rew, non_blocking=True)
-            h_done.copy_(done, non_blocking=True)
-            h_newly.copy_(newly, non_blocking=True)
-            h_time.copy_(tm, non_blocking=True)
-            h_floor.copy_(fl, non_blocking=True)
-            torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        steps = args.e2e_steps
-        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dt = float(tt.item())
+        dense_env = BatchEnv.from_batch(gb, "dense")
+        v_dense, ph_dense = run(dense_env, 0)
+        dense_env.close()
+        out = {"value": round(v_dense, 1), "unit": UNIT, "h2d_bytes_per_step": n * 8,
+               "d2h_bytes_per_step": int(obs_bytes + small_d2h), "steps": steps,
+               "path": "BatchEnv.step (numpy in/out, writable obs arrays as the reference returns): "
+                       "H2D actions, device step, D2H of the whole observation + reward/done/info",
+               "phases": ph_dense}
+        if args.obs == "symbolic" and n * gb.obs.shape[1] < 2 ** 32:
+            delta_env = BatchEnv.from_batch(gb, "delta")
+            delta_env.step(acts[0])      # first delivery into each buffer is a full one
+            delta_env.step(acts[1])
+            delta_env.step(acts[0])
+            v_delta, ph_delta = run(delta_env, 0)
+            delta_env.close()
+            out["delta"] = {"value": round(v_delta, 1), "unit": UNIT, "h2d_bytes_per_step": n * 8,
+                            "d2h_bytes_per_step": int(ph_delta["changed_words_per_step"] * 8 + small_d2h),
+                            "steps": steps,
+                            "path": "BatchEnv(obs_transfer='delta').step: read-only obs arrays owned by the handle; "
+                                    "(index, value) of the words changed since a buffer's last step, listed on the device "
+                                    "in 8 row chunks, each copied back while the next is listed and scattered by host threads",
+                            "phases": ph_delta}
+        return out
+    d_act = torch.empty(n, dtype=torch.int64, device=gb.device)
+    h_act = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    h_obs = torch.empty(tuple(gb.obs.shape), dtype=gb.obs.dtype, pin_memory=True)
+    h_small = [torch.empty(tuple(x.shape), dtype=x.dtype, pin_memory=True)
+               for x in (gb.reward, gb.done, gb.newly, gb.time, gb.floor)]
+    t0 = time.perf_counter()
+    for k in range(steps):
+        h_act.numpy()[:] = acts[k]
+        d_act.copy_(h_act, non_blocking=True)
+        obs, *rest = env.step(d_act)
+        h_obs.copy_(obs, non_blocking=True)
+        for h, d in zip(h_small, rest):
+            h.copy_(d, non_blocking=True)
+        torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    dt = float(tt.item())
     return {"value": round(n * world * steps / dt, 1), "unit": UNIT, "h2d_bytes_per_step": n * 8,
-            "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "path": "gr_step_host (C ABI, pinned host buffers)" if world == 1 else
-                    "ShardedBatch.step + pinned H2D/D2H copies"}
+            "d2h_bytes_per_step": int(obs_bytes + small_d2h), "steps": steps,
+            "path": "ShardedBatch.step + pinned H2D/D2H copies (per rank)"}
 
 
 if __name__ == "__main__":

@@ -146,6 +146,12 @@ int gr_step_local(gr_env *env, const int64_t *actions_dev, float *reward_dev, ui
                   int32_t *exchange_dev /* int32[4] */, void *stream);
 int gr_step_finish(gr_env *env, const int32_t *exchange_all_dev /* int32[world*4] */,
                    int32_t rank, int32_t world, void *obs_dev, void *stream);
+/* Both halves and the caller's collective between them are capturable
+ * (validation off): a caller that captured local + all-gather + finish in one
+ * CUDA graph and replayed it `steps` times reports it here, so the host-side
+ * step index and launch counter stay exact (launches_per_step = the kernels
+ * the captured step contains). */
+int gr_account_replay(gr_env *env, int64_t steps, int64_t launches_per_step);
 
 /* ---- end-to-end (host buffers) ------------------------------------------ *
  * Same contract as gr_step with host arrays: H2D of actions, the step,
@@ -223,6 +229,17 @@ int gr_levels_install(gr_levels *lv, int64_t count, const int64_t *env_idx, cons
  * loot, qty; -1 rows pad), potion permutation [6] */
 int gr_levels_export_world(gr_levels *lv, int64_t level, uint8_t *blocks, uint8_t *items, int16_t *spawn,
                            int16_t *ladders, int64_t *chests, uint8_t *potion);
+/* the level's LevelParams seed and which floors are the _template_floor
+ * fallback (bit f; their FloorMap.spawn is the map centre, worldgen.py:549-575,
+ * while every generated lower floor spawns on its up ladder) */
+int gr_levels_world_info(gr_levels *lv, int64_t level, uint64_t *seed, uint32_t *template_floors);
+/* write a World (worldgen.World, e.g. read with serialize.world_from_bytes,
+ * serialize.py:97-118) into level slot `level`, in the layout
+ * gr_levels_export_world produces; seed = its LevelParams.seed.  The slot can
+ * then be installed like a generated one. */
+int gr_levels_import_world(gr_levels *lv, int64_t level, uint64_t seed, const uint8_t *blocks,
+                           const uint8_t *items, const int16_t *spawn, const int16_t *ladders,
+                           const int64_t *chests, const uint8_t *potion, uint32_t template_floors);
 
 /* ---- metrics ------------------------------------------------------------- */
 int gr_stats_get(gr_env *env, gr_stats *out);                 /* EpisodeStats */

@@ -125,6 +125,7 @@ def lib():
         L.go_np_cosf.argtypes = [c.c_float]
         L.go_np_argsort6.argtypes = [P, P]
         L.go_set_max_gen_retries.argtypes = [c.c_int]
+        L.go_level_angles.argtypes = [c.c_uint64, P, P]
         L.go_generate_world.argtypes = [c.c_uint64, c.c_int, P]
         L.go_state_new.restype = P
         L.go_state_new.argtypes = [c.c_int, c.c_int64, c.c_int64]

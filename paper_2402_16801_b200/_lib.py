@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
         "gr_host_obs_attach": (I32, [P, P]),
         "gr_host_obs_detach": (I32, [P, P]),
         "gr_host_phase_times": (I32, [P, P, P, P]),
+        "gr_account_replay": (I32, [P, I64, I64]),
         "gr_export_field": (I32, [P, I32, P]),
         "gr_import_field": (I32, [P, I32, P]),
         "gr_observe": (I32, [P, P, P]),
@@ -116,6 +117,8 @@ def lib() -> ctypes.CDLL:
         "gr_levels_mutate": (I32, [P, I32, I64, P, P, P, ctypes.c_double]),
         "gr_levels_install": (I32, [P, I64, P, P, P]),
         "gr_levels_export_world": (I32, [P, I64, P, P, P, P, P, P]),
+        "gr_levels_world_info": (I32, [P, I64, P, P]),
+        "gr_levels_import_world": (I32, [P, I64, U64, P, P, P, P, P, P, ctypes.c_uint32]),
         "gr_import_episode": (I32, [P, P, P]),
         "gr_get_step_index": (I32, [P, ctypes.POINTER(I64)]),
         "gr_set_step_index": (I32, [P, I64]),

@@ -263,14 +263,16 @@ struct gr_env {
   cudaStream_t h_stream = nullptr;
   // delta observation transfer into attached host buffers
   std::vector<HostObs> host_obs;
-  // the changed-word list lives in mapped pinned host memory: the delta
-  // kernel writes it across PCIe while it runs (no separate copy)
+  // the changed-word list: device copy written by k_obs_delta, pinned host
+  // stage it is copied into chunk by chunk on dl_copy
   uint2* dl_host = nullptr;
   uint2* dl_dev = nullptr;
   int64_t dl_cap = 0;                          // entries, split evenly over DL_CHUNKS
-  unsigned long long* dl_cnt_host = nullptr;   // [DL_CHUNKS] mapped counters
+  unsigned long long* dl_cnt_host = nullptr;   // [DL_CHUNKS] pinned copies of the chunk counters
   unsigned long long* dl_cnt_dev = nullptr;
-  cudaEvent_t dl_ev[DL_CHUNKS] = {};
+  cudaStream_t dl_copy = nullptr;
+  cudaEvent_t dl_ev[DL_CHUNKS] = {};           // chunk listed + its count on the host
+  cudaEvent_t dl_evd[DL_CHUNKS] = {};          // chunk's list on the host
   std::unique_ptr<HostPool> hpool;            // host threads of the delta scatter
   double host_ms[4] = {0, 0, 0, 0};            // enqueue, wait, scatter, tail (gr_host_phase_times)
   int64_t host_calls = 0;
@@ -391,8 +393,13 @@ void gr_destroy(gr_env* e) {
   for (auto& h : e->host_obs)
     if (h.shadow) cudaFree(h.shadow);
   if (e->dl_host) cudaFreeHost(e->dl_host);
+  if (e->dl_dev) cudaFree(e->dl_dev);
   if (e->dl_cnt_host) cudaFreeHost(e->dl_cnt_host);
+  if (e->dl_cnt_dev) cudaFree(e->dl_cnt_dev);
+  if (e->dl_copy) cudaStreamDestroy(e->dl_copy);
   for (auto& ev : e->dl_ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : e->dl_evd)
     if (ev) cudaEventDestroy(ev);
   e->hpool.reset();
   if (e->side) cudaStreamDestroy(e->side);
@@ -797,6 +804,13 @@ int gr_step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank, int
   return step_finish(e, exchange_all_dev, rank, world, obs_dev, stream, false);
 }
 
+int gr_account_replay(gr_env* e, int64_t steps, int64_t launches_per_step) {
+  if (!e || steps < 0 || launches_per_step < 0) return fail(GR_E_INVALID, "bad replay accounting");
+  e->step_index += steps;
+  e->launches += steps * launches_per_step;
+  return GR_OK;
+}
+
 // One-shard steps replay a CUDA graph of the whole launch sequence (step,
 // scan tail, compaction, worldgen, install, observation writers on two
 // streams), captured once per set of output buffers on the handle's own
@@ -886,8 +900,7 @@ static int ensure_host_scratch(gr_env* e) {
 // shadow 32 words at a time and keeps the ballot masks in shared memory
 // (259 words per extended row), reserves the row's slice of the list with
 // one atomic, then walks the masks: only the changed words are re-read (from
-// L2: the row was just streamed) and written to the list -- mapped pinned
-// host memory, so the list crosses PCIe while the kernel runs -- and to the
+// L2: the row was just streamed) and written to the list and to the
 // shadow.  Row order in the list varies run to run; positions are distinct,
 // so the host array after the scatter does not.
 constexpr int DL_WARPS = 8;
@@ -993,26 +1006,31 @@ static double ms_since(hclock::time_point t0) {
 static int ensure_delta_list(gr_env* e, int64_t cap) {
   if (e->dl_host && e->dl_cap >= cap) return GR_OK;
   if (e->dl_host) cudaFreeHost(e->dl_host);
+  if (e->dl_dev) cudaFree(e->dl_dev);
   e->dl_host = nullptr;
+  e->dl_dev = nullptr;
   e->dl_cap = 0;
-  CK(cudaHostAlloc((void**)&e->dl_host, (size_t)cap * sizeof(uint2), cudaHostAllocMapped));
-  CK(cudaHostGetDevicePointer((void**)&e->dl_dev, e->dl_host, 0));
+  CK(cudaMalloc((void**)&e->dl_dev, (size_t)cap * sizeof(uint2)));
+  CK(cudaHostAlloc((void**)&e->dl_host, (size_t)cap * sizeof(uint2), cudaHostAllocDefault));
   e->dl_cap = cap;
   return GR_OK;
 }
 
 // after the observation is in e->h_obs_dev (ordered on st): list the words
 // that differ from the buffer's shadow and scatter them into the host
-// buffer, chunk by chunk (rows split in DL_CHUNKS ranges, one kernel + event
-// each), so the host scatters chunk c while the device lists chunk c+1.
-// If a chunk outgrows its share of the list, whole-buffer passes with a
-// larger list follow (each pass applies what it listed).  Synchronous.
+// buffer, pipelined over DL_CHUNKS row ranges: kernel c (+ its count) on st,
+// the copy of chunk c's list on dl_copy once its count is known, and the
+// host scatter of chunk c-1 meanwhile.  If a chunk outgrows its share of the
+// list, whole-buffer passes with a larger list follow (each pass applies
+// what it listed).  Synchronous.
 static int host_obs_deliver(gr_env* e, HostObs& h, cudaStream_t st, hclock::time_point t_call) {
   const int W = (int)obs_elems_of(e);
   if (!e->dl_cnt_host) {
-    CK(cudaHostAlloc((void**)&e->dl_cnt_host, DL_CHUNKS * sizeof(unsigned long long), cudaHostAllocMapped));
-    CK(cudaHostGetDevicePointer((void**)&e->dl_cnt_dev, e->dl_cnt_host, 0));
-    for (auto& ev : e->dl_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync));
+    CK(cudaHostAlloc((void**)&e->dl_cnt_host, DL_CHUNKS * sizeof(unsigned long long), cudaHostAllocDefault));
+    CK(cudaMalloc((void**)&e->dl_cnt_dev, DL_CHUNKS * sizeof(unsigned long long)));
+    CK(cudaStreamCreateWithFlags(&e->dl_copy, cudaStreamNonBlocking));
+    for (auto& ev : e->dl_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    for (auto& ev : e->dl_evd) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     unsigned hc = std::thread::hardware_concurrency();
     e->hpool.reset(new HostPool((int)std::min<unsigned>(hc ? hc : 1, 32)));
   }
@@ -1022,7 +1040,7 @@ static int host_obs_deliver(gr_env* e, HostObs& h, cudaStream_t st, hclock::time
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  volatile unsigned long long* cnt = e->dl_cnt_host;
+  const unsigned long long* cnt = e->dl_cnt_host;
   auto scatter = [&](const uint2* list, int64_t k) {
     uint32_t* p = h.ptr;
     e->hpool->run(k, [&](int64_t lo, int64_t hi) {
@@ -1031,10 +1049,16 @@ static int host_obs_deliver(gr_env* e, HostObs& h, cudaStream_t st, hclock::time
     e->host_words += k;
   };
   double t_wait = 0, t_scatter = 0;
+  auto wait = [&](cudaEvent_t ev) -> int {
+    const auto t0 = hclock::now();
+    CK(cudaEventSynchronize(ev));
+    t_wait += ms_since(t0);
+    return GR_OK;
+  };
   // pipelined pass
   const int C = (int)std::min<int64_t>(DL_CHUNKS, std::max<int64_t>(1, e->n / 256));
   const int64_t capc = e->dl_cap / C;
-  for (int c = 0; c < C; ++c) cnt[c] = 0;
+  CK(cudaMemsetAsync(e->dl_cnt_dev, 0, C * sizeof(unsigned long long), st));
   for (int c = 0; c < C; ++c) {
     const int64_t r0 = e->n * c / C, r1 = e->n * (c + 1) / C;
     const int grid = (int)std::min<int64_t>((r1 - r0 + DL_WARPS - 1) / DL_WARPS, (int64_t)sms * 8);
@@ -1042,38 +1066,52 @@ static int host_obs_deliver(gr_env* e, HostObs& h, cudaStream_t st, hclock::time
                                                  e->dl_dev + c * capc, capc, e->dl_cnt_dev + c);
     e->launches += 1;
     CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(e->dl_cnt_host + c, e->dl_cnt_dev + c, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       st));
     CK(cudaEventRecord(e->dl_ev[c], st));
   }
   e->host_ms[0] += ms_since(t_call);
   bool overflow = false;
   int64_t total = 0;
-  for (int c = 0; c < C; ++c) {
-    auto t0 = hclock::now();
-    CK(cudaEventSynchronize(e->dl_ev[c]));
-    t_wait += ms_since(t0);
-    const int64_t count = (int64_t)cnt[c];
-    total += count;
-    t0 = hclock::now();
-    scatter(e->dl_host + c * capc, std::min(count, capc));
-    t_scatter += ms_since(t0);
-    overflow |= count > capc;
+  int64_t kc[DL_CHUNKS];
+  for (int c = 0; c <= C; ++c) {
+    if (c < C) {
+      if ((rc = wait(e->dl_ev[c]))) return rc;
+      total += (int64_t)cnt[c];
+      overflow |= (int64_t)cnt[c] > capc;
+      kc[c] = std::min((int64_t)cnt[c], capc);
+      CK(cudaStreamWaitEvent(e->dl_copy, e->dl_ev[c], 0));
+      if (kc[c])
+        CK(cudaMemcpyAsync(e->dl_host + c * capc, e->dl_dev + c * capc, (size_t)kc[c] * sizeof(uint2),
+                           cudaMemcpyDeviceToHost, e->dl_copy));
+      CK(cudaEventRecord(e->dl_evd[c], e->dl_copy));
+    }
+    if (c > 0) {
+      if ((rc = wait(e->dl_evd[c - 1]))) return rc;
+      const auto t0 = hclock::now();
+      scatter(e->dl_host + (c - 1) * capc, kc[c - 1]);
+      t_scatter += ms_since(t0);
+    }
   }
   // overflow: whole-buffer passes until every changed word is listed
   for (int pass = 0; overflow && pass < 64; ++pass) {
     rc = ensure_delta_list(e, std::min<int64_t>(total + total / 4 + 1024, host_obs_words(e)));
     if (rc) return rc;
-    cnt[0] = 0;
+    CK(cudaMemsetAsync(e->dl_cnt_dev, 0, sizeof(unsigned long long), st));
     k_obs_delta<<<sms * 8, DL_WARPS * 32, 0, st>>>((const uint32_t*)e->h_obs_dev, h.shadow, 0, e->n, W, e->dl_dev,
                                                     e->dl_cap, e->dl_cnt_dev);
     e->launches += 1;
     CK(cudaGetLastError());
-    auto t0 = hclock::now();
+    CK(cudaMemcpyAsync(e->dl_cnt_host, e->dl_cnt_dev, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(e->dl_ev[0], st));
-    CK(cudaEventSynchronize(e->dl_ev[0]));
-    t_wait += ms_since(t0);
+    if ((rc = wait(e->dl_ev[0]))) return rc;
     total = (int64_t)cnt[0];
-    t0 = hclock::now();
-    scatter(e->dl_host, std::min(total, e->dl_cap));
+    const int64_t k = std::min(total, e->dl_cap);
+    if (k) CK(cudaMemcpyAsync(e->dl_host, e->dl_dev, (size_t)k * sizeof(uint2), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(e->dl_ev[0], st));
+    if ((rc = wait(e->dl_ev[0]))) return rc;
+    const auto t0 = hclock::now();
+    scatter(e->dl_host, k);
     t_scatter += ms_since(t0);
     overflow = total > e->dl_cap;
   }
@@ -1491,6 +1529,61 @@ int gr_levels_export_world(gr_levels* lv, int64_t level, uint8_t* blocks, uint8_
           chests[(f * 6 + jj) * 4 + q] = (e->ext && jj < m.nch[f]) ? (int64_t)m.chest[f][jj][q] : -1;
   if (potion)
     for (int k = 0; k < 6; ++k) potion[k] = m.potion[k];
+  return GR_OK;
+}
+
+int gr_levels_world_info(gr_levels* lv, int64_t level, uint64_t* seed, uint32_t* template_floors) {
+  int rc = lv_range(lv, level, 1);
+  if (rc) return rc;
+  CK(cudaSetDevice(lv->e->cfg.device));
+  CK(cudaDeviceSynchronize());
+  WMeta m;
+  CK(cudaMemcpy(&m, lv->w.meta + level, sizeof(m), cudaMemcpyDeviceToHost));
+  if (seed) *seed = m.seed;
+  if (template_floors) *template_floors = (m.flags >> 8) & 0x1ffu;
+  return GR_OK;
+}
+
+int gr_levels_import_world(gr_levels* lv, int64_t level, uint64_t seed, const uint8_t* blocks, const uint8_t* items,
+                           const int16_t* spawn, const int16_t* ladders, const int64_t* chests, const uint8_t* potion,
+                           uint32_t template_floors) {
+  int rc = lv_range(lv, level, 1);
+  if (rc) return rc;
+  if (!blocks || !items || !spawn || !ladders || !chests || !potion) return fail(GR_E_INVALID, "null argument");
+  gr_env* e = lv->e;
+  const int F = e->d.F, H = e->d.H, W = e->d.W;
+  WMeta m;
+  memset(&m, 0, sizeof(m));
+  m.spawn[0] = spawn[0];
+  m.spawn[1] = spawn[1];
+  for (int f = 0; f < F; ++f) {
+    m.ld[f][0] = ladders[4 * f];
+    m.ld[f][1] = ladders[4 * f + 1];
+    m.lu[f][0] = ladders[4 * f + 2];
+    m.lu[f][1] = ladders[4 * f + 3];
+    int k = 0;
+    for (int j = 0; j < 6; ++j) {
+      const int64_t* c = chests + (f * 6 + j) * 4;
+      if (c[0] < 0) continue;
+      if (!e->ext) return fail(GR_E_INVALID, "the classic tier has no chests");
+      if (c[0] >= H || c[1] < 0 || c[1] >= W) return fail(GR_E_INVALID, "chest outside the map");
+      for (int q = 0; q < 4; ++q) m.chest[f][k][q] = (int16_t)c[q];
+      ++k;
+    }
+    m.nch[f] = (uint8_t)k;
+  }
+  for (int q = 0; q < 6; ++q) {
+    if (potion[q] > 5) return fail(GR_E_INVALID, "potion permutation entry %d out of range", (int)potion[q]);
+    m.potion[q] = potion[q];
+  }
+  m.seed = seed;
+  m.flags = ((template_floors & 0x1ffu) << 8) | (template_floors ? WG_FLAG_TEMPLATE : 0u);
+  CK(cudaSetDevice(e->cfg.device));
+  CK(cudaDeviceSynchronize());
+  const size_t mb = (size_t)F * H * W;
+  CK(cudaMemcpy(lv->w.blocks + level * mb, blocks, mb, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(lv->w.items + level * mb, items, mb, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(lv->w.meta + level, &m, sizeof(m), cudaMemcpyHostToDevice));
   return GR_OK;
 }
 

@@ -90,7 +90,8 @@ struct WMeta {
   uint32_t flags;             // WG_FLAG_*
   uint32_t pad2;
 };
-enum : uint32_t { WG_FLAG_RETRY = 1, WG_FLAG_TEMPLATE = 2, WG_FLAG_POTION_TIE = 4, WG_FLAG_FRAGILE = 8 };
+enum : uint32_t { WG_FLAG_RETRY = 1, WG_FLAG_TEMPLATE = 2, WG_FLAG_POTION_TIE = 4,
+                  WG_FLAG_TEMPLATE_F0 = 1u << 8 };   // + f: floor f is the _template_floor fallback
 
 struct WBuf {
   uint8_t* blocks;            // [cap][F][H][W]

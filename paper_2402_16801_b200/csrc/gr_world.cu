@@ -888,7 +888,7 @@ __global__ void __launch_bounds__(WT<EXT>::THREADS, WT<EXT>::MINB) k_worldgen(Wo
     if (attempt > 1) flags |= WG_FLAG_RETRY;
     if (!ok) {
       gen_template<EXT>(sm, f, &fo);
-      flags |= WG_FLAG_TEMPLATE;
+      flags |= WG_FLAG_TEMPLATE | (WG_FLAG_TEMPLATE_F0 << f);
     }
     if (EXT && f >= 1 && f <= 7) assign_chests<EXT>(sm, seed, f, meta);
     // write the floor out (16-byte vectors)

@@ -289,7 +289,8 @@ class BatchEnv:
 
     def __init__(self, n_envs: int, tier: str = "extended", seed: int = 0,
                  obs_mode: str = "symbolic", max_episode_length: int | None = None,
-                 tile_px: int | None = None, device: int = 0, obs_transfer: str = "dense"):
+                 tile_px: int | None = None, device: int = 0, obs_transfer: str = "dense",
+                 _batch: GridrogueBatch | None = None):
         if obs_mode not in self.metadata["obs_modes"]:
             raise ValueError(f"unknown obs_mode {obs_mode!r}")
         if obs_transfer not in ("dense", "delta"):
@@ -301,10 +302,10 @@ class BatchEnv:
         self.n_envs = int(n_envs)
         self.obs_mode = obs_mode
         self.seed = int(seed)
-        self._batch = GridrogueBatch(self.n_envs, self.tier_name, self.seed, obs_mode,
-                                     max_episode_length, tile_px, device)
+        self._batch = _batch if _batch is not None else GridrogueBatch(
+            self.n_envs, self.tier_name, self.seed, obs_mode, max_episode_length, tile_px, device)
         self._stepping = threading.Lock()
-        self._ready = False
+        self._ready = _batch is not None
         import torch
         n = self.n_envs
         t = TIERS[self.tier_name]
@@ -331,7 +332,7 @@ class BatchEnv:
         if obs_transfer == "delta":
             for b in [self._h_obs, *self._obs_pool]:
                 check(lib().gr_host_obs_attach(self._batch.h, b.ctypes.data_as(ctypes.c_void_p)))
-                self._attached.append(b)
+                self._attached.append(b.ctypes.data)   # the address only: refcounts pick free buffers
                 b.flags.writeable = False   # views handed out cannot be made writable again
         self._h_act = torch.empty(n, dtype=torch.int64, **pin).numpy()
         self._h_rew = torch.empty(n, dtype=torch.float32, **pin).numpy()
@@ -340,6 +341,13 @@ class BatchEnv:
         self._h_time = torch.empty(n, dtype=torch.int32, **pin).numpy()
         self._h_floor = torch.empty(n, dtype=torch.uint8, **pin).numpy()
 
+    @classmethod
+    def from_batch(cls, batch: GridrogueBatch, obs_transfer: str = "dense") -> "BatchEnv":
+        """The numpy contract over an existing device batch that has been
+        reset (and possibly stepped) -- e.g. a benchmark's pre-rolled batch."""
+        return cls(batch.n, batch.tier, int(batch.cfg.seed), batch.obs_mode, None, batch.tile_px,
+                   batch.device.index or 0, obs_transfer, _batch=batch)
+
     def close(self) -> None:
         """Detach the delta-transfer buffers from the handle (idempotent): the
         handle may outlive this object (``env.batch``), and its attachments
@@ -347,10 +355,10 @@ class BatchEnv:
         att = getattr(self, "_attached", None)
         b = getattr(self, "_batch", None)
         while att:
-            buf = att.pop()
+            addr = att.pop()
             if b is not None and getattr(b, "h", None) is not None and b.h.value:
                 try:
-                    lib().gr_host_obs_detach(b.h, buf.ctypes.data_as(ctypes.c_void_p))
+                    lib().gr_host_obs_detach(b.h, ctypes.c_void_p(addr))
                 except Exception:   # interpreter shutdown
                     pass
 

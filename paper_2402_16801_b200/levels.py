@@ -112,3 +112,36 @@ class LevelBuffer:
         check(lib().gr_levels_export_world(self.h, int(level), _p(out["blocks"]), _p(out["items"]), _p(out["spawn"]),
                                            _p(out["ladders"]), _p(out["chests"]), _p(out["potion"])))
         return out
+
+    # --- interchange with the reference's level formats (serialize.py) -------
+    def level_params(self, level: int):
+        """serialize.LevelParams of one level."""
+        from .serialize import LevelParams
+        s, a, f = self.params(level, 1)
+        return LevelParams(int(s[0]), a[0], f[0])
+
+    def set_level_params(self, level: int, p) -> None:
+        self.set_params(level, [p.seed], p.angles[None, :], p.floor_seeds[None, :])
+
+    def export_world(self, level: int):
+        """The level's world as serialize.World (its params included)."""
+        from .serialize import World
+        w = self.world(level)
+        seed, tmpl = ctypes.c_uint64(), ctypes.c_uint32()
+        check(lib().gr_levels_world_info(self.h, int(level), ctypes.byref(seed), ctypes.byref(tmpl)))
+        return World(self.tier, w["blocks"], w["items"], w["spawn"], w["ladders"], w["chests"], w["potion"],
+                     self.level_params(level), int(tmpl.value))
+
+    def import_world(self, level: int, w) -> None:
+        """Write a serialize.World (e.g. world_from_bytes of a reference blob)
+        into level slot ``level``, params included; install() then places it."""
+        from .layout import TIER_DIMS
+        d = TIER_DIMS[self.tier]
+        if w.tier != self.tier or w.blocks.shape != (d["F"], d["H"], d["W"]):
+            raise ValueError(f"a {w.tier} world of shape {w.blocks.shape} does not fit a {self.tier} level buffer")
+        self.set_level_params(level, w.params)
+        b, it = np.ascontiguousarray(w.blocks, np.uint8), np.ascontiguousarray(w.items, np.uint8)
+        sp, lad = np.ascontiguousarray(w.spawn, np.int16), np.ascontiguousarray(w.ladders, np.int16)
+        ch, pot = np.ascontiguousarray(w.chests, np.int64), np.ascontiguousarray(w.potion, np.uint8)
+        check(lib().gr_levels_import_world(self.h, int(level), int(w.params.seed), _p(b), _p(it), _p(sp), _p(lad),
+                                           _p(ch), _p(pot), int(w.template_floors)))

@@ -38,7 +38,8 @@ class ShardedBatch:
 
     def __init__(self, n_envs_global: int, tier: str = "extended", seed: int = 0,
                  obs_mode: str = "symbolic", max_episode_length: int | None = None,
-                 tile_px: int | None = None, reset_ratio: int = 16, group=None, device=None):
+                 tile_px: int | None = None, reset_ratio: int = 16, group=None, device=None,
+                 graph: bool = False):
         import torch
         import torch.distributed as dist
         from .env import GridrogueBatch
@@ -53,6 +54,16 @@ class ShardedBatch:
                                     n_envs_global=n_envs_global)
         self.ex = torch.zeros(4, dtype=torch.int32, device=self.batch.device)
         self.ex_all = torch.zeros(4 * self.world, dtype=torch.int32, device=self.batch.device)
+        # graph=True (NCCL): after two eager steps, gr_step_local + the NCCL
+        # all-gather + gr_step_finish are captured in ONE CUDA graph and
+        # replayed (action validation off: the device policy's actions are
+        # valid by construction; validation would synchronise the stream)
+        self.graph = bool(graph)
+        self._graph = None
+        self._eager_steps = 0
+        self._launches_per_step = 0
+        if self.graph:
+            self.batch.set_validate(False)
 
     def reset(self):
         return self.batch.reset()
@@ -65,9 +76,38 @@ class ShardedBatch:
         if a is not self.batch.actions:
             self.batch.actions.copy_(a)   # int64, on this rank's device
             a = self.batch.actions
+        if self._graph is not None:
+            from ._lib import check, lib
+            self._graph.replay()
+            check(lib().gr_account_replay(self.batch.h, 1, self._launches_per_step))
+            return self._outputs()
+        if self.graph and self._eager_steps >= 2:
+            return self._capture_and_run(a)
+        self._eager_steps += 1
+        return self._step_eager(a)
+
+    def _step_eager(self, a):
         self.batch.step_local(a, self.ex)
         self.dist.all_gather_into_tensor(self.ex_all, self.ex, group=self.group)
         return self.batch.step_finish(self.ex_all, self.rank, self.world)
+
+    def _outputs(self):
+        b = self.batch
+        return b.obs, b.reward, b.done, b.newly, b.time, b.floor
+
+    def _capture_and_run(self, a):
+        """Capture local step + all-gather + finish once, then replay.  The
+        library's host-side bookkeeping advanced once during the capture; that
+        advance stands for the first replay, issued right after."""
+        import torch
+        l0 = self.batch.kernel_launches()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._step_eager(a)
+        self._launches_per_step = self.batch.kernel_launches() - l0
+        self._graph = g
+        g.replay()
+        return self._outputs()
 
     def stats(self) -> dict:
         import torch

@@ -19,7 +19,9 @@ shard of the global batch (parallel.ShardedBatch, so pools and resets match
 one global batch), gradients all-reduced over NCCL by DDP.
 
     python -m paper_2402_16801_b200.ppo --total-timesteps 20000000
-    torchrun --nproc-per-node 8 -m paper_2402_16801_b200.ppo --total-timesteps 1000000000
+    python -m paper_2402_16801_b200.ppo --gpus 8 --total-timesteps 1000000000
+    (--gpus N re-launches itself under torch.distributed.run, one rank per GPU;
+    torchrun --nproc-per-node 8 -m paper_2402_16801_b200.ppo ... is equivalent)
 """
 
 from __future__ import annotations
@@ -630,7 +632,22 @@ def main(argv=None) -> int:
             ap.add_argument(f"--{k.replace('_', '-')}", type=type(v), default=v)
     ap.add_argument("--max-updates", type=int, default=None)
     ap.add_argument("--out", default=None, help="write the result JSON here")
+    ap.add_argument("--gpus", type=int, default=1, help="ranks (one per GPU); >1 outside torchrun re-launches")
     args = ap.parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+        import subprocess
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), "-m", "paper_2402_16801_b200.ppo",
+               *(argv if argv is not None else sys.argv[1:])]
+        return subprocess.call(cmd, env=env)
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus and args.gpus > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}")
     kw = {k: getattr(args, k) for k in asdict(PPOConfig())}
     res = train(PPOConfig(**kw), log=lambda s: print(s, file=sys.stderr, flush=True), max_updates=args.max_updates)
     if int(os.environ.get("RANK", "0")) == 0:

@@ -10,14 +10,35 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_reference_arm_json_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--envs", "64",
-                          "--steps", "3", "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+                          "--steps", "3", "--warmup", "3", "--preroll", "5"], capture_output=True, text=True, timeout=300,
+                         cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference"
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "higher_is_better", "scaling", "config",
               "cpu_baseline", "e2e", "dtype", "data"):
         assert k in line, k
-    assert line["steps"] == 3 and line["warmup"] == 1 and line["value"] > 0
+    assert line["steps"] == 3 and line["warmup"] == 3 and line["preroll"] == 5 and line["value"] > 0
+    assert "resets_per_step" in line
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["value"] == line["value"] and line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["config"]["n_envs_per_gpu"] == 64 and line["config"]["tier"] == "extended"
+
+
+def test_gpus_flag_launches_one_rank_per_gpu():
+    """--gpus N outside torchrun re-launches bench.py under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous); rank 0 prints
+    the line for the whole job (dry run: gloo, launch / config plumbing only)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.strip().splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    assert lines[0]["n_gpus"] == 2 and lines[0]["config"]["global_envs"] == 131072
+
+
+def test_gpus_flag_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE" in out.stderr

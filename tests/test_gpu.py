@@ -913,3 +913,101 @@ def test_template_floors_match_reference(torch_cuda):
             for key in ("blocks", "items", "spawn", "ladders", "chests", "potion"):
                 assert np.array_equal(w[key], g[f"{tag}_{key}"]), f"{tag} {key}"
         assert gb.worldgen_counters()["template_floors"] == len(seeds) * (1 if tier == "classic" else 9)
+
+
+def _graph_worker(port, q):
+    import torch
+    import torch.distributed as dist
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        from paper_2402_16801_b200 import GridrogueBatch, ShardedBatch
+        n, seed = 2048, 23
+        sb = ShardedBatch(n, "extended", seed, "symbolic", max_episode_length=20, graph=True)
+        ref = GridrogueBatch(n, "extended", seed, "symbolic", 20, newly=False, info=False)
+        sb.reset()
+        ref.reset()
+        ref.set_validate(False)
+        l0 = sb.batch.kernel_launches()
+        for k in range(30):
+            sb.batch.random_actions(seed, k)
+            obs, rew, done, *_ = sb.step(sb.batch.actions)
+            ref.random_actions(seed, k)
+            o2, r2, d2, *_ = ref.step(ref.actions)
+            assert torch.equal(obs, o2) and torch.equal(rew, r2) and torch.equal(done, d2), f"step {k}"
+        assert sb._graph is not None, "the sharded step was not captured"
+        assert sb.batch.step_index == ref.step_index == 30
+        assert sb.batch.kernel_launches() - l0 >= 30 * 5
+        st = sb.stats()
+        assert st["episodes"] == ref.stats()["episodes"] > 0
+        q.put("ok")
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put(traceback.format_exc())
+
+
+def test_sharded_step_graph_with_nccl(torch_cuda):
+    """gr_step_local + the NCCL all-gather + gr_step_finish captured in ONE
+    CUDA graph (ShardedBatch(graph=True), world size 1 on this GPU) replays
+    the same steps as the plain one-shard path, and the host-side step index
+    and launch count stay exact (gr_account_replay)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_graph_worker, args=(29400 + os.getpid() % 200, q))
+    p.start()
+    msg = q.get(timeout=600)
+    p.join(timeout=60)
+    assert msg == "ok", msg
+
+
+def _gold_blob(name):
+    with open(os.path.join(GOLD, name), "rb") as fh:
+        return fh.read()
+
+
+@pytest.mark.parametrize("tag,seed,attempts", [("classic_3", 3, 16), ("extended_77", 77, 16),
+                                               ("extended_template_7", 7, 0)])
+def test_device_world_written_as_reference_bytes(torch_cuda, tag, seed, attempts):
+    """serialize.world_to_bytes of a world the device generated is the blob the
+    reference's world_to_bytes wrote (serialize.py:77-94), byte for byte."""
+    from paper_2402_16801_b200 import GridrogueBatch, serialize as S
+    from paper_2402_16801_b200._lib import check, lib
+    from paper_2402_16801_b200.levels import LevelBuffer
+    tier = tag.split("_")[0]
+    gb = GridrogueBatch(2, tier, 0, "symbolic")
+    gb.reset()
+    check(lib().gr_set_worldgen_attempts(gb.h, attempts))
+    lv = LevelBuffer(gb, 1)
+    lv.set_params(0, [seed])
+    lv.generate(0, 1)
+    w = lv.export_world(0)
+    assert S.world_to_bytes(w) == _gold_blob(f"world_{tag}.bin")
+    if seed == 77:
+        assert S.params_to_bytes(lv.level_params(0)) == _gold_blob("level_params_77.bin")
+
+
+@pytest.mark.parametrize("tag", ["classic_3", "extended_77", "extended_rswap_5", "extended_template_7"])
+def test_reference_world_blob_installs_like_reference(torch_cuda, tag):
+    """world_from_bytes of a reference blob -> LevelBuffer.import_world ->
+    install into an env slot gives the SimState the reference's engine.reset
+    gives for that world and key (state.py:169-249); export_world writes the
+    blob back byte for byte."""
+    from paper_2402_16801_b200 import GridrogueBatch, serialize as S
+    from paper_2402_16801_b200.layout import field_shapes, FIELD_NAMES
+    from paper_2402_16801_b200.levels import LevelBuffer
+    tier = tag.split("_")[0]
+    blob = _gold_blob(f"world_{tag}.bin")
+    ref = np.load(os.path.join(GOLD, f"world_{tag}_installed.npz"))
+    gb = GridrogueBatch(3, tier, 0, "symbolic")
+    gb.reset()
+    lv = LevelBuffer(gb, 2)
+    lv.import_world(1, S.world_from_bytes(blob))
+    assert S.world_to_bytes(lv.export_world(1)) == blob
+    lv.install([2], [1], [int(ref["key"])])
+    ex = gb.export_state(field_shapes(tier, 3))
+    bad = [f for f in FIELD_NAMES if not np.array_equal(ex[f][2:3], ref[f])]
+    assert not bad, f"installed fields differ from the reference: {bad}"
