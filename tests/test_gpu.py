@@ -1011,3 +1011,39 @@ def test_reference_world_blob_installs_like_reference(torch_cuda, tag):
     ex = gb.export_state(field_shapes(tier, 3))
     bad = [f for f in FIELD_NAMES if not np.array_equal(ex[f][2:3], ref[f])]
     assert not bad, f"installed fields differ from the reference: {bad}"
+
+
+@pytest.mark.parametrize("tier,obs_mode,n,spec", [("extended", "symbolic", 8192, "0"), ("extended", "pixels", 2048, "0"),
+                                                  ("classic", "symbolic", 4096, "1"), ("extended", "symbolic", 1024, "1")])
+def test_two_stream_step_equals_serialised_step(torch_cuda, monkeypatch, tier, obs_mode, n, spec):
+    """Race evidence for the two-stream step (compute-sanitizer is not available
+    on this GPU pool): the step whose reset chain (compaction, worldgen,
+    install, reset-env obs) runs on a side stream beside the main observation
+    writer -- replayed as a CUDA graph, with the speculative pool where noted --
+    produces the same observations, rewards, dones and full state, step for
+    step, as the same batch with everything serialised on one stream, kernel
+    by kernel (GR_OVERLAP=0, GR_GRAPH=0, GR_SPEC=0).  Reset stress: every
+    episode ends within 10 steps, so every step runs the reset chain."""
+    from paper_2402_16801_b200 import GridrogueBatch
+    from paper_2402_16801_b200.layout import field_shapes, FIELD_NAMES
+    torch = torch_cuda
+    monkeypatch.setenv("GR_SPEC", spec)
+    fast = GridrogueBatch(n, tier, 9, obs_mode, 10)
+    for k, v in (("GR_OVERLAP", "0"), ("GR_GRAPH", "0"), ("GR_SPEC", "0")):
+        monkeypatch.setenv(k, v)
+    slow = GridrogueBatch(n, tier, 9, obs_mode, 10)
+    for b in (fast, slow):
+        b.reset()
+        b.set_validate(False)
+    for k in range(120):
+        outs = []
+        for b in (fast, slow):
+            b.random_actions(9, k)
+            outs.append([x.clone() for x in b.step(b.actions)[:4]])
+        for x, y in zip(*outs):
+            assert torch.equal(x, y), f"step {k}"
+        if k % 40 == 39:
+            sa, sb = fast.export_state(field_shapes(tier, n)), slow.export_state(field_shapes(tier, n))
+            bad = [f for f in FIELD_NAMES if not np.array_equal(sa[f], sb[f])]
+            assert not bad, f"state differs at step {k}: {bad}"
+    assert fast.episodes_completed() == slow.episodes_completed() >= n * 10
