@@ -62,6 +62,12 @@ SEED = 0
 STEP_BYTES = {("extended", "symbolic"): 34579, ("classic", "symbolic"): 6281,
               ("extended", "pixels"): 44407, ("classic", "pixels"): 12808,
               ("extended", "none"): 1507, ("classic", "none"): 901}
+# k_step: bytes per env per launch -- 2 x the current floor's non-map state
+# (SURVEY.md 8(d) S_active), the map window, actions / reward / done and the
+# 256-byte observation descriptor it writes
+STEP_KERNEL_BYTES = {"extended": 2 * 456 + 99 + 255 + 9 + 256, "classic": 2 * 395 + 63 + 9 + 256}
+# k_worldgen: the maps of one generated world (blocks + items, all floors)
+WORLD_BYTES = {"extended": 2 * 9 * 48 * 48, "classic": 2 * 64 * 64}
 # dominant kernel (the observation writer): bytes per env per launch.
 # symbolic: row written + block/item view window read + the 256 B
 # descriptor (gr_desc.cuh, read whole); pixels (k_pixels, after k_pixprep): frame written + the 848 /
@@ -349,14 +355,18 @@ def main():
     clk = clocks.stop()
     # pass 2, the per-kernel breakdown behind the roofline: the same steps
     # again with a CUDA event pair around every launch (kernel-by-kernel
-    # launches, no graph), timed the same way (one shard only: the sharded
-    # step is graph-captured with its collective)
+    # launches, no graph), timed the same way
     ktimes, ms_prof = None, None
-    if world == 1:
-        gb.set_profiling(True)
-        ms_prof, t = timed_steps(args.steps, t)
-        gb.set_profiling(False)
-        ktimes = gb.kernel_times()
+    worlds0 = gb.worldgen_counters()["worlds"]
+    gb.set_profiling(True)
+    if world > 1:   # the same sharded step, launched eagerly so every kernel gets its event pair
+        graphed_step, env.step = env.step, env._step_eager
+    ms_prof, t = timed_steps(args.steps, t)
+    if world > 1:
+        env.step = graphed_step
+    gb.set_profiling(False)
+    ktimes = gb.kernel_times()
+    worlds_prof = gb.worldgen_counters()["worlds"] - worlds0
     if dist:
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -377,6 +387,11 @@ def main():
             # the main writer renders every env not reset this step; the reset
             # envs are rendered by a small launch after their install (obs_reset)
             bytes_per_launch = int(OBS_KERNEL_BYTES[key] * (gb.n - resets_per_step))
+        elif dom == "step":
+            bytes_per_launch = STEP_KERNEL_BYTES[args.tier] * gb.n
+        elif dom == "worldgen":
+            # the maps it writes (compute / latency bound: the fraction is small)
+            bytes_per_launch = int(WORLD_BYTES[args.tier] * worlds_prof / max(dom_n, 1))
         else:
             bytes_per_launch = STEP_BYTES[key] * gb.n
         per_launch_ms = dom_ms / max(dom_n, 1)

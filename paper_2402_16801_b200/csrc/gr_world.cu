@@ -497,6 +497,21 @@ __device__ __noinline__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floo
     sm.room[k][0] = r0; sm.room[k][1] = r0 + rh; sm.room[k][2] = c0; sm.room[k][3] = c0 + rw;
   }
   __syncthreads();
+  // The attempt fails at the end unless both ladder tiles (the first and last
+  // room centres, always PATH after carving) stay PATH: the sewer water /
+  // vault gravel pass below turns a PATH tile with u > 0.82 / 0.85 into
+  // water / gravel, and the two must differ.  Those outcomes are known now,
+  // so a doomed attempt (a third of floor-3 / floor-4 attempts) returns
+  // here instead of after the tile passes -- same result, same next attempt.
+  const UField u(hash2(seed, 7 + (uint64_t)attempt), 4);
+  bool doomed;
+  {
+    const int up = sm.cr[0] * T::W + sm.cc[0], down = sm.cr[n - 1] * T::W + sm.cc[n - 1];
+    const float thr = floor == 3 ? 0.82f : floor == 4 ? 0.85f : 2.0f;
+    doomed = up == down || u(up) > thr || u(down) > thr;
+  }
+  __syncthreads();   // every thread has read the centres before a returning one rewrites them
+  if (doomed) return false;
   // the rooms as one column bitmask per row, then one lookup per tile
   for (int r = threadIdx.x; r < T::H; r += WT<EXT>::THREADS) {
     uint64_t m = 0;
@@ -522,7 +537,6 @@ __device__ __noinline__ bool gen_dungeon(WSmem<EXT>& sm, uint64_t seed, int floo
   __syncthreads();
   // moss / sewer water / vault gravel read the pre-pass PATH mask: compute
   // into registers first, write after the barrier
-  const UField u(hash2(seed, 7 + (uint64_t)attempt), 4);
   constexpr int PER = (T::HW + WT<EXT>::THREADS - 1) / WT<EXT>::THREADS;
   uint8_t nb[PER];
 #pragma unroll
