@@ -20,6 +20,7 @@
 #ifndef GRIDROGUE_B200_H
 #define GRIDROGUE_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -181,6 +182,7 @@ int gr_host_obs_detach(gr_env *env, void *obs_host);
  * changed words, [3] final synchronisation (small outputs, dense obs copy);
  * calls / words: host-path calls and changed words delivered. */
 int gr_host_phase_times(gr_env *env, double out[4], int64_t *calls, int64_t *words);
+
 
 /* ---- state channel (parity / checkpoint) -------------------------------- *
  * Copy one SimState field to / from host memory in the reference layout

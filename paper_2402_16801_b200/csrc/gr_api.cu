@@ -274,6 +274,7 @@ struct gr_env {
   cudaEvent_t dl_ev[DL_CHUNKS] = {};           // chunk listed + its count on the host
   cudaEvent_t dl_evd[DL_CHUNKS] = {};          // chunk's list on the host
   std::unique_ptr<HostPool> hpool;            // host threads of the delta scatter
+  int scatter_prefetch = 16;                   // GR_SCATTER_PF: prefetch distance of the scatter (0: off)
   double host_ms[4] = {0, 0, 0, 0};            // enqueue, wait, scatter, tail (gr_host_phase_times)
   int64_t host_calls = 0;
   int64_t host_words = 0;                      // changed words delivered
@@ -440,11 +441,15 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   // extended symbolic: the pool worldgen beside the writer at 3 CTAs/SM (not
   // 8) ends about when the writer does and leaves it more issue slots (writer
   // 0.407 -> 0.395 ms, step 0.470 -> 0.468; pixels and obs-off measured slower)
-  if (cfg->tier == GR_TIER_EXTENDED && cfg->obs_mode == GR_OBS_SYMBOLIC) e->wg_ctas = 3;
+  // pool worldgen CTAs per SM beside the extended symbolic writer: 2 leave the
+  // writer 0.396 ms instead of 0.406 at 65,536 envs while worldgen (0.31 ms)
+  // still ends first (round 2, after the glibc sin/cos and dungeon early exit)
+  if (cfg->tier == GR_TIER_EXTENDED && cfg->obs_mode == GR_OBS_SYMBOLIC) e->wg_ctas = cfg->n_envs >= 32768 ? 2 : 3;
   if (const char* wc = getenv("GR_WG_CTAS")) e->wg_ctas = atoi(wc);
   if (const char* of = getenv("GR_OBS_FIRST")) e->obs_first = atoi(of) != 0;
   if (const char* sp = getenv("GR_SIDE_PRIO")) e->side_prio = atoi(sp);
   if (const char* gg = getenv("GR_GRAPH")) e->graphs = atoi(gg) != 0;
+  if (const char* pf = getenv("GR_SCATTER_PF")) e->scatter_prefetch = atoi(pf);
   e->ext = cfg->tier == GR_TIER_EXTENDED;
   e->d = e->ext ? EXT_DIMS : CLASSIC_DIMS;
   e->n = cfg->n_envs;
@@ -1041,10 +1046,20 @@ static int host_obs_deliver(gr_env* e, HostObs& h, cudaStream_t st, hclock::time
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned long long* cnt = e->dl_cnt_host;
+  const int pf = e->scatter_prefetch;
   auto scatter = [&](const uint2* list, int64_t k) {
     uint32_t* p = h.ptr;
     e->hpool->run(k, [&](int64_t lo, int64_t hi) {
-      for (int64_t i = lo; i < hi; ++i) p[list[i].x] = list[i].y;
+      if (pf > 0) {   // software prefetch pf entries ahead: more misses in flight per thread
+        const int64_t mid = std::max(lo, hi - pf);
+        for (int64_t i = lo; i < mid; ++i) {
+          __builtin_prefetch(p + list[i + pf].x, 1, 0);
+          p[list[i].x] = list[i].y;
+        }
+        for (int64_t i = mid; i < hi; ++i) p[list[i].x] = list[i].y;
+      } else {
+        for (int64_t i = lo; i < hi; ++i) p[list[i].x] = list[i].y;
+      }
     });
     e->host_words += k;
   };
