@@ -1,6 +1,6 @@
 """Mint the north-star parity goldens from the unmodified numpy reference.
 
-    python tests/golden/make_long_golden.py [long|north_star|all]
+    python tests/golden/make_long_golden.py [long|north_star|pixels_px|all]
 
 Run HERE (where /root/reference exists); the GPU box has no reference, so
 the fixtures are committed and both the C oracle (tests/test_oracle_golden.py)
@@ -23,6 +23,10 @@ and the CUDA product (tests/test_gpu.py) are checked against them directly.
   65,536 envs, seed 0): the reset state and observation, then 12 steps with
   reward / done / newly / info / observation / full-state digests per step
   and per-field digests at the end (maps included).
+* ``pixels_px.npz`` (``python tests/golden/make_long_golden.py pixels_px``) -- every supported tile size (``tiles.SUPPORTED_TILE_PX``)
+  for both tiers: 120-step BatchEnv-semantics rollouts of 8 envs (seed 5,
+  ``max_episode_length`` 40) with the stacked ``render_tiles(state, px)``
+  frames digested every step.
 
 Digests: tests/_digest.py (blake2b-64 over dtype name + bytes).
 """
@@ -139,8 +143,32 @@ def north_star():
         episodes=np.int64(st.episodes), level_seeds_digest=np.uint64(digest(bs.level_seeds())))
 
 
+def pixels_px():
+    _ref()
+    from gridrogue import CLASSIC, EXTENDED
+    from gridrogue.batch import BatchConfig, batch_reset, batch_step
+    from gridrogue.policies import RandomPolicy
+    from gridrogue.state import GameState
+    from gridrogue.tiles import render_tiles, SUPPORTED_TILE_PX
+    out = {"px": np.array(SUPPORTED_TILE_PX, np.int64)}
+    n, steps, seed, ml = 8, 120, 5, 40
+    for tier, t in (("classic", CLASSIC), ("extended", EXTENDED)):
+        for px in SUPPORTED_TILE_PX:
+            bs = batch_reset(BatchConfig(n_envs=n, tier=t, max_episode_length=ml), seed)
+            pol = RandomPolicy(seed, t.n_actions)
+            frames = lambda: np.stack([render_tiles(GameState(bs.sim.view(slice(i, i + 1))), px) for i in range(n)])
+            dg = [digest(frames())]
+            for k in range(steps):
+                bs, _ = batch_step(bs, pol.actions(bs.sim))
+                dg.append(digest(frames()))
+            out[f"{tier}_{px}"] = np.array(dg, np.uint64)
+    np.savez_compressed(os.path.join(OUT, "pixels_px.npz"), n=n, steps=steps, seed=seed, max_len=ml, **out)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what == "pixels_px":
+        pixels_px()
     if what in ("long", "all"):
         for nm in (sys.argv[2:] or LONG):
             long_rollout(nm)

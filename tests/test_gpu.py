@@ -1047,3 +1047,20 @@ def test_two_stream_step_equals_serialised_step(torch_cuda, monkeypatch, tier, o
             bad = [f for f in FIELD_NAMES if not np.array_equal(sa[f], sb[f])]
             assert not bad, f"state differs at step {k}: {bad}"
     assert fast.episodes_completed() == slow.episodes_completed() >= n * 10
+
+
+@pytest.mark.parametrize("tier", ["classic", "extended"])
+@pytest.mark.parametrize("px", [7, 10, 16])
+def test_pixels_every_tile_size_match_reference(torch_cuda, tier, px):
+    """The device pixel writer at every supported tile size, both tiers,
+    against frames rendered by the reference itself (tests/golden/pixels_px.npz)."""
+    from paper_2402_16801_b200 import GridrogueBatch
+    from tests._digest import digest
+    g = np.load(os.path.join(GOLD, "pixels_px.npz"))
+    n, steps, seed, ml = (int(g[k]) for k in ("n", "steps", "seed", "max_len"))
+    want = g[f"{tier}_{px}"]
+    gb = GridrogueBatch(n, tier, seed, "pixels", ml, tile_px=px)
+    assert digest(gb.reset().cpu().numpy()) == int(want[0]), "reset"
+    for k in range(steps):
+        obs = gb.step(gb.random_actions(seed, k))[0]
+        assert digest(obs.cpu().numpy()) == int(want[k + 1]), f"step {k}"

@@ -280,3 +280,20 @@ def test_template_floors_match_reference(oracle_lib):
             assert np.array_equal(ch, g[f"{tag}_chests"]), tag
     finally:
         L.go_set_max_gen_retries(16)
+
+
+@pytest.mark.parametrize("tier", ["classic", "extended"])
+def test_pixels_every_tile_size_match_reference(oracle_lib, tier):
+    """tiles.render_tiles at every supported tile size (7, 10, 16 px), both
+    tiers, 120 auto-resetting steps (tests/golden/pixels_px.npz)."""
+    O = oracle_lib
+    g = np.load(os.path.join(GOLD, "pixels_px.npz"))
+    n, steps, seed, ml = (int(g[k]) for k in ("n", "steps", "seed", "max_len"))
+    na = O.TIERS[tier]["NA"]
+    for px in g["px"]:
+        b = O.OracleBatch(tier, n, seed, max_episode_length=ml)
+        want = g[f"{tier}_{int(px)}"]
+        assert digest(b.state.render_pixels(int(px))) == int(want[0]), f"{px} px reset"
+        for k in range(steps):
+            b.step(O.random_actions(seed, k, n, na))
+            assert digest(b.state.render_pixels(int(px))) == int(want[k + 1]), f"{px} px step {k}"
