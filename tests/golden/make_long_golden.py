@@ -19,6 +19,9 @@ and the CUDA product (tests/test_gpu.py) are checked against them directly.
   full SimState digest (every field of ``state.FIELD_NAMES``, maps included)
   plus the f64 episode accumulators (``batch.py:200-201``), which pin the f64
   reward sums.
+* ``long_{classic,extended}_symbolic_n1024.npz`` -- the same for 1,024 envs
+  (seed 77, no episode cap: natural deaths only), the observation digested
+  every 50 steps: 10^7 env-steps per tier.
 * ``north_star_ext_n65536.npz`` -- the bench workload (Craftax-Symbolic,
   65,536 envs, seed 0): the reset state and observation, then 12 steps with
   reward / done / newly / info / observation / full-state digests per step
@@ -44,13 +47,17 @@ OUT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
 from tests._digest import digest, state_digest  # noqa: E402
 
-LONG = {   # name: (tier, obs, n)
-    "classic_symbolic": ("classic", "symbolic", 32),
-    "extended_symbolic": ("extended", "symbolic", 32),
-    "classic_pixels": ("classic", "pixels", 16),
-    "extended_pixels": ("extended", "pixels", 12),
+LONG = {   # name: (tier, obs, n, seed, max_episode_length, observation digest every k steps)
+    "classic_symbolic": ("classic", "symbolic", 32, 31, 700, 1),
+    "extended_symbolic": ("extended", "symbolic", 32, 31, 700, 1),
+    "classic_pixels": ("classic", "pixels", 16, 31, 700, 1),
+    "extended_pixels": ("extended", "pixels", 12, 31, 700, 1),
+    # 1,024 envs, natural episode ends (no cap): 10^7 env-steps per tier;
+    # rewards / dones every step, observations every 50 steps
+    "classic_symbolic_n1024": ("classic", "symbolic", 1024, 77, None, 50),
+    "extended_symbolic_n1024": ("extended", "symbolic", 1024, 77, None, 50),
 }
-LONG_STEPS, LONG_SEED, LONG_MAXLEN, LONG_EVERY = 10_000, 31, 700, 2500
+LONG_STEPS, LONG_EVERY = 10_000, 2500
 
 
 def _ref():
@@ -68,11 +75,11 @@ def long_rollout(name):
     from gridrogue.state import FIELD_NAMES, GameState
     from gridrogue.tiles import render_tiles
 
-    tier, obs_mode, n = LONG[name]
+    tier, obs_mode, n, seed, max_len, obs_every = LONG[name]
     t = {"classic": CLASSIC, "extended": EXTENDED}[tier]
     px = 7 if tier == "classic" else 10
-    bs = batch_reset(BatchConfig(n_envs=n, tier=t, max_episode_length=LONG_MAXLEN), LONG_SEED)
-    pol = RandomPolicy(LONG_SEED, t.n_actions)
+    bs = batch_reset(BatchConfig(n_envs=n, tier=t, max_episode_length=max_len), seed)
+    pol = RandomPolicy(seed, t.n_actions)
 
     def observe():
         if obs_mode == "symbolic":
@@ -89,14 +96,14 @@ def long_rollout(name):
         bs, out = batch_step(bs, pol.actions(bs.sim))
         rew.append(digest(out.reward.astype(np.float32)))
         done.append(digest(out.done))
-        obs.append(digest(observe()))
+        obs.append(digest(observe()) if k % obs_every == 0 else 0)
         if (k + 1) % LONG_EVERY == 0:
             ckpt.append([full_state(), digest(bs.ep_return, bs.ep_length)])
             print(f"  {name}: step {k + 1} ({time.time() - t0:.0f} s)", flush=True)
     st = bs.stats
     np.savez_compressed(
         os.path.join(OUT, f"long_{name}.npz"), tier=tier, obs_mode=obs_mode, n=n, steps=LONG_STEPS,
-        seed=LONG_SEED, max_len=LONG_MAXLEN, every=LONG_EVERY, tile_px=px, reset=reset,
+        seed=seed, max_len=max_len or 0, every=LONG_EVERY, tile_px=px, obs_every=obs_every, reset=reset,
         reward=np.array(rew, np.uint64), done=np.array(done, np.uint64), obs=np.array(obs, np.uint64),
         ckpt=np.array(ckpt, np.uint64),
         final_fields=np.array([digest(getattr(bs.sim, f)) for f in FIELD_NAMES], np.uint64),

@@ -498,7 +498,8 @@ LONG = sorted(f[len("long_"):-4] for f in os.listdir(GOLD) if f.startswith("long
 @pytest.mark.parametrize("name", LONG)
 def test_long_rollout_parity_10k(torch_cuda, name):
     """BASELINE.json north star, pinned to the reference itself: 10^4-step random
-    rollouts of all four variants (Classic/Full x Symbolic/Pixels) against digests
+    rollouts of all four variants (Classic/Full x Symbolic/Pixels), and of the
+    symbolic variants at 1,024 envs with natural episode ends, against digests
     minted from the unmodified numpy reference (tests/golden/make_long_golden.py):
     every step's reward / done / observation, the full SimState (maps included)
     and the f64 episode accumulators every 2,500 steps, final fields and
@@ -511,8 +512,9 @@ def test_long_rollout_parity_10k(torch_cuda, name):
     g = np.load(os.path.join(GOLD, f"long_{name}.npz"))
     tier, obs_mode, n = str(g["tier"]), str(g["obs_mode"]), int(g["n"])
     steps, seed, ml, every, px = (int(g[k]) for k in ("steps", "seed", "max_len", "every", "tile_px"))
+    obs_every = int(g["obs_every"]) if "obs_every" in g.files else 1
     shapes = field_shapes(tier, n)
-    gb = GridrogueBatch(n, tier, seed, obs_mode, ml, tile_px=px, newly=False, info=False)
+    gb = GridrogueBatch(n, tier, seed, obs_mode, ml or None, tile_px=px, newly=False, info=False)
     obs = gb.reset()
     assert state_digest(gb.export_state(shapes), FIELD_NAMES) == int(g["reset"][0]), "reset state"
     assert digest(obs.cpu().numpy()) == int(g["reset"][1]), "reset obs"
@@ -522,7 +524,8 @@ def test_long_rollout_parity_10k(torch_cuda, name):
         obs, rew, done, *_ = gb.step(gb.random_actions(seed, k))
         assert digest(rew.cpu().numpy()) == int(g["reward"][k]), f"reward step {k}"
         assert digest(done.cpu().numpy().astype(bool)) == int(g["done"][k]), f"done step {k}"
-        assert digest(obs.cpu().numpy()) == int(g["obs"][k]), f"obs step {k}"
+        if k % obs_every == 0:
+            assert digest(obs.cpu().numpy()) == int(g["obs"][k]), f"obs step {k}"
         if (k + 1) % every == 0:
             assert state_digest(gb.export_state(shapes), FIELD_NAMES) == int(g["ckpt"][c][0]), f"state step {k}"
             assert digest(*gb.episode_progress()) == int(g["ckpt"][c][1]), f"episode acc step {k}"
@@ -531,7 +534,7 @@ def test_long_rollout_parity_10k(torch_cuda, name):
     bad = [f for f, dg in zip(FIELD_NAMES, g["final_fields"]) if digest(ex[f]) != int(dg)]
     assert not bad, f"fields differ from the reference: {bad}"
     s = gb.stats()
-    assert s["episodes"] == int(g["episodes"]) >= n * (steps // ml)
+    assert s["episodes"] == int(g["episodes"]) >= (n * (steps // ml) if ml else n)
     assert s["total_steps"] == int(g["total_steps"])
     assert np.array_equal(s["ach_episodes"], g["ach_episodes"])
     assert np.array_equal(gb.level_seeds(), g["level_seeds"])

@@ -157,6 +157,8 @@ LONG = sorted(f[len("long_"):-4] for f in os.listdir(GOLD) if f.startswith("long
 
 @pytest.mark.parametrize("name", LONG)
 def test_long_rollout_matches_reference(oracle_lib, name):
+    if name.endswith("_n1024") and not os.environ.get("GR_SLOW"):
+        pytest.skip("10^7 env-steps on the oracle: set GR_SLOW=1 (~1 min, 8 cores)")
     """BASELINE.json north star: 10^4-step random rollouts of all four variants
     (tests/golden/make_long_golden.py, minted from the unmodified reference):
     every step's reward / done / observation, the full SimState + f64 episode
@@ -165,7 +167,8 @@ def test_long_rollout_matches_reference(oracle_lib, name):
     g = np.load(os.path.join(GOLD, f"long_{name}.npz"))
     tier, obs_mode, n = str(g["tier"]), str(g["obs_mode"]), int(g["n"])
     steps, seed, ml, every, px = (int(g[k]) for k in ("steps", "seed", "max_len", "every", "tile_px"))
-    b = O.OracleBatch(tier, n, seed, max_episode_length=ml)
+    obs_every = int(g["obs_every"]) if "obs_every" in g.files else 1
+    b = O.OracleBatch(tier, n, seed, max_episode_length=ml or None, threads=8 if n > 256 else 1)
     st = b.state
 
     def observe():
@@ -179,7 +182,8 @@ def test_long_rollout_matches_reference(oracle_lib, name):
         r, d, _, _ = b.step(O.random_actions(seed, k, n, na))
         assert digest(r.astype(np.float32)) == int(g["reward"][k]), f"reward step {k}"
         assert digest(d) == int(g["done"][k]), f"done step {k}"
-        assert digest(observe()) == int(g["obs"][k]), f"obs step {k}"
+        if k % obs_every == 0:
+            assert digest(observe()) == int(g["obs"][k]), f"obs step {k}"
         if (k + 1) % every == 0:
             assert state_digest(st.export_fields(), O.FIELD_NAMES) == int(g["ckpt"][c][0]), f"state step {k}"
             assert digest(*b.episode_progress()) == int(g["ckpt"][c][1]), f"episode acc step {k}"
