@@ -365,7 +365,12 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(
   uint8_t* out = (uint8_t*)a.out;
   while (j >= 0) {
     const int64_t i = env_of(j);
-    const int64_t jn = next_env(j + stride);
+    // the next env: its done flag is loaded now and only looked at after
+    // the class rows are built, so the load's latency hides under the build
+    // (resolving it here stalled every frame's start on a global load)
+    const int64_t cand = j + stride;
+    const bool cand_ok = cand < count;
+    const uint8_t cand_done = (a.sel == 1 && cand_ok) ? __ldcg(a.done + cand) : (uint8_t)0;
     const PixSmem<EXT>& pm = *reinterpret_cast<const PixSmem<EXT>*>(&pmw[cur][0]);
     // 1. class rows
     {
@@ -465,6 +470,7 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(
       }
     }
     __syncthreads();
+    const int64_t jn = !cand_ok ? -1 : cand_done ? next_env(cand + stride) : cand;
     if (warp == 0 && jn >= 0) fetch(env_of(jn), cur ^ 1);   // the next env's inputs, under this env's stores
     // 2. stream the frame: bytes [f0, f0 + FB) of the output
     const int64_t f0 = i * (int64_t)G::FB;
