@@ -449,7 +449,7 @@ def _phases(gb) -> dict:
     c = max(calls.value, 1)
     return {"ms_per_step": {"enqueue": round(out[0] / c, 3), "device_wait": round(out[1] / c, 3),
                             "host_scatter": round(out[2] / c, 3), "final_sync": round(out[3] / c, 3)},
-            "changed_words_per_step": int(words.value / c)}
+            "changed_words_per_step": int(words.value / c)}   # delta: changed words; compact: non-zero words
 
 
 def run_e2e(args, gb, env, world, rank, dist, t):
@@ -482,10 +482,18 @@ def run_e2e(args, gb, env, world, rank, dist, t):
         dense_env = BatchEnv.from_batch(gb, "dense")
         v_dense, ph_dense = run(dense_env, 0)
         dense_env.close()
+        if args.obs == "symbolic" and os.environ.get("GR_HOST_COMPACT", "1") != "0":
+            nb = (gb.obs.shape[1] + 31) // 32
+            d2h_dense = n * nb * 4 + n * 8 + ph_dense["changed_words_per_step"] * 4 + small_d2h
+            how = ("the observation travels packed (per row a non-zero bitmap + its values, gr_host_phase_times "
+                   "words) and host threads expand it into the whole array (AVX-512 expand, streaming stores)")
+        else:
+            d2h_dense = obs_bytes + small_d2h
+            how = "D2H of the whole observation"
         out = {"value": round(v_dense, 1), "unit": UNIT, "h2d_bytes_per_step": n * 8,
-               "d2h_bytes_per_step": int(obs_bytes + small_d2h), "steps": steps,
+               "d2h_bytes_per_step": int(d2h_dense), "steps": steps,
                "path": "BatchEnv.step (numpy in/out, writable obs arrays as the reference returns): "
-                       "H2D actions, device step, D2H of the whole observation + reward/done/info",
+                       "H2D actions, device step, " + how + ", D2H of reward/done/info",
                "phases": ph_dense}
         if args.obs == "symbolic" and n * gb.obs.shape[1] < 2 ** 32:
             delta_env = BatchEnv.from_batch(gb, "delta")

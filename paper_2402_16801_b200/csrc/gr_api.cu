@@ -30,6 +30,7 @@
 #include <mutex>
 #include <thread>
 #include <cuda_runtime.h>
+#include <immintrin.h>
 
 #include "gr_device.cuh"
 #include "gr_state.cuh"
@@ -275,7 +276,17 @@ struct gr_env {
   cudaEvent_t dl_evd[DL_CHUNKS] = {};          // chunk's list on the host
   std::unique_ptr<HostPool> hpool;            // host threads of the delta scatter
   int scatter_prefetch = 16;                   // GR_SCATTER_PF: prefetch distance of the scatter (0: off)
-  double host_ms[4] = {0, 0, 0, 0};            // enqueue, wait, scatter, tail (gr_host_phase_times)
+  // compact transfer of symbolic observations into plain host arrays: per
+  // row a non-zero bitmap + the row's offset into a packed value list
+  uint32_t* cp_bm_dev = nullptr;               // [n][NB] bitmaps
+  uint32_t* cp_val_dev = nullptr;              // [n][W] worst case: chunk c packs into rows [r0, r1)'s region
+  int64_t* cp_off_dev = nullptr;               // [n] offset of each row's values in its chunk's list
+  uint32_t* cp_bm_host = nullptr;              // pinned twins
+  uint32_t* cp_val_host = nullptr;             // capacity cp_val_cap words, split over the chunks
+  int64_t* cp_off_host = nullptr;
+  int64_t cp_val_cap = 0;
+  bool compact = true;                         // GR_HOST_COMPACT=0: plain 2 GB copy into the host array
+  double host_ms[4] = {0, 0, 0, 0};            // enqueue, wait, scatter / decode, tail (gr_host_phase_times)
   int64_t host_calls = 0;
   int64_t host_words = 0;                      // changed words delivered
   // reset work (worldgen + install + obs of reset envs) overlaps the obs of
@@ -395,6 +406,12 @@ void gr_destroy(gr_env* e) {
     if (h.shadow) cudaFree(h.shadow);
   if (e->dl_host) cudaFreeHost(e->dl_host);
   if (e->dl_dev) cudaFree(e->dl_dev);
+  if (e->cp_bm_dev) cudaFree(e->cp_bm_dev);
+  if (e->cp_val_dev) cudaFree(e->cp_val_dev);
+  if (e->cp_off_dev) cudaFree(e->cp_off_dev);
+  if (e->cp_bm_host) cudaFreeHost(e->cp_bm_host);
+  if (e->cp_val_host) cudaFreeHost(e->cp_val_host);
+  if (e->cp_off_host) cudaFreeHost(e->cp_off_host);
   if (e->dl_cnt_host) cudaFreeHost(e->dl_cnt_host);
   if (e->dl_cnt_dev) cudaFree(e->dl_cnt_dev);
   if (e->dl_copy) cudaStreamDestroy(e->dl_copy);
@@ -450,6 +467,7 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (const char* sp = getenv("GR_SIDE_PRIO")) e->side_prio = atoi(sp);
   if (const char* gg = getenv("GR_GRAPH")) e->graphs = atoi(gg) != 0;
   if (const char* pf = getenv("GR_SCATTER_PF")) e->scatter_prefetch = atoi(pf);
+  if (const char* hc = getenv("GR_HOST_COMPACT")) e->compact = atoi(hc) != 0;
   e->ext = cfg->tier == GR_TIER_EXTENDED;
   e->d = e->ext ? EXT_DIMS : CLASSIC_DIMS;
   e->n = cfg->n_envs;
@@ -1004,6 +1022,16 @@ int gr_host_obs_detach(gr_env* e, void* obs_host) {
 }
 
 using hclock = std::chrono::steady_clock;
+
+// host threads of the delta scatter / compact expansion (GR_HOST_THREADS, default: every hardware thread, <= 32)
+static int host_threads() {
+  if (const char* t = getenv("GR_HOST_THREADS")) {
+    const int v = atoi(t);
+    if (v > 0) return std::min(v, 64);
+  }
+  const unsigned hc = std::thread::hardware_concurrency();
+  return (int)std::min<unsigned>(hc ? hc : 1, 32);
+}
 static double ms_since(hclock::time_point t0) {
   return std::chrono::duration<double, std::milli>(hclock::now() - t0).count();
 }
@@ -1036,8 +1064,7 @@ static int host_obs_deliver(gr_env* e, HostObs& h, cudaStream_t st, hclock::time
     CK(cudaStreamCreateWithFlags(&e->dl_copy, cudaStreamNonBlocking));
     for (auto& ev : e->dl_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (auto& ev : e->dl_evd) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    unsigned hc = std::thread::hardware_concurrency();
-    e->hpool.reset(new HostPool((int)std::min<unsigned>(hc ? hc : 1, 32)));
+    e->hpool.reset(new HostPool(host_threads()));
   }
   int rc = ensure_delta_list(e, e->n * (int64_t)std::min(W, 256));
   if (rc) return rc;
@@ -1137,6 +1164,176 @@ static int host_obs_deliver(gr_env* e, HostObs& h, cudaStream_t st, hclock::time
   return GR_OK;
 }
 
+// ---- compact observation transfer ------------------------------------------
+// The reference hands back a fresh, writable float32 array per step
+// (__init__.py:79): 2.17 GB at 65,536 extended envs, which as a plain copy
+// is PCIe-bound (~55 GB/s: 40 ms).  A symbolic row is ~95 % zeros, and the
+// host writes memory 3x faster than PCIe delivers it (measured on the GPU
+// box: 159-188 GB/s with non-temporal stores), so the rows travel packed --
+// per row a bitmap of its non-zero words (bitwise: -0.0f counts) and its
+// values, ~190 MB -- and host threads expand them into the caller's array
+// (AVX-512 masked expand + streaming stores), chunk by chunk so chunk c's
+// expansion overlaps chunk c+1's packing and copy.  Every word of the array
+// is written each step: the result is the dense copy, bit for bit.
+__global__ void __launch_bounds__(DL_WARPS * 32) k_obs_pack(const uint32_t* __restrict__ obs, int64_t r0, int64_t r1,
+                                                             int W, int NB, uint32_t* __restrict__ bm,
+                                                             uint32_t* __restrict__ vals, int64_t* __restrict__ off,
+                                                             unsigned long long* __restrict__ cursor) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * DL_WARPS;
+  for (int64_t r = r0 + (int64_t)blockIdx.x * DL_WARPS + wid; r < r1; r += nwarps) {
+    const uint32_t* row = obs + r * W;
+    uint32_t* b = bm + r * NB;
+    int cnt = 0;
+    for (int ch = 0; ch < NB; ++ch) {
+      const int c = (ch << 5) + lane;
+      const uint32_t m = __ballot_sync(~0u, c < W && __ldcg(row + c) != 0u);
+      if (lane == 0) b[ch] = m;
+      cnt += __popc(m);
+    }
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(cursor, (unsigned long long)cnt);
+    base = __shfl_sync(~0u, base, 0);
+    if (lane == 0) off[r] = (int64_t)base;
+    __syncwarp();
+    for (int ch = 0; ch < NB; ++ch) {
+      const uint32_t m = b[ch];   // this warp's own store, visible after __syncwarp
+      if (!m) continue;
+      if ((m >> lane) & 1u) vals[base + __popc(m & ((1u << lane) - 1u))] = row[(ch << 5) + lane];
+      base += __popc(m);
+    }
+  }
+}
+
+// expand rows [r0, r1) of a chunk into the host array
+__attribute__((target("avx512f,avx512bw"))) static void cp_expand_avx512(float* out, int W, int NB, const uint32_t* bm,
+                                                                           const float* vals, const int64_t* off,
+                                                                           int64_t r0, int64_t r1) {
+  for (int64_t r = r0; r < r1; ++r) {
+    float* dst = out + r * W;
+    const uint32_t* b = bm + r * NB;
+    const float* v = vals + off[r];
+    auto bits16 = [&](int k) -> uint32_t {   // bitmap bits k .. k+15
+      const int w = k >> 5, s = k & 31;
+      uint64_t x = b[w];
+      if (w + 1 < NB) x |= (uint64_t)b[w + 1] << 32;
+      return (uint32_t)(x >> s) & 0xFFFFu;
+    };
+    // scalar head up to the first 64-byte aligned word, streaming stores of
+    // 16 words, scalar tail
+    int k = (int)(((64 - ((uintptr_t)dst & 63)) & 63) >> 2);
+    if (k > W) k = W;
+    for (int q = 0; q < k; ++q) dst[q] = (b[q >> 5] >> (q & 31)) & 1u ? *v++ : 0.0f;
+    for (; k + 16 <= W; k += 16) {
+      const uint32_t m = bits16(k);
+      _mm512_stream_ps(dst + k, _mm512_maskz_expandloadu_ps((__mmask16)m, v));
+      v += __builtin_popcount(m);
+    }
+    for (int q = k; q < W; ++q) dst[q] = (b[q >> 5] >> (q & 31)) & 1u ? *v++ : 0.0f;
+  }
+  _mm_sfence();
+}
+
+static void cp_expand_scalar(float* out, int W, int NB, const uint32_t* bm, const float* vals, const int64_t* off,
+                             int64_t r0, int64_t r1) {
+  for (int64_t r = r0; r < r1; ++r) {
+    uint32_t* dst = reinterpret_cast<uint32_t*>(out + r * W);
+    const uint32_t* b = bm + r * NB;
+    const uint32_t* v = reinterpret_cast<const uint32_t*>(vals + off[r]);
+    for (int q = 0; q < W; ++q) dst[q] = (b[q >> 5] >> (q & 31)) & 1u ? *v++ : 0u;
+  }
+}
+
+static int host_obs_compact(gr_env* e, float* out, cudaStream_t st, hclock::time_point t_call) {
+  const int W = (int)obs_elems_of(e), NB = (W + 31) / 32;
+  if (!e->dl_cnt_host) {
+    CK(cudaHostAlloc((void**)&e->dl_cnt_host, DL_CHUNKS * sizeof(unsigned long long), cudaHostAllocDefault));
+    CK(cudaMalloc((void**)&e->dl_cnt_dev, DL_CHUNKS * sizeof(unsigned long long)));
+    CK(cudaStreamCreateWithFlags(&e->dl_copy, cudaStreamNonBlocking));
+    for (auto& ev : e->dl_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    for (auto& ev : e->dl_evd) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->hpool.reset(new HostPool(host_threads()));
+  }
+  if (!e->cp_bm_dev) {
+    CK(cudaMalloc((void**)&e->cp_bm_dev, (size_t)e->n * NB * 4));
+    CK(cudaMalloc((void**)&e->cp_val_dev, (size_t)e->n * W * 4));
+    CK(cudaMalloc((void**)&e->cp_off_dev, (size_t)e->n * 8));
+    CK(cudaHostAlloc((void**)&e->cp_bm_host, (size_t)e->n * NB * 4, cudaHostAllocDefault));
+    CK(cudaHostAlloc((void**)&e->cp_off_host, (size_t)e->n * 8, cudaHostAllocDefault));
+    e->cp_val_cap = e->n * (int64_t)std::min(W, 640);   // symbolic rows hold <= ~450 non-zeros
+    CK(cudaHostAlloc((void**)&e->cp_val_host, (size_t)e->cp_val_cap * 4, cudaHostAllocDefault));
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static const bool avx512 = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw");
+  const int C = (int)std::min<int64_t>(DL_CHUNKS, std::max<int64_t>(1, e->n / 256));
+  double t_wait = 0, t_dec = 0;
+  auto wait = [&](cudaEvent_t ev) -> int {
+    const auto t0 = hclock::now();
+    CK(cudaEventSynchronize(ev));
+    t_wait += ms_since(t0);
+    return GR_OK;
+  };
+  CK(cudaMemsetAsync(e->dl_cnt_dev, 0, C * sizeof(unsigned long long), st));
+  for (int c = 0; c < C; ++c) {
+    const int64_t r0 = e->n * c / C, r1 = e->n * (c + 1) / C;
+    const int grid = (int)std::min<int64_t>((r1 - r0 + DL_WARPS - 1) / DL_WARPS, (int64_t)sms * 8);
+    k_obs_pack<<<grid, DL_WARPS * 32, 0, st>>>((const uint32_t*)e->h_obs_dev, r0, r1, W, NB, e->cp_bm_dev,
+                                                e->cp_val_dev + r0 * W, e->cp_off_dev, e->dl_cnt_dev + c);
+    e->launches += 1;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(e->dl_cnt_host + c, e->dl_cnt_dev + c, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(e->dl_ev[c], st));
+  }
+  e->host_ms[0] += ms_since(t_call);
+  int rc;
+  int64_t vofs[DL_CHUNKS + 1];
+  bool dense[DL_CHUNKS];
+  vofs[0] = 0;
+  for (int c = 0; c <= C; ++c) {
+    if (c < C) {
+      const int64_t r0 = e->n * c / C, r1 = e->n * (c + 1) / C;
+      if ((rc = wait(e->dl_ev[c]))) return rc;
+      const int64_t k = (int64_t)e->dl_cnt_host[c];
+      dense[c] = vofs[c] + k > e->cp_val_cap;   // stage full: this chunk goes as a plain copy
+      vofs[c + 1] = dense[c] ? vofs[c] : vofs[c] + k;
+      CK(cudaStreamWaitEvent(e->dl_copy, e->dl_ev[c], 0));
+      if (dense[c]) {
+        CK(cudaMemcpyAsync(out + r0 * W, (const float*)e->h_obs_dev + r0 * W, (size_t)(r1 - r0) * W * 4,
+                           cudaMemcpyDeviceToHost, e->dl_copy));
+      } else {
+        CK(cudaMemcpyAsync(e->cp_bm_host + r0 * NB, e->cp_bm_dev + r0 * NB, (size_t)(r1 - r0) * NB * 4,
+                           cudaMemcpyDeviceToHost, e->dl_copy));
+        CK(cudaMemcpyAsync(e->cp_off_host + r0, e->cp_off_dev + r0, (size_t)(r1 - r0) * 8, cudaMemcpyDeviceToHost,
+                           e->dl_copy));
+        if (k)
+          CK(cudaMemcpyAsync(e->cp_val_host + vofs[c], e->cp_val_dev + r0 * W, (size_t)k * 4, cudaMemcpyDeviceToHost,
+                             e->dl_copy));
+      }
+      CK(cudaEventRecord(e->dl_evd[c], e->dl_copy));
+    }
+    if (c > 0) {
+      const int cc = c - 1;
+      const int64_t r0 = e->n * cc / C, r1 = e->n * (cc + 1) / C;
+      if ((rc = wait(e->dl_evd[cc]))) return rc;
+      if (!dense[cc]) {
+        const auto t0 = hclock::now();
+        const float* vals = reinterpret_cast<const float*>(e->cp_val_host + vofs[cc]);
+        e->hpool->run(r1 - r0, [&](int64_t lo, int64_t hi) {
+          if (avx512) cp_expand_avx512(out, W, NB, e->cp_bm_host, vals, e->cp_off_host, r0 + lo, r0 + hi);
+          else cp_expand_scalar(out, W, NB, e->cp_bm_host, vals, e->cp_off_host, r0 + lo, r0 + hi);
+        });
+        t_dec += ms_since(t0);
+        e->host_words += vofs[cc + 1] - vofs[cc];
+      }
+    }
+  }
+  e->host_ms[1] += t_wait;
+  e->host_ms[2] += t_dec;
+  return GR_OK;
+}
+
 int gr_reset_host(gr_env* e, void* obs_host) {
   if (!e) return fail(GR_E_INVALID, "null env");
   CK(cudaSetDevice(e->cfg.device));
@@ -1150,8 +1347,12 @@ int gr_reset_host(gr_env* e, void* obs_host) {
   const int64_t ob = obs_elems_of(e) * (e->cfg.obs_mode == GR_OBS_PIXELS ? 1 : 4);
   if (HostObs* ho = obs_host ? find_host_obs(e, obs_host) : nullptr)
     return host_obs_deliver(e, *ho, e->h_stream, t_call);
-  if (obs_host && ob)
+  if (obs_host && ob && e->compact && e->cfg.obs_mode == GR_OBS_SYMBOLIC) {
+    rc = host_obs_compact(e, (float*)obs_host, e->h_stream, t_call);
+    if (rc) return rc;
+  } else if (obs_host && ob) {
     CK(cudaMemcpyAsync(obs_host, e->h_obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, e->h_stream));
+  }
   CK(cudaStreamSynchronize(e->h_stream));
   return GR_OK;
 }
@@ -1192,6 +1393,9 @@ int gr_step_host(gr_env* e, const int64_t* actions_host, void* obs_host, float* 
   if (floor_host) CK(cudaMemcpyAsync(floor_host, e->h_floor_dev, e->n, cudaMemcpyDeviceToHost, st));
   if (HostObs* ho = obs_host ? find_host_obs(e, obs_host) : nullptr) {
     rc = host_obs_deliver(e, *ho, st, t_call);
+    if (rc) return rc;
+  } else if (obs_host && ob && e->compact && e->cfg.obs_mode == GR_OBS_SYMBOLIC) {
+    rc = host_obs_compact(e, (float*)obs_host, st, t_call);
     if (rc) return rc;
   } else {
     if (obs_host && ob) CK(cudaMemcpyAsync(obs_host, e->h_obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, st));

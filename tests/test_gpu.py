@@ -1067,3 +1067,35 @@ def test_pixels_every_tile_size_match_reference(torch_cuda, tier, px):
     for k in range(steps):
         obs = gb.step(gb.random_actions(seed, k))[0]
         assert digest(obs.cpu().numpy()) == int(want[k + 1]), f"step {k}"
+
+
+@pytest.mark.parametrize("tier", ["extended", "classic"])
+def test_host_step_compact_equals_device_obs(torch_cuda, monkeypatch, tier):
+    """gr_step_host into a plain (pageable) numpy array with the compact
+    transfer (per-row non-zero bitmap + values, expanded on the host) gives
+    exactly the device observation, every step, under reset stress -- and so
+    does the plain 2 GB copy (GR_HOST_COMPACT=0); words the host array held
+    before are all overwritten."""
+    import ctypes
+    from paper_2402_16801_b200 import GridrogueBatch
+    from paper_2402_16801_b200._lib import check, lib
+    torch = torch_cuda
+    n, seed = 1536, 3
+    for compact in ("1", "0"):
+        monkeypatch.setenv("GR_HOST_COMPACT", compact)
+        host = GridrogueBatch(n, tier, seed, "symbolic", 10)
+        dev = GridrogueBatch(n, tier, seed, "symbolic", 10)
+        W = host.obs.shape[1]
+        obs = np.full((n, W), -7.5, np.float32)            # garbage the transfer must overwrite
+        P = lambda a: ctypes.c_void_p(a.ctypes.data)
+        rew = np.zeros(n, np.float32); done = np.zeros(n, np.uint8)
+        newly = np.zeros((n, host.n_achievements), np.uint8)
+        tm = np.zeros(n, np.uint32); fl = np.zeros(n, np.uint8)
+        check(lib().gr_reset_host(host.h, P(obs)))
+        assert np.array_equal(obs.view(np.uint32), dev.reset().cpu().numpy().view(np.uint32))
+        for k in range(40):
+            a = dev.random_actions(seed, k).cpu().numpy()
+            check(lib().gr_step_host(host.h, P(a), P(obs), P(rew), P(done), P(newly), P(tm), P(fl)))
+            o2, r2, d2, *_ = dev.step(torch.from_numpy(a).cuda())
+            assert np.array_equal(obs.view(np.uint32), o2.cpu().numpy().view(np.uint32)), f"obs step {k}"
+            assert np.array_equal(rew, r2.cpu().numpy()) and np.array_equal(done, d2.cpu().numpy())
