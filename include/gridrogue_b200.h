@@ -182,6 +182,13 @@ int gr_host_obs_detach(gr_env *env, void *obs_host);
  * changed words, [3] final synchronisation (small outputs, dense obs copy);
  * calls / words: host-path calls and changed words delivered. */
 int gr_host_phase_times(gr_env *env, double out[4], int64_t *calls, int64_t *words);
+/* Copy a device observation buffer of this handle's shape (e.g. what
+ * gr_step_finish wrote on a shard) into a plain host array, every word
+ * written, ordered after the caller's work on `stream`; synchronous.
+ * Symbolic observations travel packed (per-row non-zero bitmap + values,
+ * expanded by host threads) unless GR_HOST_COMPACT=0 -- the transfer behind
+ * gr_step_host's dense path. */
+int gr_obs_to_host(gr_env *env, const void *obs_dev, void *obs_host, void *stream);
 
 
 /* ---- state channel (parity / checkpoint) -------------------------------- *

@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
         "gr_host_obs_attach": (I32, [P, P]),
         "gr_host_obs_detach": (I32, [P, P]),
         "gr_host_phase_times": (I32, [P, P, P, P]),
+        "gr_obs_to_host": (I32, [P, P, P, P]),
         "gr_account_replay": (I32, [P, I64, I64]),
         "gr_export_field": (I32, [P, I32, P]),
         "gr_import_field": (I32, [P, I32, P]),

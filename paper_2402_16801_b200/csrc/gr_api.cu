@@ -1244,7 +1244,7 @@ static void cp_expand_scalar(float* out, int W, int NB, const uint32_t* bm, cons
   }
 }
 
-static int host_obs_compact(gr_env* e, float* out, cudaStream_t st, hclock::time_point t_call) {
+static int host_obs_compact(gr_env* e, const uint32_t* src, float* out, cudaStream_t st, hclock::time_point t_call) {
   const int W = (int)obs_elems_of(e), NB = (W + 31) / 32;
   if (!e->dl_cnt_host) {
     CK(cudaHostAlloc((void**)&e->dl_cnt_host, DL_CHUNKS * sizeof(unsigned long long), cudaHostAllocDefault));
@@ -1279,7 +1279,7 @@ static int host_obs_compact(gr_env* e, float* out, cudaStream_t st, hclock::time
   for (int c = 0; c < C; ++c) {
     const int64_t r0 = e->n * c / C, r1 = e->n * (c + 1) / C;
     const int grid = (int)std::min<int64_t>((r1 - r0 + DL_WARPS - 1) / DL_WARPS, (int64_t)sms * 8);
-    k_obs_pack<<<grid, DL_WARPS * 32, 0, st>>>((const uint32_t*)e->h_obs_dev, r0, r1, W, NB, e->cp_bm_dev,
+    k_obs_pack<<<grid, DL_WARPS * 32, 0, st>>>(src, r0, r1, W, NB, e->cp_bm_dev,
                                                 e->cp_val_dev + r0 * W, e->cp_off_dev, e->dl_cnt_dev + c);
     e->launches += 1;
     CK(cudaGetLastError());
@@ -1300,7 +1300,7 @@ static int host_obs_compact(gr_env* e, float* out, cudaStream_t st, hclock::time
       vofs[c + 1] = dense[c] ? vofs[c] : vofs[c] + k;
       CK(cudaStreamWaitEvent(e->dl_copy, e->dl_ev[c], 0));
       if (dense[c]) {
-        CK(cudaMemcpyAsync(out + r0 * W, (const float*)e->h_obs_dev + r0 * W, (size_t)(r1 - r0) * W * 4,
+        CK(cudaMemcpyAsync(out + r0 * W, (const float*)src + r0 * W, (size_t)(r1 - r0) * W * 4,
                            cudaMemcpyDeviceToHost, e->dl_copy));
       } else {
         CK(cudaMemcpyAsync(e->cp_bm_host + r0 * NB, e->cp_bm_dev + r0 * NB, (size_t)(r1 - r0) * NB * 4,
@@ -1348,7 +1348,7 @@ int gr_reset_host(gr_env* e, void* obs_host) {
   if (HostObs* ho = obs_host ? find_host_obs(e, obs_host) : nullptr)
     return host_obs_deliver(e, *ho, e->h_stream, t_call);
   if (obs_host && ob && e->compact && e->cfg.obs_mode == GR_OBS_SYMBOLIC) {
-    rc = host_obs_compact(e, (float*)obs_host, e->h_stream, t_call);
+    rc = host_obs_compact(e, (const uint32_t*)e->h_obs_dev, (float*)obs_host, e->h_stream, t_call);
     if (rc) return rc;
   } else if (obs_host && ob) {
     CK(cudaMemcpyAsync(obs_host, e->h_obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, e->h_stream));
@@ -1395,7 +1395,7 @@ int gr_step_host(gr_env* e, const int64_t* actions_host, void* obs_host, float* 
     rc = host_obs_deliver(e, *ho, st, t_call);
     if (rc) return rc;
   } else if (obs_host && ob && e->compact && e->cfg.obs_mode == GR_OBS_SYMBOLIC) {
-    rc = host_obs_compact(e, (float*)obs_host, st, t_call);
+    rc = host_obs_compact(e, (const uint32_t*)e->h_obs_dev, (float*)obs_host, st, t_call);
     if (rc) return rc;
   } else {
     if (obs_host && ob) CK(cudaMemcpyAsync(obs_host, e->h_obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, st));
@@ -1403,6 +1403,30 @@ int gr_step_host(gr_env* e, const int64_t* actions_host, void* obs_host, float* 
   }
   const auto t_tail = hclock::now();
   CK(cudaStreamSynchronize(st));
+  e->host_ms[3] += ms_since(t_tail);
+  e->host_calls += 1;
+  return GR_OK;
+}
+
+int gr_obs_to_host(gr_env* e, const void* obs_dev, void* obs_host, void* stream) {
+  if (!e || !obs_dev || !obs_host) return fail(GR_E_INVALID, "null argument");
+  CK(cudaSetDevice(e->cfg.device));
+  int rc = ensure_host_scratch(e);
+  if (rc) return rc;
+  // ordered after the caller's work on `stream` (e.g. the step that wrote obs_dev)
+  CK(cudaEventRecord(e->ev_fork, (cudaStream_t)stream));
+  CK(cudaStreamWaitEvent(e->h_stream, e->ev_fork, 0));
+  const auto t_call = hclock::now();
+  const int64_t ob = obs_elems_of(e) * (e->cfg.obs_mode == GR_OBS_PIXELS ? 1 : 4);
+  if (e->compact && e->cfg.obs_mode == GR_OBS_SYMBOLIC) {
+    rc = host_obs_compact(e, (const uint32_t*)obs_dev, (float*)obs_host, e->h_stream, t_call);
+    if (rc) return rc;
+  } else if (ob) {
+    CK(cudaMemcpyAsync(obs_host, obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, e->h_stream));
+    e->host_ms[0] += ms_since(t_call);
+  }
+  const auto t_tail = hclock::now();
+  CK(cudaStreamSynchronize(e->h_stream));
   e->host_ms[3] += ms_since(t_tail);
   e->host_calls += 1;
   return GR_OK;

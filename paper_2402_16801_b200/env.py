@@ -154,6 +154,16 @@ class GridrogueBatch:
                                    self._stream()))
         return self.obs, self.reward, self.done, self.newly, self.time, self.floor
 
+    def obs_to_host(self, out: np.ndarray) -> np.ndarray:
+        """Copy the current observation buffer into a host numpy array (every
+        word written; symbolic observations travel packed, gr_obs_to_host)."""
+        if self.obs_mode == "none":
+            return out
+        if out.nbytes != self.obs.numel() * self.obs.element_size() or not out.flags.c_contiguous:
+            raise ValueError("obs_to_host needs a C-contiguous array of the observation buffer's size")
+        check(lib().gr_obs_to_host(self.h, _ptr(self.obs), out.ctypes.data_as(ctypes.c_void_p), self._stream()))
+        return out
+
     def observe(self):
         check(lib().gr_observe(self.h, self._obs_ptr(), self._stream()))
         return self.obs

@@ -40,9 +40,15 @@ class ShardedBatch:
                  obs_mode: str = "symbolic", max_episode_length: int | None = None,
                  tile_px: int | None = None, reset_ratio: int = 16, group=None, device=None,
                  graph: bool = False):
+        import os
         import torch
         import torch.distributed as dist
         from .env import GridrogueBatch
+        # ranks of one node share its host cores: the host threads of the
+        # compact / delta observation transfers get an equal share each
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        if local_world > 1:
+            os.environ.setdefault("GR_HOST_THREADS", str(max(1, (os.cpu_count() or 1) // local_world)))
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)

@@ -1099,3 +1099,17 @@ def test_host_step_compact_equals_device_obs(torch_cuda, monkeypatch, tier):
             o2, r2, d2, *_ = dev.step(torch.from_numpy(a).cuda())
             assert np.array_equal(obs.view(np.uint32), o2.cpu().numpy().view(np.uint32)), f"obs step {k}"
             assert np.array_equal(rew, r2.cpu().numpy()) and np.array_equal(done, d2.cpu().numpy())
+
+
+def test_obs_to_host_equals_device_obs(torch_cuda):
+    """GridrogueBatch.obs_to_host (gr_obs_to_host: the compact transfer of any
+    device observation buffer, used by the sharded e2e path) writes exactly the
+    device observation into a numpy array."""
+    from paper_2402_16801_b200 import GridrogueBatch
+    gb = GridrogueBatch(1000, "extended", 4, "symbolic", 8)
+    gb.reset()
+    host = np.full(tuple(gb.obs.shape), 3.25, np.float32)
+    for k in range(20):
+        obs = gb.step(gb.random_actions(4, k))[0]
+        gb.obs_to_host(host)
+        assert np.array_equal(host.view(np.uint32), obs.cpu().numpy().view(np.uint32)), f"step {k}"
