@@ -180,10 +180,11 @@ class HostPool {
     for (auto& t : th_) t.join();
   }
   int size() const { return n_; }
-  // fn(lo, hi) over n_ contiguous parts of [0, count); the caller runs part 0
-  void run(int64_t count, const std::function<void(int64_t, int64_t)>& fn) {
+  // fn(lo, hi) over n_ contiguous parts of [0, count); the caller runs part 0;
+  // below min_parallel items the caller does it all (waking the pool costs more)
+  void run(int64_t count, const std::function<void(int64_t, int64_t)>& fn, int64_t min_parallel = 4096) {
     if (count <= 0) return;
-    if (n_ == 1 || count < 4096) { fn(0, count); return; }
+    if (n_ == 1 || count < min_parallel) { fn(0, count); return; }
     {
       std::lock_guard<std::mutex> g(m_);
       fn_ = &fn;
@@ -286,6 +287,10 @@ struct gr_env {
   int64_t* cp_off_host = nullptr;
   int64_t cp_val_cap = 0;
   bool compact = true;                         // GR_HOST_COMPACT=0: plain 2 GB copy into the host array
+  // pixel frames to plain host arrays: one row per row class
+  PixRowMap prmap{};
+  uint8_t* pr_dev = nullptr;                   // [n][nused][RB] class rows
+  uint8_t* pr_stage[2] = {nullptr, nullptr};   // pinned, one chunk each
   double host_ms[4] = {0, 0, 0, 0};            // enqueue, wait, scatter / decode, tail (gr_host_phase_times)
   int64_t host_calls = 0;
   int64_t host_words = 0;                      // changed words delivered
@@ -412,6 +417,9 @@ void gr_destroy(gr_env* e) {
   if (e->cp_bm_host) cudaFreeHost(e->cp_bm_host);
   if (e->cp_val_host) cudaFreeHost(e->cp_val_host);
   if (e->cp_off_host) cudaFreeHost(e->cp_off_host);
+  if (e->pr_dev) cudaFree(e->pr_dev);
+  for (auto& p : e->pr_stage)
+    if (p) cudaFreeHost(p);
   if (e->dl_cnt_host) cudaFreeHost(e->dl_cnt_host);
   if (e->dl_cnt_dev) cudaFree(e->dl_cnt_dev);
   if (e->dl_copy) cudaStreamDestroy(e->dl_copy);
@@ -473,6 +481,16 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   e->n = cfg->n_envs;
   e->M = std::max<int64_t>(1, (ng + cfg->reset_ratio - 1) / cfg->reset_ratio);
   e->nb = (e->n + 127) / 128;
+  {
+    // below ~32 MB of observations per step the plain copy to a host array is
+    // as quick as packing + waking the host threads (extended symbolic 4,096
+    // envs, 135 MB: 1.95 vs 1.56 M env-steps/s packed vs copied; 16,384:
+    // 3.34 vs 1.66 M; 65,536: 3.89 vs 1.67 M)
+    double min_mb = 32.0;
+    if (const char* mm = getenv("GR_HOST_COMPACT_MIN_MB")) min_mb = atof(mm);
+    const double mb = (double)obs_elems_of(e) * (e->cfg.obs_mode == GR_OBS_PIXELS ? 1 : 4) * e->n / 1048576.0;
+    if (mb < min_mb) e->compact = false;
+  }
   {
     // measured (tools/dev/spec_ab.sh): classic 1,024 envs 19.4 -> 24.3 M
     // env-steps/s, extended 4,096 28.7 -> 31.8 M; extended 16,384 88 ->
@@ -1323,7 +1341,7 @@ static int host_obs_compact(gr_env* e, const uint32_t* src, float* out, cudaStre
         e->hpool->run(r1 - r0, [&](int64_t lo, int64_t hi) {
           if (avx512) cp_expand_avx512(out, W, NB, e->cp_bm_host, vals, e->cp_off_host, r0 + lo, r0 + hi);
           else cp_expand_scalar(out, W, NB, e->cp_bm_host, vals, e->cp_off_host, r0 + lo, r0 + hi);
-        });
+        }, 32);   // rows: a few dozen are worth the pool
         t_dec += ms_since(t0);
         e->host_words += vofs[cc + 1] - vofs[cc];
       }
@@ -1333,6 +1351,8 @@ static int host_obs_compact(gr_env* e, const uint32_t* src, float* out, cudaStre
   e->host_ms[2] += t_dec;
   return GR_OK;
 }
+
+static int host_obs_pixrows(gr_env* e, const uint8_t* src, uint8_t* out, cudaStream_t st, hclock::time_point t_call);
 
 int gr_reset_host(gr_env* e, void* obs_host) {
   if (!e) return fail(GR_E_INVALID, "null env");
@@ -1349,6 +1369,9 @@ int gr_reset_host(gr_env* e, void* obs_host) {
     return host_obs_deliver(e, *ho, e->h_stream, t_call);
   if (obs_host && ob && e->compact && e->cfg.obs_mode == GR_OBS_SYMBOLIC) {
     rc = host_obs_compact(e, (const uint32_t*)e->h_obs_dev, (float*)obs_host, e->h_stream, t_call);
+    if (rc) return rc;
+  } else if (obs_host && ob && e->compact && e->cfg.obs_mode == GR_OBS_PIXELS) {
+    rc = host_obs_pixrows(e, (const uint8_t*)e->h_obs_dev, (uint8_t*)obs_host, e->h_stream, t_call);
     if (rc) return rc;
   } else if (obs_host && ob) {
     CK(cudaMemcpyAsync(obs_host, e->h_obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, e->h_stream));
@@ -1397,6 +1420,9 @@ int gr_step_host(gr_env* e, const int64_t* actions_host, void* obs_host, float* 
   } else if (obs_host && ob && e->compact && e->cfg.obs_mode == GR_OBS_SYMBOLIC) {
     rc = host_obs_compact(e, (const uint32_t*)e->h_obs_dev, (float*)obs_host, st, t_call);
     if (rc) return rc;
+  } else if (obs_host && ob && e->compact && e->cfg.obs_mode == GR_OBS_PIXELS) {
+    rc = host_obs_pixrows(e, (const uint8_t*)e->h_obs_dev, (uint8_t*)obs_host, st, t_call);
+    if (rc) return rc;
   } else {
     if (obs_host && ob) CK(cudaMemcpyAsync(obs_host, e->h_obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, st));
     e->host_ms[0] += ms_since(t_call);
@@ -1405,6 +1431,112 @@ int gr_step_host(gr_env* e, const int64_t* actions_host, void* obs_host, float* 
   CK(cudaStreamSynchronize(st));
   e->host_ms[3] += ms_since(t_tail);
   e->host_calls += 1;
+  return GR_OK;
+}
+
+// pixel frames into a plain host array: per row chunk, gather each frame's
+// class rows on the device (~28 % of the frame bytes), copy them, and let
+// host threads replicate them into the frames while the next chunk moves.
+// frames [r0 + lo, r0 + hi) from their class rows: the frame written front to
+// back in 64-byte streaming stores, each a 64-byte load from its row's class
+// row (or two, blended, across a frame-row boundary); bytes before the first
+// 64-byte aligned address and after the last one go by byte
+__attribute__((target("avx512f,avx512bw"))) static void pix_expand_avx512(uint8_t* out, const PixRowMap& m,
+                                                                            const uint8_t* stage, size_t per_env,
+                                                                            int64_t r0, int64_t lo, int64_t hi) {
+  const int RB = m.RB, FB = m.FB;
+  for (int64_t r = lo; r < hi; ++r) {
+    uint8_t* f = out + (r0 + r) * (int64_t)FB;
+    const uint8_t* rows = stage + r * per_env;
+    auto byte_at = [&](int b) -> uint8_t {
+      const int y = b / RB;
+      return rows[(size_t)m.slot_of_row[y] * RB + (b - y * RB)];
+    };
+    int b = (int)((64 - ((uintptr_t)f & 63)) & 63);
+    if (b > FB) b = FB;
+    for (int q = 0; q < b; ++q) f[q] = byte_at(q);
+    int y = b / RB, o = b - y * RB;
+    for (; b + 64 <= FB; b += 64) {
+      const uint8_t* ra = rows + (size_t)m.slot_of_row[y] * RB + o;
+      __m512i v = _mm512_loadu_si512(ra);
+      const int n = RB - o;   // bytes of this block still in row y
+      if (n < 64) {
+        const uint8_t* rb = rows + (size_t)m.slot_of_row[y + 1] * RB - n;
+        v = _mm512_mask_blend_epi8((__mmask64)(~0ull << n), v, _mm512_loadu_si512(rb));
+      }
+      _mm512_stream_si512((__m512i*)(f + b), v);
+      o += 64;
+      while (o >= RB) { o -= RB; ++y; }
+    }
+    for (int q = b; q < FB; ++q) f[q] = byte_at(q);
+  }
+  _mm_sfence();
+}
+
+static int host_obs_pixrows(gr_env* e, const uint8_t* src, uint8_t* out, cudaStream_t st, hclock::time_point t_call) {
+  static const bool avx512 = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw");
+  if (!e->dl_cnt_host) {
+    CK(cudaHostAlloc((void**)&e->dl_cnt_host, DL_CHUNKS * sizeof(unsigned long long), cudaHostAllocDefault));
+    CK(cudaMalloc((void**)&e->dl_cnt_dev, DL_CHUNKS * sizeof(unsigned long long)));
+    CK(cudaStreamCreateWithFlags(&e->dl_copy, cudaStreamNonBlocking));
+    for (auto& ev : e->dl_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    for (auto& ev : e->dl_evd) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->hpool.reset(new HostPool(host_threads()));
+  }
+  const int C = (int)std::min<int64_t>(DL_CHUNKS, std::max<int64_t>(1, e->n / 256));
+  const PixRowMap& m = e->prmap;
+  const size_t per_env = (size_t)m.nused * m.RB;
+  if (!e->pr_dev) {
+    if (pixel_row_map(e->ext, e->cfg.tile_px, &e->prmap)) return fail(GR_E_INVALID, "no row map for this tile size");
+    const size_t pe = (size_t)e->prmap.nused * e->prmap.RB;
+    CK(cudaMalloc((void**)&e->pr_dev, pe * e->n));
+    const int64_t rows_max = (e->n + C - 1) / C;
+    // 64 bytes of slack at both ends: the expansion's 64-byte loads may run past a chunk's rows
+    for (auto& p : e->pr_stage) CK(cudaHostAlloc((void**)&p, pe * rows_max + 128, cudaHostAllocDefault));
+    return host_obs_pixrows(e, src, out, st, t_call);
+  }
+  double t_wait = 0, t_dec = 0;
+  for (int c = 0; c < C; ++c) {
+    const int64_t r0 = e->n * c / C, r1 = e->n * (c + 1) / C;
+    launch_pix_gather(src, r0, r1, m, e->pr_dev + r0 * per_env, st);
+    e->launches += 1;
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e->dl_ev[c], st));
+  }
+  e->host_ms[0] += ms_since(t_call);
+  for (int c = 0; c <= C; ++c) {
+    if (c < C) {   // chunk c's rows into stage c % 2 (chunk c - 2 was expanded last iteration)
+      const int64_t r0 = e->n * c / C, r1 = e->n * (c + 1) / C;
+      CK(cudaStreamWaitEvent(e->dl_copy, e->dl_ev[c], 0));
+      CK(cudaMemcpyAsync(e->pr_stage[c & 1] + 64, e->pr_dev + r0 * per_env, (size_t)(r1 - r0) * per_env,
+                         cudaMemcpyDeviceToHost, e->dl_copy));
+      CK(cudaEventRecord(e->dl_evd[c], e->dl_copy));
+    }
+    if (c > 0) {
+      const int cc = c - 1;
+      const int64_t r0 = e->n * cc / C, r1 = e->n * (cc + 1) / C;
+      auto t0 = hclock::now();
+      CK(cudaEventSynchronize(e->dl_evd[cc]));
+      t_wait += ms_since(t0);
+      t0 = hclock::now();
+      const uint8_t* stage = e->pr_stage[cc & 1] + 64;
+      e->hpool->run(r1 - r0, [&](int64_t lo, int64_t hi) {
+        if (avx512) {
+          pix_expand_avx512(out, m, stage, per_env, r0, lo, hi);
+          return;
+        }
+        for (int64_t r = lo; r < hi; ++r) {
+          uint8_t* f = out + (r0 + r) * (int64_t)m.FB;
+          const uint8_t* rows = stage + r * per_env;
+          for (int y = 0; y < m.FH; ++y) memcpy(f + (size_t)y * m.RB, rows + (size_t)m.slot_of_row[y] * m.RB, m.RB);
+        }
+      }, 32);
+      t_dec += ms_since(t0);
+      e->host_words += (r1 - r0) * (int64_t)per_env / 4;
+    }
+  }
+  e->host_ms[1] += t_wait;
+  e->host_ms[2] += t_dec;
   return GR_OK;
 }
 
@@ -1420,6 +1552,9 @@ int gr_obs_to_host(gr_env* e, const void* obs_dev, void* obs_host, void* stream)
   const int64_t ob = obs_elems_of(e) * (e->cfg.obs_mode == GR_OBS_PIXELS ? 1 : 4);
   if (e->compact && e->cfg.obs_mode == GR_OBS_SYMBOLIC) {
     rc = host_obs_compact(e, (const uint32_t*)obs_dev, (float*)obs_host, e->h_stream, t_call);
+    if (rc) return rc;
+  } else if (e->compact && e->cfg.obs_mode == GR_OBS_PIXELS) {
+    rc = host_obs_pixrows(e, (const uint8_t*)obs_dev, (uint8_t*)obs_host, e->h_stream, t_call);
     if (rc) return rc;
   } else if (ob) {
     CK(cudaMemcpyAsync(obs_host, obs_dev, (size_t)ob * e->n, cudaMemcpyDeviceToHost, e->h_stream));

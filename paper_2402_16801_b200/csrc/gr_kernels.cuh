@@ -147,5 +147,15 @@ void launch_install(bool ext, const DS& S, const InstallArgs& a, int64_t grid_en
 void launch_pixprep(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st);
 void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st);
 void launch_pixels(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st);
+// the row-class structure of a pixel frame (gr_obs.cu): row y of a frame is
+// the class row in slot slot_of_row[y]; rep[k] is a row of slot k's class
+struct PixRowMap {
+  int FH, RB, FB, nused;
+  int16_t slot_of_row[176];
+  int16_t rep[64];
+};
+int pixel_row_map(bool ext, int px, PixRowMap* m);
+void launch_pix_gather(const uint8_t* frames, int64_t r0, int64_t r1, const PixRowMap& m, uint8_t* out,
+                       cudaStream_t st);
 
 }  // namespace gr

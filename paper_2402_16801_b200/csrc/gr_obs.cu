@@ -122,7 +122,7 @@ __device__ __forceinline__ uint32_t pat_word(const uint32_t* w, int off) {
 // without the side-panel gear bar; in the bottom strip, each vital bar and
 // the blank rows.  Rows of one class are byte-identical.
 template <bool EXT, int PX>
-__device__ __forceinline__ int row_class(int y) {
+__host__ __device__ __forceinline__ int row_class(int y) {
   using G = PG<EXT, PX>;
   if (y < G::Y0) {
     const int R = y / PX, iy = y % PX;
@@ -839,6 +839,64 @@ void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
     const int grid = (int)std::min<int64_t>((a.n + NW - 1) / NW, (int64_t)sms * 4);
     k_symbolic_stage<false><<<grid, NW * 32, smem, st>>>(S, a);
   }
+}
+
+// ---- pixel frames to the host, packed by row class ------------------------
+// Rows of one class are byte-identical in every frame (k_pixels only ever
+// renders the class rows), so a frame is determined by its class rows: the
+// transfer to a host array moves one representative row per class present
+// (~12 KB of a 42.9 KB extended 10 px frame) and host threads replicate them.
+template <bool EXT, int PX>
+static void row_map_px(PixRowMap* m) {
+  using G = PG<EXT, PX>;
+  m->FH = G::FH;
+  m->RB = G::RB;
+  m->FB = G::FB;
+  int slot[64];
+  for (int c = 0; c < 64; ++c) slot[c] = -1;
+  m->nused = 0;
+  for (int y = 0; y < G::FH; ++y) {
+    const int c = row_class<EXT, PX>(y);
+    if (slot[c] < 0) {
+      slot[c] = m->nused;
+      m->rep[m->nused++] = (int16_t)y;
+    }
+    m->slot_of_row[y] = (int16_t)slot[c];
+  }
+}
+
+int pixel_row_map(bool ext, int px, PixRowMap* m) {
+  switch ((ext ? 100 : 0) + px) {
+    case 7: row_map_px<false, 7>(m); return 0;
+    case 10: row_map_px<false, 10>(m); return 0;
+    case 16: row_map_px<false, 16>(m); return 0;
+    case 107: row_map_px<true, 7>(m); return 0;
+    case 110: row_map_px<true, 10>(m); return 0;
+    case 116: row_map_px<true, 16>(m); return 0;
+    default: return -1;
+  }
+}
+
+// one CTA per env: the representative rows of frames [r0, r1) -> out[env - r0][slot][RB]
+__global__ void __launch_bounds__(256) k_pix_gather(const uint8_t* __restrict__ frames, int64_t r0, int64_t r1, int FB,
+                                                     int RB, int nused, PixRowMap map, uint8_t* __restrict__ out) {
+  for (int64_t r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+    const uint8_t* f = frames + r * (int64_t)FB;
+    uint8_t* o = out + (r - r0) * (int64_t)nused * RB;   // out is this chunk's region
+    for (int q = threadIdx.x; q < nused * RB; q += blockDim.x) {
+      const int k = q / RB, b = q - k * RB;
+      o[q] = __ldcg(f + map.rep[k] * RB + b);
+    }
+  }
+}
+
+void launch_pix_gather(const uint8_t* frames, int64_t r0, int64_t r1, const PixRowMap& m, uint8_t* out,
+                       cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>(r1 - r0, (int64_t)sms * 8);
+  if (grid > 0) k_pix_gather<<<grid, 256, 0, st>>>(frames, r0, r1, m.FB, m.RB, m.nused, m, out);
 }
 
 void launch_pixels(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {

@@ -1081,6 +1081,7 @@ def test_host_step_compact_equals_device_obs(torch_cuda, monkeypatch, tier):
     from paper_2402_16801_b200._lib import check, lib
     torch = torch_cuda
     n, seed = 1536, 3
+    monkeypatch.setenv("GR_HOST_COMPACT_MIN_MB", "0")   # the compact path at any size
     for compact in ("1", "0"):
         monkeypatch.setenv("GR_HOST_COMPACT", compact)
         host = GridrogueBatch(n, tier, seed, "symbolic", 10)
@@ -1101,11 +1102,12 @@ def test_host_step_compact_equals_device_obs(torch_cuda, monkeypatch, tier):
             assert np.array_equal(rew, r2.cpu().numpy()) and np.array_equal(done, d2.cpu().numpy())
 
 
-def test_obs_to_host_equals_device_obs(torch_cuda):
+def test_obs_to_host_equals_device_obs(torch_cuda, monkeypatch):
     """GridrogueBatch.obs_to_host (gr_obs_to_host: the compact transfer of any
     device observation buffer, used by the sharded e2e path) writes exactly the
     device observation into a numpy array."""
     from paper_2402_16801_b200 import GridrogueBatch
+    monkeypatch.setenv("GR_HOST_COMPACT_MIN_MB", "0")
     gb = GridrogueBatch(1000, "extended", 4, "symbolic", 8)
     gb.reset()
     host = np.full(tuple(gb.obs.shape), 3.25, np.float32)
@@ -1113,3 +1115,23 @@ def test_obs_to_host_equals_device_obs(torch_cuda):
         obs = gb.step(gb.random_actions(4, k))[0]
         gb.obs_to_host(host)
         assert np.array_equal(host.view(np.uint32), obs.cpu().numpy().view(np.uint32)), f"step {k}"
+
+
+@pytest.mark.parametrize("tier,px", [("extended", 10), ("classic", 7), ("extended", 16)])
+def test_host_pixels_row_classes_equal_device_frames(torch_cuda, monkeypatch, tier, px):
+    """Pixel frames into a plain numpy array through the class-row transfer
+    (one row per row class gathered on the device, replicated by host threads)
+    equal the device frames byte for byte, every step, under reset stress."""
+    from paper_2402_16801_b200 import GridrogueBatch
+    torch = torch_cuda
+    monkeypatch.setenv("GR_HOST_COMPACT_MIN_MB", "0")
+    n, seed = 600, 6
+    host = GridrogueBatch(n, tier, seed, "pixels", 10, tile_px=px)
+    dev = GridrogueBatch(n, tier, seed, "pixels", 10, tile_px=px)
+    out = np.full(tuple(host.obs.shape), 77, np.uint8)
+    host.reset()
+    assert np.array_equal(host.obs_to_host(out), dev.reset().cpu().numpy())
+    for k in range(25):
+        host.step(host.random_actions(seed, k))
+        o2 = dev.step(dev.random_actions(seed, k))[0]
+        assert np.array_equal(host.obs_to_host(out), o2.cpu().numpy()), f"step {k}"
