@@ -482,11 +482,12 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   e->M = std::max<int64_t>(1, (ng + cfg->reset_ratio - 1) / cfg->reset_ratio);
   e->nb = (e->n + 127) / 128;
   {
-    // below ~32 MB of observations per step the plain copy to a host array is
-    // as quick as packing + waking the host threads (extended symbolic 4,096
-    // envs, 135 MB: 1.95 vs 1.56 M env-steps/s packed vs copied; 16,384:
-    // 3.34 vs 1.66 M; 65,536: 3.89 vs 1.67 M)
-    double min_mb = 32.0;
+    // below ~40 MB of observations per step the plain copy to a host array is
+    // as quick as packing + waking the host threads (extended symbolic 1,024
+    // envs, 34 MB: 1.14 vs 1.33 M env-steps/s packed vs copied; classic 8,192
+    // envs, 44 MB: 10.3 vs 8.7 M; extended 4,096 / 16,384 / 65,536: 1.95 /
+    // 3.34 / 3.89 vs 1.56 / 1.66 / 1.67 M)
+    double min_mb = 40.0;
     if (const char* mm = getenv("GR_HOST_COMPACT_MIN_MB")) min_mb = atof(mm);
     const double mb = (double)obs_elems_of(e) * (e->cfg.obs_mode == GR_OBS_PIXELS ? 1 : 4) * e->n / 1048576.0;
     if (mb < min_mb) e->compact = false;
