@@ -101,11 +101,32 @@ class ShardedBatch:
         b = self.batch
         return b.obs, b.reward, b.done, b.newly, b.time, b.floor
 
+    def _collective_capturable(self) -> bool:
+        """Whether this process group's all-gather can be captured in a CUDA
+        graph here (probed on scratch tensors, so a failure touches no state)."""
+        import torch
+        try:
+            src = torch.zeros(4, dtype=torch.int32, device=self.batch.device)
+            dst = torch.zeros(4 * self.world, dtype=torch.int32, device=self.batch.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.dist.all_gather_into_tensor(dst, src, group=self.group)
+            g.replay()
+            torch.cuda.synchronize(self.batch.device)
+            return True
+        except Exception as ex:   # keep stepping eagerly rather than fail the run
+            import warnings
+            warnings.warn(f"ShardedBatch: collective not capturable here ({ex}); stepping without a graph")
+            return False
+
     def _capture_and_run(self, a):
         """Capture local step + all-gather + finish once, then replay.  The
         library's host-side bookkeeping advanced once during the capture; that
         advance stands for the first replay, issued right after."""
         import torch
+        if not self._collective_capturable():
+            self.graph = False
+            return self._step_eager(a)
         l0 = self.batch.kernel_launches()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
