@@ -40,6 +40,43 @@ int grp_sample_actions(const void* logits, const void* values, int32_t bf16, int
                        const float* prev_reward, const uint8_t* prev_done, float* reward_out, float* done_out,
                        void* stream);
 
+
+/* grp_ppo_loss over bf16 logits / values with row strides, the gradients
+ * written as bf16 (what the head GEMMs of a bf16 learner consume): d loss /
+ * d logits into dlogits[row * ld_dlogits + j] for j < n_actions and zeros for
+ * n_actions <= j < n_pad (a head padded to n_pad outputs), d loss / d value
+ * into dvalues[row * ld_dvalues].  out[4] as for grp_ppo_loss.
+ * Returns 0, -1 (unsupported n_actions, batch <= 0, n_pad < n_actions), -2. */
+int grp_ppo_loss_bf16(const void* logits, int64_t ld_logits, const void* values, int64_t ld_values,
+                      const int64_t* actions, const float* logp_old, const float* advantages,
+                      const float* values_old, const float* returns, int32_t batch, int32_t n_actions,
+                      float clip_eps, float vf_coef, float ent_coef, void* dlogits, int64_t ld_dlogits,
+                      int32_t n_pad, void* dvalues, int64_t ld_dvalues, float* out, void* stream);
+
+/* One layer of the learner's hand-written backward (bf16 activations /
+ * gradients, row-major): with dy[i, j] = dy_a[i * ld_a + j] for j < split and
+ * dy_b[i * ld_b + j - split] otherwise,
+ *   y != NULL: dz[i * cols + j] = bf16(dy[i, j] * (1 - y[i * ld_y + j]^2))   (tanh backward)
+ *   db[j] = sum over rows of dz[i, j] (or of dy when y == NULL), fp32.
+ * work: float[row_chunks * cols]; counters: unsigned[ceil(cols / 64)], zero
+ * before the first call (each call leaves them zero).  The sum order is
+ * fixed by row_chunks: results are deterministic.  0, -1 (bad arguments), -2. */
+int grp_bias_grad(const void* y, int64_t ld_y, const void* dy_a, int64_t ld_a, const void* dy_b, int64_t ld_b,
+                  int32_t split, int32_t rows, int32_t cols, void* dz, float* db, float* work,
+                  int32_t row_chunks, unsigned* counters, void* stream);
+
+/* torch.nn.utils.clip_grad_norm_(max_norm) of grads * grad_scale, then one
+ * torch.optim.Adam step (no weight decay; *lr and *step live on the device,
+ * *step is incremented) over n flat fp32 parameters, and params_bf16 = bf16
+ * (params) for the next forward.  grads are not modified.  work:
+ * float[4 + 296] (work[0..3] = gradient multiplier, step size, sqrt of the
+ * second bias correction, pre-clip norm); counter: one unsigned, zero before
+ * the first call.  fp32 buffers 16-byte aligned, params_bf16 8-byte aligned.
+ * Two launches on `stream`.  0, -1 (bad arguments), -2. */
+int grp_clip_adam(float* params, const float* grads, float* exp_avg, float* exp_avg_sq, void* params_bf16,
+                  int64_t n, const float* lr, float* step, float beta1, float beta2, float eps, float grad_scale,
+                  float max_norm, float* work, unsigned* counter, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -38,15 +38,26 @@ __device__ __forceinline__ float warp_max(float x) {
   return x;
 }
 
-template <int NA>
-__global__ void __launch_bounds__(THREADS) k_ppo_loss(const float* __restrict__ logits, const float* __restrict__ v,
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <typename T> __device__ __forceinline__ T from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16(x); }
+
+// logits / values of type TI with row strides ldl / ldv; gradients of type TO
+// (bf16: what the head's GEMMs consume) with row stride ldd, the columns
+// [NA, npad) of each gradient row written as zeros (a padded head)
+template <int NA, typename TI, typename TO>
+__global__ void __launch_bounds__(THREADS) k_ppo_loss(const TI* __restrict__ logits, int64_t ldl,
+                                                      const TI* __restrict__ v, int64_t ldv,
                                                       const int64_t* __restrict__ act,
                                                       const float* __restrict__ logp_old,
                                                       const float* __restrict__ adv,
                                                       const float* __restrict__ v_old,
                                                       const float* __restrict__ ret, int B, float clip_eps,
-                                                      float vf_coef, float ent_coef, float* __restrict__ dlogits,
-                                                      float* __restrict__ dv, float* __restrict__ out) {
+                                                      float vf_coef, float ent_coef, TO* __restrict__ dlogits,
+                                                      int64_t ldd, int npad, TO* __restrict__ dv, int64_t lddv,
+                                                      float* __restrict__ out) {
   constexpr int PER = (NA + 31) / 32;
   __shared__ float red[2][THREADS / 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -78,13 +89,13 @@ __global__ void __launch_bounds__(THREADS) k_ppo_loss(const float* __restrict__ 
   float acc_pg = 0.f, acc_vl = 0.f, acc_h = 0.f;
   const int nw = gridDim.x * (THREADS / 32);
   for (int row = blockIdx.x * (THREADS / 32) + warp; row < B; row += nw) {
-    const float* z = logits + (size_t)row * NA;
+    const TI* z = logits + (size_t)row * ldl;
     float zl[PER];
     float m = -INFINITY;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       const int j = lane + 32 * k;
-      zl[k] = j < NA ? z[j] : -INFINITY;
+      zl[k] = j < NA ? to_f(z[j]) : -INFINITY;
       m = fmaxf(m, zl[k]);
     }
     m = warp_max(m);
@@ -124,7 +135,7 @@ __global__ void __launch_bounds__(THREADS) k_ppo_loss(const float* __restrict__ 
     else g_logp = (r > 1.f - clip_eps && r < 1.f + clip_eps) ? -an * r : 0.f;
     g_logp *= invB;
     // value loss
-    const float vv = v[row], vo = v_old[row], R = ret[row];
+    const float vv = to_f(v[(size_t)row * ldv]), vo = v_old[row], R = ret[row];
     const float dvu = vv - vo;
     const float vc = vo + fminf(fmaxf(dvu, -clip_eps), clip_eps);
     const float e1 = (vv - R) * (vv - R), e2 = (vc - R) * (vc - R);
@@ -132,17 +143,18 @@ __global__ void __launch_bounds__(THREADS) k_ppo_loss(const float* __restrict__ 
     float g_v = e1 >= e2 ? (vv - R) : ((dvu > -clip_eps && dvu < clip_eps) ? (vc - R) : 0.f);
     g_v *= vf_coef * invB;
     // d loss / d z_j = g_logp (1[j==a] - p_j) + c_e/B p_j (log p_j + H)
-    float* dz = dlogits + (size_t)row * NA;
+    TO* dz = dlogits + (size_t)row * ldd;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       const int j = lane + 32 * k;
       if (j < NA) {
         const float lp = zl[k] - lse, p = expf(lp);
-        dz[j] = g_logp * ((j == a ? 1.f : 0.f) - p) + ent_coef * invB * p * (lp + h);
+        dz[j] = from_f<TO>(g_logp * ((j == a ? 1.f : 0.f) - p) + ent_coef * invB * p * (lp + h));
       }
     }
+    for (int j = NA + lane; j < npad; j += 32) dz[j] = from_f<TO>(0.f);
     if (lane == 0) {
-      dv[row] = g_v;
+      dv[(size_t)row * lddv] = from_f<TO>(g_v);
       acc_pg += pg;
       acc_vl += vl;
       acc_h += h;
@@ -256,6 +268,183 @@ __global__ void __launch_bounds__(THREADS) k_sample(const TI* __restrict__ logit
   }
 }
 
+
+// ------------------------------------------------------ hand-written backward
+// One layer's bias gradient, and for a tanh layer the activation's backward,
+// in one pass over the layer's [rows, cols] output gradient:
+//   dy[i, j] = j < split ? dy_a[i * ld_a + j] : dy_b[i * ld_b + j - split]
+//   dz[i, j] = bf16(dy[i, j] * (1 - y[i, j]^2))        (y: the tanh output; y == null: dz = dy)
+//   db[j]    = sum_i dz[i, j]                            (fp32, a fixed summation order)
+// The two dy halves are the actor's and the critic's gradients of the shared
+// first layer.  CTA (x, r) sums rows [r * rows / RCH, (r + 1) * rows / RCH)
+// of a 64-column tile into work[r * cols + j]; the tile's last CTA (counter)
+// adds the RCH partials in order, so the result is deterministic.
+constexpr int BG_COLS = 64, BG_THREADS = 256, BG_TR = BG_THREADS / 8;   // 8 columns per thread, 32 row lanes
+
+template <bool VEC>
+__global__ void __launch_bounds__(BG_THREADS) k_bias_grad(const __nv_bfloat16* __restrict__ y, int64_t ldy,
+                                                          const __nv_bfloat16* __restrict__ dya, int64_t lda,
+                                                          const __nv_bfloat16* __restrict__ dyb, int64_t ldb,
+                                                          int split, int rows, int cols,
+                                                          __nv_bfloat16* __restrict__ dz, float* __restrict__ db,
+                                                          float* __restrict__ work, unsigned* __restrict__ counters) {
+  __shared__ float red[BG_TR][BG_COLS + 1];
+  __shared__ bool last;
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int c0 = blockIdx.x * BG_COLS + tx * 8;
+  const int RCH = gridDim.y;
+  const int r0 = (int)((int64_t)rows * blockIdx.y / RCH), r1 = (int)((int64_t)rows * (blockIdx.y + 1) / RCH);
+  float acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+  for (int i = r0 + ty; i < r1; i += BG_TR) {
+    if (VEC) {   // cols, split, leading dimensions and pointers 16-byte aligned
+      if (c0 >= cols) break;
+      const __nv_bfloat16* src = c0 < split ? dya + (size_t)i * lda + c0 : dyb + (size_t)i * ldb + (c0 - split);
+      uint4 g = *reinterpret_cast<const uint4*>(src);
+      __nv_bfloat16* gv = reinterpret_cast<__nv_bfloat16*>(&g);
+      if (y) {
+        uint4 yy = *reinterpret_cast<const uint4*>(y + (size_t)i * ldy + c0);
+        const __nv_bfloat16* yv = reinterpret_cast<const __nv_bfloat16*>(&yy);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float t = __bfloat162float(yv[q]);
+          gv[q] = __float2bfloat16(__bfloat162float(gv[q]) * (1.f - t * t));
+        }
+        *reinterpret_cast<uint4*>(dz + (size_t)i * cols + c0) = g;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] += __bfloat162float(gv[q]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int c = c0 + q;
+        if (c >= cols) break;
+        float g = __bfloat162float(c < split ? dya[(size_t)i * lda + c] : dyb[(size_t)i * ldb + (c - split)]);
+        if (y) {
+          const float t = __bfloat162float(y[(size_t)i * ldy + c]);
+          const __nv_bfloat16 gz = __float2bfloat16(g * (1.f - t * t));
+          dz[(size_t)i * cols + c] = gz;
+          g = __bfloat162float(gz);
+        }
+        acc[q] += g;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) red[ty][tx * 8 + q] = acc[q];
+  __syncthreads();
+  if (threadIdx.x < BG_COLS) {
+    float s = 0.f;
+    for (int r = 0; r < BG_TR; ++r) s += red[r][threadIdx.x];
+    const int c = blockIdx.x * BG_COLS + threadIdx.x;
+    if (c < cols) work[(size_t)blockIdx.y * cols + c] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&counters[blockIdx.x], 1u) == (unsigned)RCH - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < BG_COLS) {
+    const int c = blockIdx.x * BG_COLS + threadIdx.x;
+    if (c < cols) {
+      float s = 0.f;
+      for (int r = 0; r < RCH; ++r) s += __ldcg(work + (size_t)r * cols + c);
+      db[c] = s;
+    }
+  }
+  if (threadIdx.x == 0) counters[blockIdx.x] = 0;   // ready for the next launch (graph replays)
+}
+
+// ------------------------------------------------ global-norm clip + Adam
+// torch.nn.utils.clip_grad_norm_ followed by torch.optim.Adam (capturable,
+// no weight decay, no amsgrad) over one flat fp32 parameter buffer, in two
+// launches: k_sumsq (a fixed grid of partial sums of g^2; its last CTA forms
+// the clip factor, increments the step and the bias corrections into
+// `coef`), then k_adam (m, v, p, and the bf16 copy of p the next forward
+// reads).  The gradients themselves are not modified.
+constexpr int AD_THREADS = 256, SQ_CTAS = 296;
+
+__global__ void __launch_bounds__(AD_THREADS) k_sumsq(const float* __restrict__ g, int64_t n, float grad_scale,
+                                                      float max_norm, const float* __restrict__ lr, float* step,
+                                                      float beta1, float beta2, float* __restrict__ partial,
+                                                      unsigned* __restrict__ counter, float* __restrict__ coef) {
+  __shared__ float red[AD_THREADS / 32];
+  __shared__ bool last;
+  float s = 0.f;
+  const int64_t n4 = n / 4;
+  for (int64_t k = (int64_t)blockIdx.x * AD_THREADS + threadIdx.x; k < n4; k += (int64_t)gridDim.x * AD_THREADS) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(g) + k);
+    s += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t k = n4 * 4 + threadIdx.x; k < n; k += AD_THREADS) s += g[k] * g[k];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < AD_THREADS / 32; ++w) t += red[w];
+    partial[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double tot = 0.0;
+  for (unsigned b = 0; b < gridDim.x; ++b) tot += (double)__ldcg(partial + b);
+  const float norm = grad_scale * sqrtf((float)tot);
+  const float clip = fminf(max_norm / (norm + 1e-6f), 1.f);
+  const float st = *step + 1.f;
+  *step = st;
+  const float bc1 = 1.f - powf(beta1, st), bc2 = 1.f - powf(beta2, st);
+  coef[0] = grad_scale * clip;    // gradient multiplier
+  coef[1] = *lr / bc1;            // step size
+  coef[2] = sqrtf(bc2);
+  coef[3] = norm;                 // the pre-clip global norm (stats)
+  *counter = 0;
+}
+
+__global__ void __launch_bounds__(AD_THREADS) k_adam(float* __restrict__ p, const float* __restrict__ g,
+                                                     float* __restrict__ m, float* __restrict__ v,
+                                                     __nv_bfloat16* __restrict__ pb, int64_t n,
+                                                     const float* __restrict__ coef, float beta1, float beta2,
+                                                     float eps) {
+  const float gs = coef[0], step_size = coef[1], bc2s = coef[2];
+  auto one = [&](float& pp, float gg, float& mm, float& vv) {
+    gg *= gs;
+    mm = beta1 * mm + (1.f - beta1) * gg;
+    vv = beta2 * vv + (1.f - beta2) * gg * gg;
+    const float denom = sqrtf(vv) / bc2s + eps;
+    pp -= step_size * (mm / denom);
+  };
+  const int64_t n4 = n / 4;
+  for (int64_t k = (int64_t)blockIdx.x * AD_THREADS + threadIdx.x; k < n4; k += (int64_t)gridDim.x * AD_THREADS) {
+    float4 pp = reinterpret_cast<float4*>(p)[k], mm = reinterpret_cast<float4*>(m)[k],
+           vv = reinterpret_cast<float4*>(v)[k];
+    const float4 gg = __ldg(reinterpret_cast<const float4*>(g) + k);
+    one(pp.x, gg.x, mm.x, vv.x);
+    one(pp.y, gg.y, mm.y, vv.y);
+    one(pp.z, gg.z, mm.z, vv.z);
+    one(pp.w, gg.w, mm.w, vv.w);
+    reinterpret_cast<float4*>(p)[k] = pp;
+    reinterpret_cast<float4*>(m)[k] = mm;
+    reinterpret_cast<float4*>(v)[k] = vv;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(pp.x, pp.y), hi = __floats2bfloat162_rn(pp.z, pp.w);
+    uint2 packed;
+    packed.x = *reinterpret_cast<uint32_t*>(&lo);
+    packed.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(pb)[k] = packed;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t k = n4 * 4 + threadIdx.x; k < n; k += AD_THREADS) {
+      one(p[k], g[k], m[k], v[k]);
+      pb[k] = __float2bfloat16(p[k]);
+    }
+}
+
 }  // namespace
 
 extern "C" int grp_ppo_loss(const float* logits, const float* v, const int64_t* actions, const float* logp_old,
@@ -271,8 +460,9 @@ extern "C" int grp_ppo_loss(const float* logits, const float* v, const int64_t* 
   const int grid = (int)std::min<int64_t>((batch + rows_per_cta - 1) / rows_per_cta, (int64_t)sms * 4);
 #define GRP_CASE(N)                                                                                          \
   case N:                                                                                                    \
-    k_ppo_loss<N><<<grid, THREADS, 0, st>>>(logits, v, actions, logp_old, adv, v_old, ret, batch, clip_eps, \
-                                           vf_coef, ent_coef, dlogits, dv, out);                            \
+    k_ppo_loss<N, float, float><<<grid, THREADS, 0, st>>>(logits, N, v, 1, actions, logp_old, adv, v_old, ret, \
+                                                         batch, clip_eps, vf_coef, ent_coef, dlogits, N, N, dv, 1,  \
+                                                         out);                                                    \
     break;
   switch (n_actions) {
     GRP_CASE(17)
@@ -310,5 +500,74 @@ extern "C" int grp_sample_actions(const void* logits, const void* values, int32_
       return -1;
   }
 #undef GRS_CASE
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+extern "C" int grp_ppo_loss_bf16(const void* logits, int64_t ld_logits, const void* values, int64_t ld_values,
+                                 const int64_t* actions, const float* logp_old, const float* adv,
+                                 const float* v_old, const float* ret, int32_t batch, int32_t n_actions,
+                                 float clip_eps, float vf_coef, float ent_coef, void* dlogits, int64_t ld_dlogits,
+                                 int32_t n_pad, void* dvalues, int64_t ld_dvalues, float* out, void* stream) {
+  if (batch <= 0 || n_pad < n_actions || ld_dlogits < n_pad) return -1;
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int rows_per_cta = THREADS / 32;
+  const int grid = (int)std::min<int64_t>((batch + rows_per_cta - 1) / rows_per_cta, (int64_t)sms * 4);
+  using B16 = __nv_bfloat16;
+#define GRB_CASE(N)                                                                                       \
+  case N:                                                                                                 \
+    k_ppo_loss<N, B16, B16><<<grid, THREADS, 0, st>>>(                                                    \
+        (const B16*)logits, ld_logits, (const B16*)values, ld_values, actions, logp_old, adv, v_old, ret, \
+        batch, clip_eps, vf_coef, ent_coef, (B16*)dlogits, ld_dlogits, n_pad, (B16*)dvalues, ld_dvalues,  \
+        out);                                                                                             \
+    break;
+  switch (n_actions) {
+    GRB_CASE(17)
+    GRB_CASE(43)
+    default:
+      return -1;
+  }
+#undef GRB_CASE
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+extern "C" int grp_bias_grad(const void* y, int64_t ld_y, const void* dy_a, int64_t ld_a, const void* dy_b,
+                             int64_t ld_b, int32_t split, int32_t rows, int32_t cols, void* dz, float* db,
+                             float* work, int32_t row_chunks, unsigned* counters, void* stream) {
+  if (rows <= 0 || cols <= 0 || row_chunks <= 0 || split < 0 || split > cols || (y && !dz)) return -1;
+  if (split < cols && !dy_b) return -1;
+  if (split > 0 && !dy_a) return -1;
+  auto al16 = [](const void* q) { return ((uintptr_t)q & 15) == 0; };
+  const bool vec = cols % 8 == 0 && split % 8 == 0 && ld_a % 8 == 0 && ld_b % 8 == 0 && ld_y % 8 == 0 &&
+                   (!dy_a || al16(dy_a)) && (!dy_b || al16(dy_b)) && (!y || al16(y)) && (!dz || al16(dz));
+  const dim3 grid((cols + BG_COLS - 1) / BG_COLS, row_chunks);
+  using B16 = __nv_bfloat16;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (vec)
+    k_bias_grad<true><<<grid, BG_THREADS, 0, st>>>((const B16*)y, ld_y, (const B16*)dy_a, ld_a, (const B16*)dy_b,
+                                                   ld_b, split, rows, cols, (B16*)dz, db, work, counters);
+  else
+    k_bias_grad<false><<<grid, BG_THREADS, 0, st>>>((const B16*)y, ld_y, (const B16*)dy_a, ld_a, (const B16*)dy_b,
+                                                    ld_b, split, rows, cols, (B16*)dz, db, work, counters);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+extern "C" int grp_clip_adam(float* params, const float* grads, float* exp_avg, float* exp_avg_sq,
+                             void* params_bf16, int64_t n, const float* lr, float* step, float beta1, float beta2,
+                             float eps, float grad_scale, float max_norm, float* work, unsigned* counter,
+                             void* stream) {
+  if (n <= 0) return -1;
+  if (((uintptr_t)params | (uintptr_t)grads | (uintptr_t)exp_avg | (uintptr_t)exp_avg_sq) & 15) return -1;
+  if ((uintptr_t)params_bf16 & 7) return -1;
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_sumsq<<<SQ_CTAS, AD_THREADS, 0, st>>>(grads, n, grad_scale, max_norm, lr, step, beta1, beta2, work + 4, counter,
+                                          work);
+  k_adam<<<sms * 4, AD_THREADS, 0, st>>>(params, grads, exp_avg, exp_avg_sq, (__nv_bfloat16*)params_bf16, n, work,
+                                         beta1, beta2, eps);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

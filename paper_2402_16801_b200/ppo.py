@@ -59,6 +59,7 @@ class PPOConfig:
     graphs: bool = True           # one GPU: rollout step, GAE and minibatch update as CUDA graphs
     fused_loss: bool = True       # graphed learner: PPO objective + gradient in one CUDA kernel (gr_ppo.cu)
     fused_sampler: bool = True    # graphed learner: action sampling + rollout-buffer writes in one kernel
+    manual_backward: bool = True  # graphed bf16 learner: hand-written backward + clip/Adam kernels (learner.py)
 
 
 def gae(rewards, values, dones, last_value, gamma: float, lam: float):
@@ -357,27 +358,46 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
     # aligned leading dimensions; the pad columns hold zeros, so they add
     # nothing to the pre-activations and their weights get zero gradients
     obs_pad = (obs_dim + 63) // 64 * 64
-    model = make_fused_model(obs_pad, n_actions, cfg.layer_size).to(dev)
-    params = list(model.parameters())
-    # gradients as views of one flat buffer: one all-reduce per minibatch
-    flat_grad = torch.zeros(sum(p.numel() for p in params), dtype=torch.float32, device=dev)
-    off = 0
-    for p_ in params:
-        p_.grad = flat_grad[off:off + p_.numel()].view_as(p_)
-        off += p_.numel()
+    batch_size = n * T
+    mb = batch_size // cfg.n_minibatches
+    manual = cfg.manual_backward and cfg.bf16 and cfg.fused_loss
+    learner = None
+    if manual:
+        from .learner import ManualLearner, pad_actions
+        # the action head padded to a multiple of 8 outputs (zero rows that
+        # stay zero: their gradients are exactly zero)
+        model = make_fused_model(obs_pad, pad_actions(n_actions), cfg.layer_size).to(dev)
+        with torch.no_grad():
+            model.actor[-1].weight[n_actions:].zero_()
+            model.actor[-1].bias[n_actions:].zero_()
+        learner = ManualLearner(model, n_actions, mb, dev)
+        params = learner.params
+        flat_grad = learner.G   # the .grad tensors are views of it
+    else:
+        model = make_fused_model(obs_pad, n_actions, cfg.layer_size).to(dev)
+        params = list(model.parameters())
+        # gradients as views of one flat buffer: one all-reduce per minibatch
+        flat_grad = torch.zeros(sum(p.numel() for p in params), dtype=torch.float32, device=dev)
+        off = 0
+        for p_ in params:
+            p_.grad = flat_grad[off:off + p_.numel()].view_as(p_)
+            off += p_.numel()
     if world > 1:
         for p_ in params:
             dist.broadcast(p_.data, 0)
-    # rollout weights: bf16 copies refreshed once per rollout (the weights do
-    # not change within one), so the 64 per-step graphs cast nothing
-    roll_w = [p.detach().to(torch.bfloat16 if cfg.bf16 else torch.float32) for p in params]
+    if learner is not None:
+        learner.Pb.copy_(learner.P)
+        # the rollout reads the learner's bf16 weights (refreshed by every Adam step)
+        roll_w = learner.bf16_weights()
+    else:
+        # rollout weights: bf16 copies refreshed once per rollout (the weights do
+        # not change within one), so the 64 per-step graphs cast nothing
+        roll_w = [p.detach().to(torch.bfloat16 if cfg.bf16 else torch.float32) for p in params]
     lr_t = torch.tensor(cfg.lr, dtype=torch.float32, device=dev)
-    opt = torch.optim.Adam(params, lr=lr_t, eps=1e-5, capturable=True, fused=True)
-    batch_size = n * T
+    opt = None if manual else torch.optim.Adam(params, lr=lr_t, eps=1e-5, capturable=True, fused=True)
     n_updates = max(1, cfg.total_timesteps // (batch_size * world))
     if max_updates is not None:
         n_updates = min(n_updates, max_updates)
-    mb = batch_size // cfg.n_minibatches
     odt = torch.bfloat16 if cfg.bf16 else torch.float32   # autocast casts the input to bf16 anyway
 
     buf_obs = torch.zeros((T, n, obs_pad), dtype=odt, device=dev)
@@ -398,13 +418,13 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
         # no autocast weight cache: graphs must own their casts
         with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.bf16, cache_enabled=False):
             logits, v = model(x)
-        return logits.float(), v.float()
+        return logits[:, :n_actions].float(), v.float()
 
     lin_ix = [(k, k + 1) for k in range(0, len(params), 2)]   # (weight, bias) per Linear, module order
 
     def roll_policy(x):
         ha, hc = roll_policy_raw(x)
-        return ha.float(), hc.float().squeeze(-1)
+        return ha[:, :n_actions].float(), hc.float().squeeze(-1)
 
     def roll_policy_raw(x):
         """Rollout forward on the pre-cast weights (module order: first,
@@ -429,8 +449,9 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
     rng_ctr = torch.zeros(1, dtype=torch.int64, device=dev)   # sampler counter, one per rollout
 
     def refresh_roll_w():
-        for dst, src in zip(roll_w, params):
-            dst.copy_(src.detach())
+        if learner is None:
+            for dst, src in zip(roll_w, params):
+                dst.copy_(src.detach())
         rng_ctr.add_(1)
 
     def roll_step(t):
@@ -477,8 +498,18 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
     b_act, b_logp = buf_act.view(-1), buf_logp.view(-1)
     b_adv, b_ret, b_val = adv.view(-1), ret.view(-1), buf_val.view(-1)
 
+    x_mb = torch.empty((mb, obs_pad), dtype=odt, device=dev) if learner is not None else None
+
     def mb_step():
         idx = idx_s
+        if learner is not None:
+            torch.index_select(b_obs, 0, idx, out=x_mb)
+            learner.forward(x_mb)
+            learner.loss(b_act.index_select(0, idx), b_logp.index_select(0, idx), b_adv.index_select(0, idx),
+                         b_val.index_select(0, idx), b_ret.index_select(0, idx), cfg.clip_eps, cfg.vf_coef,
+                         cfg.ent_coef, stats_s)
+            learner.backward(x_mb)
+            return
         logits, v = policy(b_obs.index_select(0, idx))
         if cfg.fused_loss:
             loss, st = ppo_objective(logits, v, b_act.index_select(0, idx), b_logp.index_select(0, idx),
@@ -502,13 +533,17 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
         stats_s.copy_(torch.stack([loss.detach(), pg.detach(), vl.detach(), ent.detach()]))
 
     def mb_opt():
+        if learner is not None:   # clip + Adam, the ranks' gradient sum averaged inside
+            learner.clip_adam(lr_t, cfg.max_grad_norm, 1.0 / world)
+            return
         if world > 1:
             flat_grad.div_(world)   # the all-reduce summed the ranks' gradients
         torch.nn.utils.clip_grad_norm_(params, cfg.max_grad_norm, foreach=True)
         opt.step()
 
     def mb_grad():
-        opt.zero_grad(set_to_none=False)   # the .grad views of flat_grad stay
+        if opt is not None:   # (the manual learner writes every gradient element)
+            opt.zero_grad(set_to_none=False)   # the .grad views of flat_grad stay
         mb_step()
 
     def update_epochs(g_grad=None, g_opt=None):
