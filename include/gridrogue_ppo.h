@@ -45,13 +45,16 @@ int grp_sample_actions(const void* logits, const void* values, int32_t bf16, int
  * written as bf16 (what the head GEMMs of a bf16 learner consume): d loss /
  * d logits into dlogits[row * ld_dlogits + j] for j < n_actions and zeros for
  * n_actions <= j < n_pad (a head padded to n_pad outputs), d loss / d value
- * into dvalues[row * ld_dvalues].  out[4] as for grp_ppo_loss.
+ * into dvalues[row * ld_dvalues].  out[4] as for grp_ppo_loss.  index: null,
+ * or int64[batch] -- row i's actions / logp_old / advantages / values_old /
+ * returns are entry index[i] of those arrays (the minibatch gather fused).
  * Returns 0, -1 (unsupported n_actions, batch <= 0, n_pad < n_actions), -2. */
 int grp_ppo_loss_bf16(const void* logits, int64_t ld_logits, const void* values, int64_t ld_values,
                       const int64_t* actions, const float* logp_old, const float* advantages,
                       const float* values_old, const float* returns, int32_t batch, int32_t n_actions,
                       float clip_eps, float vf_coef, float ent_coef, void* dlogits, int64_t ld_dlogits,
-                      int32_t n_pad, void* dvalues, int64_t ld_dvalues, float* out, void* stream);
+                      int32_t n_pad, void* dvalues, int64_t ld_dvalues, float* out, const int64_t* index,
+                      void* stream);
 
 /* One layer of the learner's hand-written backward (bf16 activations /
  * gradients, row-major): with dy[i, j] = dy_a[i * ld_a + j] for j < split and

@@ -136,7 +136,7 @@ def lib() -> ctypes.CDLL:
         "grp_sample_actions": (I32, [P, P, I32, I32, I32, I64, I64, U64, P, ctypes.c_uint32, P, P, P, P, P, P,
                                      P, P, P]),
         "grp_ppo_loss_bf16": (I32, [P, I64, P, I64, P, P, P, P, P, I32, I32, ctypes.c_float, ctypes.c_float,
-                                    ctypes.c_float, P, I64, I32, P, I64, P, P]),
+                                    ctypes.c_float, P, I64, I32, P, I64, P, P, P]),
         "grp_bias_grad": (I32, [P, I64, P, I64, P, I64, I32, I32, I32, P, P, P, I32, P, P]),
         "grp_clip_adam": (I32, [P, P, P, P, P, I64, P, P, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                 ctypes.c_float, ctypes.c_float, P, P, P]),

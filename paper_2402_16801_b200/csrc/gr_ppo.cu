@@ -57,14 +57,17 @@ __global__ void __launch_bounds__(THREADS) k_ppo_loss(const TI* __restrict__ log
                                                       const float* __restrict__ ret, int B, float clip_eps,
                                                       float vf_coef, float ent_coef, TO* __restrict__ dlogits,
                                                       int64_t ldd, int npad, TO* __restrict__ dv, int64_t lddv,
-                                                      float* __restrict__ out) {
+                                                      float* __restrict__ out, const int64_t* __restrict__ index) {
+  // index != null: the per-sample inputs (act, logp_old, adv, v_old, ret)
+  // of minibatch row i are entry index[i] of the rollout-wide arrays
+  auto src = [&](int i) -> int64_t { return index ? index[i] : (int64_t)i; };
   constexpr int PER = (NA + 31) / 32;
   __shared__ float red[2][THREADS / 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // advantage mean and unbiased std over the minibatch
   float s = 0.f, s2 = 0.f;
   for (int i = threadIdx.x; i < B; i += THREADS) {
-    const float a = adv[i];
+    const float a = adv[src(i)];
     s += a;
     s2 += a * a;
   }
@@ -115,7 +118,8 @@ __global__ void __launch_bounds__(THREADS) k_ppo_loss(const TI* __restrict__ log
       }
     }
     h = warp_sum(h);
-    const int a = (int)act[row];
+    const int64_t sr = src(row);
+    const int a = (int)act[sr];
     float zsel = 0.f;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
@@ -123,8 +127,8 @@ __global__ void __launch_bounds__(THREADS) k_ppo_loss(const TI* __restrict__ log
       if (k == a / 32) zsel = zk;
     }
     const float logp = zsel - lse;
-    const float r = expf(logp - logp_old[row]);
-    const float an = (adv[row] - mean) * inv_std;
+    const float r = expf(logp - logp_old[sr]);
+    const float an = (adv[sr] - mean) * inv_std;
     const float s1 = r * an;
     const float rc = fminf(fmaxf(r, 1.f - clip_eps), 1.f + clip_eps);
     const float s2c = rc * an;
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(THREADS) k_ppo_loss(const TI* __restrict__ log
     else g_logp = (r > 1.f - clip_eps && r < 1.f + clip_eps) ? -an * r : 0.f;
     g_logp *= invB;
     // value loss
-    const float vv = to_f(v[(size_t)row * ldv]), vo = v_old[row], R = ret[row];
+    const float vv = to_f(v[(size_t)row * ldv]), vo = v_old[sr], R = ret[sr];
     const float dvu = vv - vo;
     const float vc = vo + fminf(fmaxf(dvu, -clip_eps), clip_eps);
     const float e1 = (vv - R) * (vv - R), e2 = (vc - R) * (vc - R);
@@ -462,7 +466,7 @@ extern "C" int grp_ppo_loss(const float* logits, const float* v, const int64_t* 
   case N:                                                                                                    \
     k_ppo_loss<N, float, float><<<grid, THREADS, 0, st>>>(logits, N, v, 1, actions, logp_old, adv, v_old, ret, \
                                                          batch, clip_eps, vf_coef, ent_coef, dlogits, N, N, dv, 1,  \
-                                                         out);                                                    \
+                                                         out, nullptr);                                           \
     break;
   switch (n_actions) {
     GRP_CASE(17)
@@ -507,7 +511,8 @@ extern "C" int grp_ppo_loss_bf16(const void* logits, int64_t ld_logits, const vo
                                  const int64_t* actions, const float* logp_old, const float* adv,
                                  const float* v_old, const float* ret, int32_t batch, int32_t n_actions,
                                  float clip_eps, float vf_coef, float ent_coef, void* dlogits, int64_t ld_dlogits,
-                                 int32_t n_pad, void* dvalues, int64_t ld_dvalues, float* out, void* stream) {
+                                 int32_t n_pad, void* dvalues, int64_t ld_dvalues, float* out, const int64_t* index,
+                                 void* stream) {
   if (batch <= 0 || n_pad < n_actions || ld_dlogits < n_pad) return -1;
   cudaStream_t st = (cudaStream_t)stream;
   int dev = 0, sms = 148;
@@ -521,7 +526,7 @@ extern "C" int grp_ppo_loss_bf16(const void* logits, int64_t ld_logits, const vo
     k_ppo_loss<N, B16, B16><<<grid, THREADS, 0, st>>>(                                                    \
         (const B16*)logits, ld_logits, (const B16*)values, ld_values, actions, logp_old, adv, v_old, ret, \
         batch, clip_eps, vf_coef, ent_coef, (B16*)dlogits, ld_dlogits, n_pad, (B16*)dvalues, ld_dvalues,  \
-        out);                                                                                             \
+        out, index);                                                                                      \
     break;
   switch (n_actions) {
     GRB_CASE(17)

@@ -177,9 +177,11 @@ class ManualLearner:
         self._bias_grad(self.h0, self.dya, self.dyc, L, 2 * L, self.dz0, gb)
         torch.mm(self.dz0.t(), x, out_dtype=torch.float32, out=gw)
 
-    def loss(self, actions, logp_old, adv, v_old, ret, clip_eps, vf_coef, ent_coef, stats):
+    def loss(self, actions, logp_old, adv, v_old, ret, clip_eps, vf_coef, ent_coef, stats, index=None):
         """The PPO objective of the last forward; stats (float[4], zeroed
-        here) <- [loss, pg, vl, entropy]; gradients into dlogits / dvalue."""
+        here) <- [loss, pg, vl, entropy]; gradients into dlogits / dvalue.
+        index (int64[rows], optional): row i's per-sample inputs are entry
+        index[i] of the given arrays (the minibatch gather in the kernel)."""
         torch = self.torch
         stats.zero_()
         _check(lib().grp_ppo_loss_bf16(
@@ -187,7 +189,7 @@ class ManualLearner:
             actions.data_ptr(), logp_old.data_ptr(), adv.data_ptr(), v_old.data_ptr(), ret.data_ptr(), self.rows,
             self.n_actions, float(clip_eps), float(vf_coef), float(ent_coef), self.dlogits.data_ptr(),
             self.dlogits.stride(0), self.a_pad, self.dvalue.data_ptr(), self.dvalue.stride(0), stats.data_ptr(),
-            torch.cuda.current_stream().cuda_stream), f"grp_ppo_loss_bf16 (n_actions {self.n_actions})")
+            None if index is None else index.data_ptr(), torch.cuda.current_stream().cuda_stream), f"grp_ppo_loss_bf16 (n_actions {self.n_actions})")
 
     # --- optimizer -------------------------------------------------------------
     def clip_adam(self, lr_t, max_norm: float, grad_scale: float = 1.0):

@@ -505,9 +505,8 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
         if learner is not None:
             torch.index_select(b_obs, 0, idx, out=x_mb)
             learner.forward(x_mb)
-            learner.loss(b_act.index_select(0, idx), b_logp.index_select(0, idx), b_adv.index_select(0, idx),
-                         b_val.index_select(0, idx), b_ret.index_select(0, idx), cfg.clip_eps, cfg.vf_coef,
-                         cfg.ent_coef, stats_s)
+            learner.loss(b_act, b_logp, b_adv, b_val, b_ret, cfg.clip_eps, cfg.vf_coef, cfg.ent_coef, stats_s,
+                         index=idx)
             learner.backward(x_mb)
             return
         logits, v = policy(b_obs.index_select(0, idx))
