@@ -61,12 +61,21 @@ int grp_ppo_loss_bf16(const void* logits, int64_t ld_logits, const void* values,
  * dy_b[i * ld_b + j - split] otherwise,
  *   y != NULL: dz[i * cols + j] = bf16(dy[i, j] * (1 - y[i * ld_y + j]^2))   (tanh backward)
  *   db[j] = sum over rows of dz[i, j] (or of dy when y == NULL), fp32.
- * work: float[row_chunks * cols]; counters: unsigned[ceil(cols / 64)], zero
- * before the first call (each call leaves them zero).  The sum order is
- * fixed by row_chunks: results are deterministic.  0, -1 (bad arguments), -2. */
+ * batch > 1 (split == cols): entry b reads y + b * bs_y, dy_a + b * bs_a, writes
+ * dz + b * bs_dz and db + b * cols (the actor's and critic's layers at once).
+ * work: float[batch * row_chunks * cols]; counters: unsigned[batch *
+ * ceil(cols / 64)], zero before the first call (each call leaves them zero).
+ * The sum order is fixed by row_chunks: results are deterministic.
+ * 0, -1 (bad arguments), -2. */
 int grp_bias_grad(const void* y, int64_t ld_y, const void* dy_a, int64_t ld_a, const void* dy_b, int64_t ld_b,
                   int32_t split, int32_t rows, int32_t cols, void* dz, float* db, float* work,
-                  int32_t row_chunks, unsigned* counters, void* stream);
+                  int32_t row_chunks, unsigned* counters, int32_t batch, int64_t bs_y, int64_t bs_a,
+                  int64_t bs_dz, void* stream);
+
+/* z[b, i, j] = bf16(tanh(z[b, i, j] + bias[b, j])) in place; z a contiguous
+ * bf16 [batch, rows, cols] tensor, bias bf16 [batch, cols]; cols % 8 == 0,
+ * both 16-byte aligned.  0, -1 (bad arguments), -2. */
+int grp_bias_tanh(void* z, const void* bias, int32_t batch, int32_t rows, int32_t cols, void* stream);
 
 /* torch.nn.utils.clip_grad_norm_(max_norm) of grads * grad_scale, then one
  * torch.optim.Adam step (no weight decay; *lr and *step live on the device,

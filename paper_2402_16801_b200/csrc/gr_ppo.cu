@@ -291,9 +291,19 @@ __global__ void __launch_bounds__(BG_THREADS) k_bias_grad(const __nv_bfloat16* _
                                                           const __nv_bfloat16* __restrict__ dyb, int64_t ldb,
                                                           int split, int rows, int cols,
                                                           __nv_bfloat16* __restrict__ dz, float* __restrict__ db,
-                                                          float* __restrict__ work, unsigned* __restrict__ counters) {
+                                                          float* __restrict__ work, unsigned* __restrict__ counters,
+                                                          int64_t bsy, int64_t bsa, int64_t bsz) {
   __shared__ float red[BG_TR][BG_COLS + 1];
   __shared__ bool last;
+  {   // batch entry blockIdx.z: its own operands, bias gradient, partials and counters
+    const int z = blockIdx.z;
+    if (y) y += z * bsy;
+    dya += z * bsa;
+    if (dz) dz += z * bsz;
+    db += (size_t)z * cols;
+    work += (size_t)z * gridDim.y * cols;
+    counters += (size_t)z * gridDim.x;
+  }
   const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
   const int c0 = blockIdx.x * BG_COLS + tx * 8;
   const int RCH = gridDim.y;
@@ -359,6 +369,25 @@ __global__ void __launch_bounds__(BG_THREADS) k_bias_grad(const __nv_bfloat16* _
     }
   }
   if (threadIdx.x == 0) counters[blockIdx.x] = 0;   // ready for the next launch (graph replays)
+}
+
+// z[b, i, j] = bf16(tanh(z[b, i, j] + bias[b, j])) in place over a contiguous
+// [batch, rows, cols] bf16 tensor (the actor's and critic's hidden layers as
+// one batched GEMM without a bias epilogue, then this); 8 elements per thread.
+__global__ void __launch_bounds__(256) k_bias_tanh(__nv_bfloat16* __restrict__ z,
+                                                   const __nv_bfloat16* __restrict__ bias, int64_t n8, int cols,
+                                                   int64_t per_batch) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n8; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = k * 8;
+    const int b = (int)(e / per_batch), j = (int)(e % cols);
+    uint4 v = reinterpret_cast<uint4*>(z)[k];
+    const uint4 bb = *reinterpret_cast<const uint4*>(bias + (size_t)b * cols + j);
+    __nv_bfloat16* vv = reinterpret_cast<__nv_bfloat16*>(&v);
+    const __nv_bfloat16* bv = reinterpret_cast<const __nv_bfloat16*>(&bb);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) vv[q] = __float2bfloat16(tanhf(__bfloat162float(vv[q]) + __bfloat162float(bv[q])));
+    reinterpret_cast<uint4*>(z)[k] = v;
+  }
 }
 
 // ------------------------------------------------ global-norm clip + Adam
@@ -460,8 +489,10 @@ extern "C" int grp_ppo_loss(const float* logits, const float* v, const int64_t* 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int rows_per_cta = THREADS / 32;
-  const int grid = (int)std::min<int64_t>((batch + rows_per_cta - 1) / rows_per_cta, (int64_t)sms * 4);
+  // >= 8 rows per warp: every CTA first re-reads the whole advantage column
+  // (mean / std), so fewer, fuller CTAs (8,192 rows: 128 CTAs)
+  const int rows_per_cta = 8 * (THREADS / 32);
+  const int grid = (int)std::min<int64_t>((batch + rows_per_cta - 1) / rows_per_cta, (int64_t)sms);
 #define GRP_CASE(N)                                                                                          \
   case N:                                                                                                    \
     k_ppo_loss<N, float, float><<<grid, THREADS, 0, st>>>(logits, N, v, 1, actions, logp_old, adv, v_old, ret, \
@@ -518,8 +549,10 @@ extern "C" int grp_ppo_loss_bf16(const void* logits, int64_t ld_logits, const vo
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int rows_per_cta = THREADS / 32;
-  const int grid = (int)std::min<int64_t>((batch + rows_per_cta - 1) / rows_per_cta, (int64_t)sms * 4);
+  // >= 8 rows per warp: every CTA first re-reads the whole advantage column
+  // (mean / std), so fewer, fuller CTAs (8,192 rows: 128 CTAs)
+  const int rows_per_cta = 8 * (THREADS / 32);
+  const int grid = (int)std::min<int64_t>((batch + rows_per_cta - 1) / rows_per_cta, (int64_t)sms);
   using B16 = __nv_bfloat16;
 #define GRB_CASE(N)                                                                                       \
   case N:                                                                                                 \
@@ -540,22 +573,27 @@ extern "C" int grp_ppo_loss_bf16(const void* logits, int64_t ld_logits, const vo
 
 extern "C" int grp_bias_grad(const void* y, int64_t ld_y, const void* dy_a, int64_t ld_a, const void* dy_b,
                              int64_t ld_b, int32_t split, int32_t rows, int32_t cols, void* dz, float* db,
-                             float* work, int32_t row_chunks, unsigned* counters, void* stream) {
+                             float* work, int32_t row_chunks, unsigned* counters, int32_t batch, int64_t bs_y,
+                             int64_t bs_a, int64_t bs_dz, void* stream) {
   if (rows <= 0 || cols <= 0 || row_chunks <= 0 || split < 0 || split > cols || (y && !dz)) return -1;
   if (split < cols && !dy_b) return -1;
   if (split > 0 && !dy_a) return -1;
+  if (batch < 1 || (batch > 1 && split != cols)) return -1;   // batched: one source per entry
   auto al16 = [](const void* q) { return ((uintptr_t)q & 15) == 0; };
   const bool vec = cols % 8 == 0 && split % 8 == 0 && ld_a % 8 == 0 && ld_b % 8 == 0 && ld_y % 8 == 0 &&
+                   bs_y % 8 == 0 && bs_a % 8 == 0 && bs_dz % 8 == 0 &&
                    (!dy_a || al16(dy_a)) && (!dy_b || al16(dy_b)) && (!y || al16(y)) && (!dz || al16(dz));
-  const dim3 grid((cols + BG_COLS - 1) / BG_COLS, row_chunks);
+  const dim3 grid((cols + BG_COLS - 1) / BG_COLS, row_chunks, batch);
   using B16 = __nv_bfloat16;
   cudaStream_t st = (cudaStream_t)stream;
   if (vec)
     k_bias_grad<true><<<grid, BG_THREADS, 0, st>>>((const B16*)y, ld_y, (const B16*)dy_a, ld_a, (const B16*)dy_b,
-                                                   ld_b, split, rows, cols, (B16*)dz, db, work, counters);
+                                                   ld_b, split, rows, cols, (B16*)dz, db, work, counters, bs_y, bs_a,
+                                                   bs_dz);
   else
     k_bias_grad<false><<<grid, BG_THREADS, 0, st>>>((const B16*)y, ld_y, (const B16*)dy_a, ld_a, (const B16*)dy_b,
-                                                    ld_b, split, rows, cols, (B16*)dz, db, work, counters);
+                                                    ld_b, split, rows, cols, (B16*)dz, db, work, counters, bs_y, bs_a,
+                                                    bs_dz);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
@@ -574,5 +612,17 @@ extern "C" int grp_clip_adam(float* params, const float* grads, float* exp_avg, 
                                           work);
   k_adam<<<sms * 4, AD_THREADS, 0, st>>>(params, grads, exp_avg, exp_avg_sq, (__nv_bfloat16*)params_bf16, n, work,
                                          beta1, beta2, eps);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+extern "C" int grp_bias_tanh(void* z, const void* bias, int32_t batch, int32_t rows, int32_t cols, void* stream) {
+  if (batch < 1 || rows <= 0 || cols <= 0 || cols % 8 || ((uintptr_t)z & 15) || ((uintptr_t)bias & 15)) return -1;
+  const int64_t n8 = (int64_t)batch * rows * cols / 8;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>((n8 + 255) / 256, (int64_t)sms * 8);
+  k_bias_tanh<<<grid, 256, 0, (cudaStream_t)stream>>>((__nv_bfloat16*)z, (const __nv_bfloat16*)bias, n8, cols,
+                                                      (int64_t)rows * cols);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

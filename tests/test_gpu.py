@@ -751,7 +751,7 @@ def test_bias_grad_kernel_exact(torch_cuda):
         for o in out:
             rc = lib().grp_bias_grad(y.data_ptr(), y.stride(0), da.data_ptr(), da.stride(0), db_.data_ptr(),
                                      db_.stride(0), split, rows, cols, dz.data_ptr(), o.data_ptr(), work.data_ptr(),
-                                     32, ctr.data_ptr(), torch.cuda.current_stream().cuda_stream)
+                                     32, ctr.data_ptr(), 1, 0, 0, 0, torch.cuda.current_stream().cuda_stream)
             assert rc == 0
         torch.cuda.synchronize()
         ref_dz = (dy.float() * (1 - y.float() ** 2)).to(torch.bfloat16)
@@ -760,6 +760,30 @@ def test_bias_grad_kernel_exact(torch_cuda):
         assert torch.allclose(out[0].double(), ref_db, rtol=1e-5, atol=1e-4), (rows, cols)
         assert torch.equal(out[0], out[1])
         assert int(ctr.abs().sum()) == 0
+    # batched: the actor / critic pair of a hidden layer, [2, rows, cols]
+    rows, cols = 4096, 512
+    y = torch.tanh(torch.randn(2, rows, cols, device="cuda", generator=g)).to(torch.bfloat16)
+    dy = torch.randn(2, rows, cols, device="cuda", generator=g).to(torch.bfloat16)
+    dz = torch.empty_like(dy)
+    db = torch.empty(2, cols, device="cuda")
+    work = torch.zeros(2 * 32 * cols, device="cuda")
+    ctr = torch.zeros(2 * (cols // 64), dtype=torch.int32, device="cuda")
+    rc = lib().grp_bias_grad(y.data_ptr(), cols, dy.data_ptr(), cols, None, 0, cols, rows, cols, dz.data_ptr(),
+                             db.data_ptr(), work.data_ptr(), 32, ctr.data_ptr(), 2, rows * cols, rows * cols,
+                             rows * cols, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert rc == 0
+    ref_dz = (dy.float() * (1 - y.float() ** 2)).to(torch.bfloat16)
+    assert torch.equal(dz, ref_dz)
+    assert torch.allclose(db.double(), ref_dz.double().sum(1), rtol=1e-5, atol=1e-4)
+    # grp_bias_tanh: z <- bf16(tanh(z + bias[b])) (float tanh: within 1 bf16 ulp of the float64 value)
+    z = torch.randn(2, rows, cols, device="cuda", generator=g).to(torch.bfloat16)
+    bias = torch.randn(2, cols, device="cuda", generator=g).to(torch.bfloat16)
+    ref = torch.tanh(z.double() + bias.double()[:, None, :])
+    assert lib().grp_bias_tanh(z.data_ptr(), bias.data_ptr(), 2, rows, cols,
+                               torch.cuda.current_stream().cuda_stream) == 0
+    torch.cuda.synchronize()
+    assert float((z.double() - ref).abs().max()) <= 2 ** -8
 
 
 def test_clip_adam_matches_torch(torch_cuda):
