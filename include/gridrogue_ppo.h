@@ -89,6 +89,13 @@ int grp_clip_adam(float* params, const float* grads, float* exp_avg, float* exp_
                   int64_t n, const float* lr, float* step, float beta1, float beta2, float eps, float grad_scale,
                   float max_norm, float* work, unsigned* counter, void* stream);
 
+/* dst[i * ld_dst + j] = bf16(src[i * width + j]) (round to nearest even) for
+ * rows i and j < width: a batch's float32 observations into a bf16 rollout
+ * buffer with padded rows (ld_dst >= width; vectorised when width and ld_dst
+ * are multiples of 4, src 16-byte and dst 8-byte aligned).
+ * 0, -1 (bad arguments), -2. */
+int grp_rows_to_bf16(const float* src, int64_t rows, int32_t width, void* dst, int64_t ld_dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

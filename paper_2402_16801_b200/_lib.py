@@ -139,6 +139,7 @@ def lib() -> ctypes.CDLL:
                                     ctypes.c_float, P, I64, I32, P, I64, P, P, P]),
         "grp_bias_grad": (I32, [P, I64, P, I64, P, I64, I32, I32, I32, P, P, P, I32, P, I32, I64, I64, I64, P]),
         "grp_bias_tanh": (I32, [P, P, I32, I32, I32, P]),
+        "grp_rows_to_bf16": (I32, [P, I64, I32, P, I64, P]),
         "grp_clip_adam": (I32, [P, P, P, P, P, I64, P, P, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                 ctypes.c_float, ctypes.c_float, P, P, P]),
     }

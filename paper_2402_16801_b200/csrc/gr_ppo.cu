@@ -390,6 +390,33 @@ __global__ void __launch_bounds__(256) k_bias_tanh(__nv_bfloat16* __restrict__ z
   }
 }
 
+// dst[i * ld_dst + j] = bf16(src[i * w + j]) for j < w (float4 loads, 8-byte
+// stores; the rollout buffer's copy of a step's observation, which the
+// writer has just left in L2)
+__global__ void __launch_bounds__(256) k_f32_to_bf16_rows(const float* __restrict__ src, int64_t rows, int w4,
+                                                          __nv_bfloat16* __restrict__ dst, int64_t ld_dst) {
+  const int64_t total = rows * w4;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = k / w4;
+    const int j4 = (int)(k - i * w4);
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(src) + k);
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    uint2 packed;
+    packed.x = *reinterpret_cast<uint32_t*>(&lo);
+    packed.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(dst + i * ld_dst + (int64_t)j4 * 4) = packed;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_f32_to_bf16_any(const float* __restrict__ src, int64_t rows, int w,
+                                                         __nv_bfloat16* __restrict__ dst, int64_t ld_dst) {
+  const int64_t total = rows * w;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = k / w;
+    dst[i * ld_dst + (k - i * w)] = __float2bfloat16(__ldcs(src + k));
+  }
+}
+
 // ------------------------------------------------ global-norm clip + Adam
 // torch.nn.utils.clip_grad_norm_ followed by torch.optim.Adam (capturable,
 // no weight decay, no amsgrad) over one flat fp32 parameter buffer, in two
@@ -624,5 +651,24 @@ extern "C" int grp_bias_tanh(void* z, const void* bias, int32_t batch, int32_t r
   const int grid = (int)std::min<int64_t>((n8 + 255) / 256, (int64_t)sms * 8);
   k_bias_tanh<<<grid, 256, 0, (cudaStream_t)stream>>>((__nv_bfloat16*)z, (const __nv_bfloat16*)bias, n8, cols,
                                                       (int64_t)rows * cols);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+extern "C" int grp_rows_to_bf16(const float* src, int64_t rows, int32_t width, void* dst, int64_t ld_dst,
+                                void* stream) {
+  if (rows <= 0 || width <= 0 || ld_dst < width) return -1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (width % 4 == 0 && ld_dst % 4 == 0 && !((uintptr_t)src & 15) && !((uintptr_t)dst & 7)) {
+    const int64_t total = rows * (width / 4);
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+    k_f32_to_bf16_rows<<<grid, 256, 0, st>>>(src, rows, width / 4, (__nv_bfloat16*)dst, ld_dst);
+  } else {   // any width (Craftax-Classic: 1,345 floats per row)
+    const int64_t total = rows * width;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+    k_f32_to_bf16_any<<<grid, 256, 0, st>>>(src, rows, width, (__nv_bfloat16*)dst, ld_dst);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

@@ -124,11 +124,9 @@ class ManualLearner:
         # activations and gradients of one minibatch
         bf = dict(dtype=torch.bfloat16, device=device)
         R = self.rows
-        self.h0 = torch.empty((R, 2 * L), **bf)
-        self.h0_pair = self.h0.view(R, 2, L).transpose(0, 1)   # [2, R, L] view: actor / critic halves
-        self.hs = [torch.empty((2, R, L), **bf) for _ in range(self.n_hidden)]
-        self.logits = torch.empty((R, self.a_pad), **bf)
-        self.value = torch.empty((R, self.critic[-1].out_features), **bf)
+        self.acts = self.make_acts(R)
+        self.h0, self.h0_pair, self.hs = self.acts.h0, self.acts.h0_pair, self.acts.hs
+        self.logits, self.value = self.acts.logits, self.acts.value
         self.dlogits = torch.empty((R, self.a_pad), **bf)
         self.dvalue = torch.empty_like(self.value)
         self.dy = torch.empty((2, R, L), **bf)
@@ -136,6 +134,21 @@ class ManualLearner:
         self.dz0 = torch.empty((R, 2 * L), **bf)
         self.bg_work = torch.zeros(2 * ROW_CHUNKS * max(2 * L, self.a_pad), **f32)
         self.bg_ctr = torch.zeros(2 * ((2 * L + 63) // 64 + 1), dtype=torch.int32, device=device)
+
+    def make_acts(self, rows: int):
+        """Activation buffers of a forward over `rows` rows (the minibatch's
+        are self.acts; the rollout keeps its own set)."""
+        import types
+        torch = self.torch
+        bf = dict(dtype=torch.bfloat16, device=self.P.device)
+        L = self.L
+        a = types.SimpleNamespace(rows=rows)
+        a.h0 = torch.empty((rows, 2 * L), **bf)
+        a.h0_pair = a.h0.view(rows, 2, L).transpose(0, 1)   # [2, rows, L] view: actor / critic halves
+        a.hs = [torch.empty((2, rows, L), **bf) for _ in range(self.n_hidden)]
+        a.logits = torch.empty((rows, self.a_pad), **bf)
+        a.value = torch.empty((rows, self.critic[-1].out_features), **bf)
+        return a
 
     # --- views -------------------------------------------------------------
     def w(self, lin):
@@ -153,22 +166,24 @@ class ManualLearner:
         return self.torch.cuda.current_stream().cuda_stream
 
     # --- forward -------------------------------------------------------------
-    def forward(self, x):
-        """x: [rows, obs_pad] bf16 -> (logits [rows, a_pad], value [rows, 1]) bf16."""
+    def forward(self, x, acts=None):
+        """x: [rows, obs_pad] bf16 -> (logits [rows, a_pad], value [rows, 1])
+        bf16, in `acts` (make_acts; default the minibatch's buffers)."""
         torch = self.torch
+        a = acts or self.acts
         w, b = self.w(self.first)
-        torch.addmm(b, x, w.t(), out=self.h0).tanh_()
-        inp = self.h0_pair
+        torch.addmm(b, x, w.t(), out=a.h0).tanh_()
+        inp = a.h0_pair
         for k in range(self.n_hidden):   # actor and critic layer k: one batched GEMM, then bias + tanh
-            torch.bmm(inp, self.hw[k].transpose(1, 2), out=self.hs[k])
-            _check(lib().grp_bias_tanh(self.hs[k].data_ptr(), self.hb[k].data_ptr(), 2, self.rows, self.L,
+            torch.bmm(inp, self.hw[k].transpose(1, 2), out=a.hs[k])
+            _check(lib().grp_bias_tanh(a.hs[k].data_ptr(), self.hb[k].data_ptr(), 2, a.rows, self.L,
                                        self._stream()), "grp_bias_tanh")
-            inp = self.hs[k]
+            inp = a.hs[k]
         w, b = self.w(self.actor[-1])
-        torch.addmm(b, inp[0], w.t(), out=self.logits)
+        torch.addmm(b, inp[0], w.t(), out=a.logits)
         w, b = self.w(self.critic[-1])
-        torch.addmm(b, inp[1], w.t(), out=self.value)
-        return self.logits, self.value
+        torch.addmm(b, inp[1], w.t(), out=a.value)
+        return a.logits, a.value
 
     # --- backward --------------------------------------------------------------
     def _bias_grad(self, y, dy_a, dy_b, split, cols, dz, db, batch=1):

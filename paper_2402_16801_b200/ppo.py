@@ -426,10 +426,14 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
         ha, hc = roll_policy_raw(x)
         return ha[:, :n_actions].float(), hc.float().squeeze(-1)
 
+    roll_acts = learner.make_acts(n) if learner is not None else None
+
     def roll_policy_raw(x):
         """Rollout forward on the pre-cast weights (module order: first,
         actor 2 + head, critic 2 + head); logits [N, A] and values [N, 1] in
         the rollout dtype."""
+        if learner is not None:   # the learner's forward on its bf16 weights
+            return learner.forward(x, roll_acts)
         F = torch.nn.functional
         (w0, b0), rest = lin_ix[0], lin_ix[1:]
         h = torch.tanh(F.linear(x, roll_w[w0], roll_w[b0]))
@@ -448,6 +452,17 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
 
     rng_ctr = torch.zeros(1, dtype=torch.int64, device=dev)   # sampler counter, one per rollout
 
+    def obs_to(dst, obs):
+        """A step's float32 observations into a (padded) rollout row block."""
+        if dst.dtype == torch.bfloat16:
+            from ._lib import lib
+            rc = lib().grp_rows_to_bf16(obs.data_ptr(), n, obs_dim, dst.data_ptr(), dst.stride(0),
+                                        torch.cuda.current_stream(dev).cuda_stream)
+            if rc != 0:
+                raise RuntimeError(f"grp_rows_to_bf16 failed ({rc})")
+        else:
+            dst[:, :obs_dim].copy_(obs)
+
     def refresh_roll_w():
         if learner is None:
             for dst, src in zip(roll_w, params):
@@ -459,11 +474,11 @@ def _train_graphed(cfg: PPOConfig, log, max_updates: int | None) -> dict:
             buf_rew[t - 1].copy_(gb.reward)
             buf_done[t - 1].copy_(gb.done)
         if t == T:   # closing step: the bootstrap value
-            last_obs[:, :obs_dim].copy_(gb.obs)
+            obs_to(last_obs, gb.obs)
             _, v = roll_policy(last_obs)
             last_v.copy_(v)
             return
-        buf_obs[t, :, :obs_dim].copy_(gb.obs)
+        obs_to(buf_obs[t], gb.obs)
         if cfg.fused_sampler:
             # sampling, log-prob, value and the previous reward / done in one
             # launch (gr_ppo.cu): the step's other ~15 small kernels

@@ -786,6 +786,28 @@ def test_bias_grad_kernel_exact(torch_cuda):
     assert float((z.double() - ref).abs().max()) <= 2 ** -8
 
 
+def test_rows_to_bf16_exact(torch_cuda):
+    """grp_rows_to_bf16 (the rollout buffer's copy of a step's observation):
+    equal to torch's float32 -> bf16 cast into the padded rows, pads untouched."""
+    import torch
+    from paper_2402_16801_b200._lib import lib
+    g = torch.Generator(device="cuda").manual_seed(2)
+    src = torch.randn(1000, 8268, device="cuda", generator=g) * 3
+    dst = torch.full((1000, 8320), 7.0, dtype=torch.bfloat16, device="cuda")
+    assert lib().grp_rows_to_bf16(src.data_ptr(), 1000, 8268, dst.data_ptr(), 8320,
+                                  torch.cuda.current_stream().cuda_stream) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(dst[:, :8268], src.to(torch.bfloat16))
+    assert bool((dst[:, 8268:] == 7.0).all())
+    src = torch.randn(300, 1345, device="cuda", generator=g)   # Craftax-Classic rows: the scalar path
+    dst = torch.full((300, 1408), 7.0, dtype=torch.bfloat16, device="cuda")
+    assert lib().grp_rows_to_bf16(src.data_ptr(), 300, 1345, dst.data_ptr(), 1408,
+                                  torch.cuda.current_stream().cuda_stream) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(dst[:, :1345], src.to(torch.bfloat16))
+    assert bool((dst[:, 1345:] == 7.0).all())
+
+
 def test_clip_adam_matches_torch(torch_cuda):
     """grp_clip_adam (global-norm clip of the scaled gradient + Adam + the
     bf16 copy) against torch.nn.utils.clip_grad_norm_ and torch.optim.Adam
