@@ -102,19 +102,37 @@ struct PG {
   static constexpr int BAR_H = (2 * PX) / (NS + 1) > 2 ? (2 * PX) / (NS + 1) : 2;
   static constexpr int Y0 = O::VR * PX;
   static constexpr int NCLASS = O::VR * 4 + 6;                     // row classes (see row_class)
-  static constexpr int PS = ((RB + 20) + ((RB + 20) >> 7) * 4 + 15) / 16 * 16;   // padded pattern row stride
+  // class-row stride: 32-word segments 37 words apart (see pix_word) over
+  // the RB bytes plus the 8 the last chunk's funnel shift may read beyond
+  static constexpr int PS = ((RB + 8 + 3) / 4 + 31) / 32 * 37 * 4;
   static constexpr int SMEM = NCLASS * PS;
+  static_assert(NCLASS * PS < 65536, "row offsets are 16-bit");
 };
 
-// Pattern rows are stored with one pad word after every 32 words, so that
-// lanes reading words 16 bytes apart (consecutive 16-byte chunks) hit
-// distinct shared-memory banks: logical byte B of a row sits at pix_off(B).
-__device__ __forceinline__ int pix_off(int B) { return B + ((B >> 7) << 2); }
-__device__ __forceinline__ int pix_word(int L) { return L + (L >> 5); }   // the same for word L
-// the 4 bytes at logical byte offset off >= 0 of a padded pattern row
+// Pattern (class) rows are stored as 32-word segments 37 words apart; the 4
+// words after a segment repeat the first 4 of the next one.  So the 5 words
+// a 16-byte chunk is shifted out of sit at 5 consecutive addresses (one base
+// + immediate offsets, no per-word fix-up), and lanes reading words 16 bytes
+// apart (consecutive chunks) hit distinct banks (37 = 5 mod 32).  Logical
+// word L sits at pix_word(L); its repeat (first 4 words of a segment) 5
+// words before.
+__device__ __forceinline__ int pix_word(int L) { return L + 5 * (L >> 5); }
+__device__ __forceinline__ int pix_off(int B) { return 4 * pix_word(B >> 2) + (B & 3); }
+__device__ __forceinline__ void put_word(uint32_t* w, int L, uint32_t v) {
+  const int a = pix_word(L);
+  w[a] = v;
+  if ((L & 31) < 4 && L >= 32) w[a - 5] = v;
+}
+__device__ __forceinline__ void put_byte(uint8_t* p, int B, uint8_t v) {
+  const int a = pix_off(B);
+  p[a] = v;
+  if (((B >> 2) & 31) < 4 && B >= 128) p[a - 20] = v;
+}
+// the 4 bytes at logical byte offset off >= 0 of a pattern row
 __device__ __forceinline__ uint32_t pat_word(const uint32_t* w, int off) {
   const int L = off >> 2;
-  return __funnelshift_r(w[pix_word(L)], w[pix_word(L + 1)], (off & 3) * 8);
+  const uint32_t* x = w + pix_word(L);
+  return __funnelshift_r(x[0], x[1], (off & 3) * 8);
 }
 
 // The frame rows fall into a few classes that depend on the geometry only:
@@ -314,6 +332,7 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(
   uint8_t* pat = reinterpret_cast<uint8_t*>(pix_dyn);   // [NCLASS][PS]
   __shared__ __align__(16) uint32_t pmw[2][PW];
   __shared__ uint8_t rowcls[G::FH];
+  __shared__ uint16_t rowoff[G::FH];   // byte offset of frame row y's class row
   __shared__ int16_t rep[G::NCLASS];
   __shared__ uint8_t ucls[G::NCLASS];
   __shared__ int nused;
@@ -326,6 +345,7 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(
   for (int y = threadIdx.x; y < G::FH; y += blockDim.x) {
     const int c = row_class<EXT, PX>(y);
     rowcls[y] = (uint8_t)c;
+    rowoff[y] = (uint16_t)(c * G::PS);
     rep[c] = (int16_t)y;
   }
   __syncthreads();
@@ -409,7 +429,7 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(
             const uint32_t rgb = ix >= G::INSET && ix < PX - G::INSET ? ci[k] : ct[k];
             v |= ((rgb >> (8 * (2 - ch))) & 0xFFu) << (8 * j);
           }
-          wp[pix_word(L0 + w)] = v;
+          put_word(wp, L0 + w, v);
         }
       }
       constexpr int LEFT = O::VC - NGR * GS;
@@ -425,9 +445,9 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(
 #pragma unroll
         for (int ix = 0; ix < PX; ++ix) {
           const uint32_t rgb = ins && ix >= G::INSET && ix < PX - G::INSET ? ic : tc;
-          p[pix_off(B0 + 3 * ix)] = (uint8_t)(rgb >> 16);
-          p[pix_off(B0 + 3 * ix + 1)] = (uint8_t)(rgb >> 8);
-          p[pix_off(B0 + 3 * ix + 2)] = (uint8_t)rgb;
+          put_byte(p, B0 + 3 * ix, (uint8_t)(rgb >> 16));
+          put_byte(p, B0 + 3 * ix + 1, (uint8_t)(rgb >> 8));
+          put_byte(p, B0 + 3 * ix + 2, (uint8_t)rgb);
         }
       }
       // side panel of the tile-row classes (gear bar k = tile row, per
@@ -443,9 +463,9 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(
                                         : 0x1E1E1Eu;
         uint8_t* p = pat + c * G::PS;
         const int B0 = 3 * (O::VC * PX + xx);
-        p[pix_off(B0)] = (uint8_t)(rgb >> 16);
-        p[pix_off(B0 + 1)] = (uint8_t)(rgb >> 8);
-        p[pix_off(B0 + 2)] = (uint8_t)rgb;
+        put_byte(p, B0, (uint8_t)(rgb >> 16));
+        put_byte(p, B0 + 1, (uint8_t)(rgb >> 8));
+        put_byte(p, B0 + 2, (uint8_t)rgb);
       }
       // ... and the bottom-strip classes (vital bar k, or blank), 4 pixels
       // -> 3 words per task
@@ -462,11 +482,11 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(
           cl[m] = k < G::NS && x >= 1 && x < 1 + O::VC * PX - 2 ? (x < 1 + fl ? barc : 0x1E1E1Eu) : 0u;
         }
         // bytes r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3 (little-endian words)
-        uint8_t* p = pat + c * G::PS;
-        const int B0 = 3 * x0;   // a multiple of 4
-        *reinterpret_cast<uint32_t*>(p + pix_off(B0)) = __byte_perm(cl[0], cl[1], 0x6012);
-        *reinterpret_cast<uint32_t*>(p + pix_off(B0 + 4)) = __byte_perm(cl[1], cl[2], 0x5601);
-        *reinterpret_cast<uint32_t*>(p + pix_off(B0 + 8)) = __byte_perm(cl[2], cl[3], 0x4560);
+        uint32_t* p = reinterpret_cast<uint32_t*>(pat + c * G::PS);
+        const int L0 = 3 * x0 / 4;   // 3 * x0 is a multiple of 4
+        put_word(p, L0, __byte_perm(cl[0], cl[1], 0x6012));
+        put_word(p, L0 + 1, __byte_perm(cl[1], cl[2], 0x5601));
+        put_word(p, L0 + 2, __byte_perm(cl[2], cl[3], 0x4560));
       }
     }
     __syncthreads();
@@ -526,20 +546,28 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(
       // pattern is addressed in words with the pad word per 32 folded in
       constexpr int NT = pix_threads<EXT, PX>();
       constexpr int DY = NT * 16 / G::RB, DO = NT * 16 - DY * G::RB;
-      const uint32_t* patw = reinterpret_cast<const uint32_t*>(pat);
+      // shared-space addresses (32-bit, laundered through a mov so they stay
+      // in registers instead of being re-derived from the CTA id every
+      // chunk): per chunk one row-offset load, 5 pattern loads at immediate
+      // offsets, 4 funnel shifts and the store
+      uint32_t pat_s, row_s;
+      asm volatile("mov.u32 %0, %1;" : "=r"(pat_s) : "r"((uint32_t)__cvta_generic_to_shared(pat)));
+      asm volatile("mov.u32 %0, %1;" : "=r"(row_s) : "r"((uint32_t)__cvta_generic_to_shared(rowoff)));
       int b = (int)(c0 - f0) + 16 * (int)threadIdx.x;
       int y = b / G::RB, o = b - y * G::RB;
       uint4* dst = reinterpret_cast<uint4*>(out + c0) + threadIdx.x;
+#pragma unroll 2
       for (int q = threadIdx.x; q < nchunk; q += NT) {
-        if (o + 16 <= G::RB) {
-          const uint32_t* w = patw + rowcls[y] * (G::PS / 4);
-          const int L = o >> 2, sh = (o & 3) * 8, r = L & 31;
-          const uint32_t* wl = w + L + (L >> 5);
-          const uint32_t x0 = wl[0];
-          const uint32_t x1 = wl[1 + (r >= 31)];
-          const uint32_t x2 = wl[2 + (r >= 30)];
-          const uint32_t x3 = wl[3 + (r >= 29)];
-          const uint32_t x4 = wl[4 + (r >= 28)];
+        if (o <= G::RB - 16) {
+          uint32_t ro, x0, x1, x2, x3, x4;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=r"(ro) : "r"(row_s + 2u * (uint32_t)y));
+          const uint32_t ad = pat_s + ro + (uint32_t)(o & ~3) + 20u * (uint32_t)(o >> 7);
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x0) : "r"(ad));
+          asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(x1) : "r"(ad));
+          asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(x2) : "r"(ad));
+          asm volatile("ld.shared.u32 %0, [%1+12];" : "=r"(x3) : "r"(ad));
+          asm volatile("ld.shared.u32 %0, [%1+16];" : "=r"(x4) : "r"(ad));
+          const uint32_t sh = (uint32_t)(o & 3) * 8u;
           *dst = make_uint4(__funnelshift_r(x0, x1, sh), __funnelshift_r(x1, x2, sh), __funnelshift_r(x2, x3, sh),
                             __funnelshift_r(x3, x4, sh));
         }
