@@ -614,6 +614,7 @@ static int observe(gr_env* e, void* obs_dev, cudaStream_t st, bool recompute_fla
     if (pixels) launch_pixels(e->ext, e->S, oa, st);
     else launch_symbolic(e->ext, e->S, oa, st);
   }
+  if (recompute_flags) CK(cudaMemsetAsync(e->cur_flags, 0, sizeof(uint32_t), st));   // k_step expects it zero
   CK(cudaGetLastError());
   return GR_OK;
 }
@@ -700,7 +701,8 @@ static int step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, 
     const int rc = validate_actions(e, actions_dev, st);
     if (rc) return rc;
   }
-  CK(cudaMemsetAsync(e->cur_flags, 0, sizeof(uint32_t), st));
+  // cur_flags is zero here: k_step's last CTA clears it after use, observe()
+  // after its k_dark pass (no memset node per step)
   StepArgs a{};
   a.actions = actions_dev;
   a.reward = reward_dev;

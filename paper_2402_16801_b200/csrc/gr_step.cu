@@ -1453,6 +1453,7 @@ __global__ void __launch_bounds__(128, GR_STEP_MINB) k_step(DS S, StepArgs a) {
     a.exchange[3] = 0;
     if (a.info) combine_info(a.exchange, 0, 1, a.M, a.pool_key, a.dstep, a.info, a.flags_out, !a.defer_advance);
     *a.arrive = 0u;
+    *a.cur_flags = 0u;   // consumed: clean for the next step (no memset node per step)
   }
 }
 
