@@ -112,7 +112,9 @@ int gr_reset(gr_env *env, void *obs_dev, void *stream);
 /* BatchEnv.step (__init__.py:63-84) == batch_step(bs, actions)
  * (batch.py:193-234) + post-reset encode_symbolic_batch.
  *   actions_dev  int64[n]                 (validate: see gr_set_validate)
- *   obs_dev      float32[n, L] or uint8[n, H, W, 3], post-reset; may be NULL
+ *   obs_dev      float32[n, L] or uint8[n, H, W, 3], post-reset; may be NULL;
+ *                any alignment of its element type (16-byte-aligned buffers
+ *                take the TMA row stores, others plain stores)
  *   reward_dev   float32[n]               (reward.astype(float32))
  *   done_dev     uint8[n]
  *   newly_dev    uint8[n, A] or NULL      (info["newly_unlocked"])

@@ -602,7 +602,7 @@ static int observe(gr_env* e, void* obs_dev, cudaStream_t st, bool recompute_fla
     k_dark<<<(unsigned)e->nb, 128, 0, st>>>(e->S, e->n, e->cur_flags);
   }
   ObsArgs oa{obs_dev, e->n, recompute_flags ? e->cur_flags : e->prev_flags, e->cfg.tile_px, e->last_done, sel,
-             e->tma ? 1 : 0, sel == 1 ? e->obs_ctas_overlap : e->obs_ctas_solo, e->done_list, e->info,
+             e->tma && (reinterpret_cast<uintptr_t>(obs_dev) & 15u) == 0 ? 1 : 0, sel == 1 ? e->obs_ctas_overlap : e->obs_ctas_solo, e->done_list, e->info,
              e->pix};
   const bool pixels = e->cfg.obs_mode == GR_OBS_PIXELS;
   if (pixels) {   // k_pixprep

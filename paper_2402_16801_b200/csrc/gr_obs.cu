@@ -382,7 +382,11 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(
   }
   __syncthreads();
   int cur = 0;
-  uint8_t* out = (uint8_t*)a.out;
+  // frame offsets are taken from the 16-byte-aligned address at or below
+  // the buffer, so the "aligned" chunks are aligned in absolute terms for
+  // any buffer alignment (a uint8 tensor view may start anywhere)
+  const int mis = (int)(reinterpret_cast<uintptr_t>(a.out) & 15u);
+  uint8_t* out = (uint8_t*)a.out - mis;
   while (j >= 0) {
     const int64_t i = env_of(j);
     // the next env: its done flag is loaded now and only looked at after
@@ -493,7 +497,7 @@ __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(
     const int64_t jn = !cand_ok ? -1 : cand_done ? next_env(cand + stride) : cand;
     if (warp == 0 && jn >= 0) fetch(env_of(jn), cur ^ 1);   // the next env's inputs, under this env's stores
     // 2. stream the frame: bytes [f0, f0 + FB) of the output
-    const int64_t f0 = i * (int64_t)G::FB;
+    const int64_t f0 = i * (int64_t)G::FB + mis;
     const int64_t c0 = (f0 + 15) & ~(int64_t)15, c1 = (f0 + G::FB) & ~(int64_t)15;
     const int nchunk = (int)((c1 - c0) >> 4);
     auto byte_at = [&](int b) -> uint32_t {

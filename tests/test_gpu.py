@@ -1308,3 +1308,34 @@ def test_host_pixels_row_classes_equal_device_frames(torch_cuda, monkeypatch, ti
         host.step(host.random_actions(seed, k))
         o2 = dev.step(dev.random_actions(seed, k))[0]
         assert np.array_equal(host.obs_to_host(out), o2.cpu().numpy()), f"step {k}"
+
+
+@pytest.mark.parametrize("tier,obs_mode,px,n,offset", [
+    ("extended", "symbolic", None, 700, 0), ("extended", "symbolic", None, 700, 4),
+    ("classic", "symbolic", None, 523, 12), ("extended", "pixels", 10, 301, 0),
+    ("extended", "pixels", 10, 301, 3), ("classic", "pixels", 7, 259, 1),
+    ("extended", "pixels", 16, 77, 9), ("extended", "pixels", 7, 101, 14)])
+def test_writers_stay_inside_the_observation_buffer(torch_cuda, tier, obs_mode, px, n, offset):
+    """Out-of-bounds evidence without compute-sanitizer (closed on this GPU
+    pool): the observation buffer is a view into a larger allocation whose
+    guard bands hold a fill pattern, at 16-byte-aligned and unaligned starts
+    (the writers take TMA / 16-byte stores from the aligned address at or
+    below the buffer); every step under reset stress, the guard bands stay
+    untouched and the frames equal a normally allocated twin's."""
+    from paper_2402_16801_b200 import GridrogueBatch
+    torch = torch_cuda
+    kw = {"tile_px": px} if px else {}
+    gb = GridrogueBatch(n, tier, 5, obs_mode, 9, **kw)
+    twin = GridrogueBatch(n, tier, 5, obs_mode, 9, **kw)
+    nbytes = gb.obs.numel() * gb.obs.element_size()
+    G = 4096
+    big = torch.full((nbytes + 2 * G,), 0xA5, dtype=torch.uint8, device="cuda")
+    gb.obs = big[G + offset:G + offset + nbytes].view(gb.obs.dtype).view(gb.obs.shape)
+    guard = lambda: (big[:G + offset].eq(0xA5).all().item() and big[G + offset + nbytes:].eq(0xA5).all().item())
+    gb.reset()
+    assert torch.equal(gb.obs, twin.reset()) and guard()
+    for k in range(30):
+        gb.step(gb.random_actions(5, k))
+        twin.step(twin.random_actions(5, k))
+        assert guard(), f"guard band written at step {k}"
+        assert torch.equal(gb.obs.view(torch.uint8), twin.obs.view(torch.uint8)), f"step {k}"
