@@ -31,7 +31,9 @@ timed region.  ``e2e.value`` is the reference's contract (writable
 observation arrays, a dense 2.17 GB copy per step, PCIe-bound);
 ``e2e.delta`` is BatchEnv(obs_transfer="delta") (read-only arrays owned by the
 handle; only the words changed since a buffer's last step cross PCIe).  Each
-carries the host-measured phase breakdown (gr_host_phase_times).  State
+carries the host-measured phase breakdown (gr_host_phase_times) and is the
+median of three windows of --e2e-steps steps (listed with their spread: the
+host-side phases vary with the box's host load).  State
 (~2.8 GB) and the per-step obs (2.17 GB) exceed the 126 MB L2, so no explicit
 flush is needed between steps.
 
@@ -452,6 +454,9 @@ def _phases(gb) -> dict:
             "changed_words_per_step": int(words.value / c)}   # delta: changed words; compact: non-zero words
 
 
+E2E_WINDOWS = 3
+
+
 def run_e2e(args, gb, env, world, rank, dist, t):
     import numpy as np
     import torch
@@ -460,7 +465,7 @@ def run_e2e(args, gb, env, world, rank, dist, t):
     n = gb.n
     pol = RandomPolicy(SEED, gb.n_actions)
     steps = args.e2e_steps
-    acts = [pol.actions_at(t + k, n, env0=gb.cfg.env_offset) for k in range(steps + 2)]
+    acts = [pol.actions_at(t + k, n, env0=gb.cfg.env_offset) for k in range(steps * E2E_WINDOWS + 2)]
     small_d2h = n * (4 + 1 + gb.n_achievements + 4 + 1)   # reward, done, newly, time, floor
     obs_bytes = int(np.prod(gb.obs.shape[1:])) * gb.obs.element_size() * n
     torch.cuda.synchronize()
@@ -469,15 +474,22 @@ def run_e2e(args, gb, env, world, rank, dist, t):
     if world == 1:
         def run(be, k0):
             # BatchEnv.step is the timed call; the caller drops each step's
-            # arrays before the next step, like a training loop would
+            # arrays before the next step, like a training loop would.  Three
+            # windows of `steps` steps: the median is reported, the windows
+            # beside it (the host-side phases vary with the box's host load)
             be.step(acts[k0])
             _phases(gb)
-            t0 = time.perf_counter()
-            for k in range(steps):
-                obs, rew, done, info = be.step(acts[k0 + 1 + k])
-                del obs, rew, done, info
-            dt = time.perf_counter() - t0
-            return n * steps / dt, _phases(gb)
+            vals = []
+            for w in range(E2E_WINDOWS):
+                t0 = time.perf_counter()
+                for k in range(steps):
+                    obs, rew, done, info = be.step(acts[k0 + 1 + w * steps + k])
+                    del obs, rew, done, info
+                vals.append(n * steps / (time.perf_counter() - t0))
+            ph = _phases(gb)
+            ph["windows"] = [round(v, 1) for v in vals]
+            ph["spread"] = round((max(vals) - min(vals)) / statistics.median(vals), 4)
+            return statistics.median(vals), ph
 
         dense_env = BatchEnv.from_batch(gb, "dense")
         v_dense, ph_dense = run(dense_env, 0)
