@@ -308,6 +308,7 @@ struct gr_env {
                               // inside a step graph the other order starves the writer (0.55 vs 0.49 ms)
   int side_prio = 0;          // side stream priority (0 default, >0 lowest, <0 highest)
   bool graph_prio = true;     // GR_GRAPH_PRIO=0: step graphs instantiated without per-node priorities
+  int install_parts = 1;      // CTAs per env in the pool install (GR_INSTALL_PARTS; 4 up to 16,384 extended envs)
   bool graphs = true;         // GR_GRAPH=0: launch the step kernel by kernel
   // speculative pool (one-shard steps): the side stream generates the first
   // spec_k worlds of this step's pool beside k_step, before the done count
@@ -475,6 +476,8 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (const char* of = getenv("GR_OBS_FIRST")) e->obs_first = atoi(of) != 0;
   if (const char* sp = getenv("GR_SIDE_PRIO")) e->side_prio = atoi(sp);
   if (const char* gp = getenv("GR_GRAPH_PRIO")) e->graph_prio = atoi(gp) != 0;
+  e->install_parts = e->ext && cfg->n_envs <= 16384 ? 4 : 1;
+  if (const char* ip = getenv("GR_INSTALL_PARTS")) e->install_parts = std::max(1, atoi(ip));
   if (const char* gg = getenv("GR_GRAPH")) e->graphs = atoi(gg) != 0;
   if (const char* pf = getenv("GR_SCATTER_PF")) e->scatter_prefetch = atoi(pf);
   if (const char* hc = getenv("GR_HOST_COMPACT")) e->compact = atoi(hc) != 0;
@@ -816,6 +819,7 @@ static int step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank,
   InstallArgs ia{};
   ia.mode = 1;
   ia.n = e->n;
+  ia.parts = e->install_parts;
   ia.done_list = e->done_list;
   ia.info = e->info;
   ia.pool = e->pool;

@@ -108,6 +108,7 @@ struct InstallArgs {
   int32_t* spec_k;
   int64_t spec_cap;
   int64_t n;                  // mode 0 env count
+  int parts;                  // mode 1: CTAs per installed env (>= 1)
   const int32_t* done_list;   // mode 1: env index per local done rank (k_compact)
   const StepInfo* info;
   WBuf pool;
