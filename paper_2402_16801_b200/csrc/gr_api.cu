@@ -72,6 +72,9 @@ __global__ void k_selftest_argsort6(const float* keys, uint8_t* idx, int64_t n) 
 }
 
 // first invalid action (engine.py:715-717)
+// an empty kernel: the single root of a speculative step graph (see step_local)
+__global__ void k_fork_root() {}
+
 __global__ void k_validate(const int64_t* a, int64_t n, int na, unsigned long long* bad) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && (a[i] < 0 || a[i] >= na)) atomicMin(bad, (unsigned long long)i);
@@ -309,6 +312,12 @@ struct gr_env {
   int side_prio = 0;          // side stream priority (0 default, >0 lowest, <0 highest)
   bool graph_prio = true;     // GR_GRAPH_PRIO=0: step graphs instantiated without per-node priorities
   int install_parts = 1;      // CTAs per env in the pool install (GR_INSTALL_PARTS; 4 up to 16,384 extended envs)
+  bool fork_root = false;     // GR_FORK_ROOT=1: an empty root kernel before the speculative fork
+  int spec_ctas = 0;          // grid cap of the speculative worldgen pass (GR_SPEC_CTAS, 0 none)
+  bool spec_pdl = true;       // GR_SPEC_PDL=0: the speculative pass as a second graph root on the side stream
+  bool spec_main = false;     // this step's speculative pass runs behind k_step on the caller's stream
+  cudaEvent_t ev_k = nullptr; // k_step complete (spec_pdl)
+  int spec_rem_ctas = 0;      // grid cap of the pool remainder after a speculative pass (GR_SPEC_REM_CTAS, 0 none)
   bool graphs = true;         // GR_GRAPH=0: launch the step kernel by kernel
   // speculative pool (one-shard steps): the side stream generates the first
   // spec_k worlds of this step's pool beside k_step, before the done count
@@ -436,6 +445,7 @@ void gr_destroy(gr_env* e) {
   if (e->ev_fork) cudaEventDestroy(e->ev_fork);
   if (e->ev_join) cudaEventDestroy(e->ev_join);
   if (e->ev_spec) cudaEventDestroy(e->ev_spec);
+  if (e->ev_k) cudaEventDestroy(e->ev_k);
   for (auto x : e->prof.pool) cudaEventDestroy(x);
   delete e;
 }
@@ -478,6 +488,15 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (const char* gp = getenv("GR_GRAPH_PRIO")) e->graph_prio = atoi(gp) != 0;
   e->install_parts = e->ext && cfg->n_envs <= 16384 ? 4 : 1;
   if (const char* ip = getenv("GR_INSTALL_PARTS")) e->install_parts = std::max(1, atoi(ip));
+  if (const char* sr = getenv("GR_SPEC_REM_CTAS")) e->spec_rem_ctas = std::max(0, atoi(sr));
+  if (const char* fr = getenv("GR_FORK_ROOT")) e->fork_root = atoi(fr) != 0;
+  if (const char* sc = getenv("GR_SPEC_CTAS")) e->spec_ctas = std::max(0, atoi(sc));
+  // without observations the worldgen, not k_step, is the step's critical
+  // path: there the speculative pass keeps its own root (worldgen first
+  // pays: extended / classic obs-off 65,536 envs 335 / 774-833 M as a second
+  // root vs 287 / 773-781 M behind k_step)
+  e->spec_pdl = cfg->obs_mode != GR_OBS_NONE;
+  if (const char* sp = getenv("GR_SPEC_PDL")) e->spec_pdl = atoi(sp) != 0;
   if (const char* gg = getenv("GR_GRAPH")) e->graphs = atoi(gg) != 0;
   if (const char* pf = getenv("GR_SCATTER_PF")) e->scatter_prefetch = atoi(pf);
   if (const char* hc = getenv("GR_HOST_COMPACT")) e->compact = atoi(hc) != 0;
@@ -508,8 +527,22 @@ int gr_create(const gr_config* cfg, gr_env** out) {
     // pixels lose beyond 1,024 envs (4,096: 59.7 -> 57.1 M, 65,536: 171 -> 166 M)
     // Extended without observations (the reset chain follows k_step with no
     // writer to hide behind) gains too: 65,536 envs 288 -> 299 M.
-    const bool any_size = cfg->obs_mode == GR_OBS_NONE || (!e->ext && cfg->obs_mode != GR_OBS_PIXELS);
-    e->spec_on = (any_size || e->nb <= (e->ext ? 32 : 8)) && ng == cfg->n_envs;
+    // End of round 2 the pass became k_step's programmatic dependent (it
+    // starts once k_step's CTAs are resident, in every graph instantiation),
+    // which removed the slow schedules the figures above were partly taken
+    // from; re-measured: on for every classic and every pixel configuration
+    // (classic pixels 4,096 / 65,536: 61.6 -> 66.7 / 180 -> 187 M; extended
+    // pixels 4,096 / 16,384 / 65,536: 32.1 -> 34.7 / 55.7 -> 61.3 / 72.5 ->
+    // 73.2 M) and for extended symbolic up to 16,384 envs (8,192: 61.1 ->
+    // 71.8 M, 16,384: 95.7 -> 97.4 M; 24,576: 119 -> 110 M, 65,536: 143 -> 122 M)
+    // Short episode caps (reset stress: thousands of worlds a step) leave it
+    // off when there are observations: a quarter more worlds than needed
+    // then costs more than it hides (extended pixels, 16-step episodes:
+    // 69.7 M off, 63-64 M on either way)
+    const bool short_eps = cfg->max_episode_length > 0 && cfg->max_episode_length < 64;
+    const bool any_size = !e->ext || cfg->obs_mode == GR_OBS_PIXELS;
+    e->spec_on = ng == cfg->n_envs &&
+                 (cfg->obs_mode == GR_OBS_NONE || (!short_eps && (any_size || e->n <= 16384)));
     if (const char* sp = getenv("GR_SPEC")) e->spec_on = atoi(sp) != 0 && ng == cfg->n_envs;
     e->wg_wide = e->nb <= 32;
     if (const char* ww = getenv("GR_WG_WIDE")) e->wg_wide = atoi(ww) != 0;
@@ -567,7 +600,8 @@ int gr_create(const gr_config* cfg, gr_env** out) {
                                      e->side_prio > 0 ? lo : e->side_prio < 0 ? hi : 0) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&e->ev_spec, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&e->ev_spec, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_k, cudaEventDisableTiming) != cudaSuccess)
       rc = fail(GR_E_CUDA, "stream/event creation failed");
   }
   if (rc != GR_OK) {
@@ -735,13 +769,12 @@ static int step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, 
     a.flags_out = e->prev_flags;
   }
   e->spec_pending = false;
-  if (fuse_info && e->spec_on) {
-    // the first spec_k worlds of this step's pool, on the side stream beside
-    // k_step; k_step leaves the step counter to k_install_pool so the
-    // speculative pass reads a stable value
-    CK(cudaEventRecord(e->ev_fork, st));
-    CK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
-    WorldJob sj{};
+  const bool spec = fuse_info && e->spec_on;
+  WorldJob sj{};
+  if (spec) {
+    // the first spec_k worlds of this step's pool beside k_step; k_step
+    // leaves the step counter to k_install_pool so the speculative pass
+    // reads a stable value
     sj.mode = 3;
     sj.M = e->M;
     sj.out = e->pool;
@@ -752,18 +785,38 @@ static int step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, 
     sj.pool_key = e->pool_key;
     sj.dstep = e->dstep;
     sj.wide = e->wg_wide;
-    {
-      PTimer t(e, PK_WORLDGEN, e->side);
-      launch_worldgen(e->ext, sj, e->side);
-    }
-    CK(cudaEventRecord(e->ev_spec, e->side));
+    sj.max_ctas = e->spec_ctas;
     a.defer_advance = 1;
     e->spec_pending = true;
+    e->spec_main = e->spec_pdl;
+    if (!e->spec_pdl) {
+      // a second root on the side stream.  Captured this way, about one graph
+      // instantiation in four (classic 65,536 envs: one in two) dispatched
+      // the worldgen's CTAs first; they fill the SMs and k_step starts ~18
+      // us late (4,096 extended envs 0.114 instead of 0.087 ms per step)
+      CK(cudaEventRecord(e->ev_fork, st));
+      CK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+      {
+        PTimer t(e, PK_WORLDGEN, e->side);
+        launch_worldgen(e->ext, sj, e->side);
+      }
+      CK(cudaEventRecord(e->ev_spec, e->side));
+    }
   }
   e->last_done = done_dev;
   {
     PTimer t(e, PK_STEP, st);
     launch_step(e->ext, e->S, a, st);
+  }
+  if (spec && e->spec_pdl) {
+    // behind k_step on the same stream as its programmatic dependent: the
+    // worldgen starts once every k_step CTA is resident and fills the rest
+    // of the machine, in that order in every graph instantiation; the
+    // observation writer moves to the side stream (step_finish)
+    CK(cudaEventRecord(e->ev_k, st));
+    sj.pdl = 1;
+    PTimer t(e, PK_WORLDGEN, st);
+    launch_worldgen(e->ext, sj, st);
   }
   CK(cudaGetLastError());
   return GR_OK;
@@ -784,24 +837,34 @@ static int step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank,
     launch_finish_info(exchange_all_dev ? exchange_all_dev : e->exchange, rank, world, e->M, e->pool_key, e->dstep,
                        e->info, e->prev_flags, st);
   }
-  // reset work on the side stream, overlapping the obs of the other envs
+  // reset work on the side stream, overlapping the obs of the other envs --
+  // or, with the speculative pool behind k_step on the caller's stream
+  // (spec_main), the reset work behind it there and the obs writer forked off
   const bool split = e->overlap && obs_dev && e->cfg.obs_mode != GR_OBS_NONE && e->last_done;
-  cudaStream_t rs = split ? e->side : st;
+  const bool spec = e->spec_pending;
+  const bool spec_main = spec && e->spec_main;
+  e->spec_pending = false;
+  cudaStream_t rs = split && !spec_main ? e->side : st;
+  if (spec_main) CK(cudaStreamWaitEvent(st, e->ev_k, 0));   // k_step complete (the worldgen only followed its start)
   if (split) {
-    CK(cudaEventRecord(e->ev_fork, st));
-    CK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
-    if (e->obs_first) {   // the non-reset obs reaches the block scheduler first
-      const int rc = observe(e, obs_dev, st, false, 1);
+    if (spec_main) {
+      CK(cudaStreamWaitEvent(e->side, e->ev_k, 0));
+      const int rc = observe(e, obs_dev, e->side, false, 1);
       if (rc) return rc;
+    } else {
+      CK(cudaEventRecord(e->ev_fork, st));
+      CK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+      if (e->obs_first) {   // the non-reset obs reaches the block scheduler first
+        const int rc = observe(e, obs_dev, st, false, 1);
+        if (rc) return rc;
+      }
     }
   }
   {
     PTimer t(e, PK_SCAN, rs);
     launch_compact((const uint8_t*)e->S.f[GR_F_DONE], e->n, e->block_off, e->done_list, rs);
   }
-  const bool spec = e->spec_pending;
-  e->spec_pending = false;
-  if (spec && rs != e->side) CK(cudaStreamWaitEvent(rs, e->ev_spec, 0));
+  if (spec && !spec_main && rs != e->side) CK(cudaStreamWaitEvent(rs, e->ev_spec, 0));
   WorldJob j{};
   j.mode = 1;
   j.info = e->info;
@@ -811,6 +874,9 @@ static int step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank,
   j.max_attempts = e->wg_attempts;
   j.ctas_per_sm = e->wg_ctas;
   j.spec_k = spec ? e->spec_k : nullptr;   // only the slots the speculative pass did not make
+  // (usually none: a small grid, whose empty launch costs less on the
+  // small-batch critical path; a rare shortfall takes more items per CTA)
+  j.max_ctas = spec ? e->spec_rem_ctas : 0;
   j.wide = e->wg_wide;
   {
     PTimer t(e, PK_WORLDGEN, rs);
@@ -842,7 +908,7 @@ static int step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank,
   if (!split) return observe(e, obs_dev, st, false);
   int rc = observe(e, obs_dev, rs, false, 2);   // reset envs, after their install
   if (rc) return rc;
-  if (!e->obs_first) {
+  if (!e->obs_first && !spec_main) {
     rc = observe(e, obs_dev, st, false, 1);     // everyone else, concurrently
     if (rc) return rc;
   }
@@ -905,6 +971,12 @@ int gr_step(gr_env* e, const int64_t* actions_dev, void* obs_dev, float* reward_
       return rc;
     }
     if (ce != cudaSuccess) return fail(GR_E_CUDA, "step graph capture: %s", cudaGetErrorString(ce));
+    if (const char* dot = getenv("GR_GRAPH_DOT")) {   // dev: dump each captured step graph
+      static int ndot = 0;
+      char path[512];
+      snprintf(path, sizeof(path), "%s.%d.dot", dot, ndot++);
+      cudaGraphDebugDotPrint(graph, path, cudaGraphDebugDotFlagsVerbose);
+    }
     StepGraph ng{};
     memcpy(ng.key, key, sizeof(key));
     // per-node priorities (all equal unless GR_SIDE_PRIO is set) make the

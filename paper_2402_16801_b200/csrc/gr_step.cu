@@ -1260,6 +1260,10 @@ __global__ void __launch_bounds__(128, GR_STEP_MINB) k_step(DS S, StepArgs a) {
     s_blk_base = (uint8_t*)S.f[GR_F_BLOCKS];
     s_itm_base = (uint8_t*)S.f[GR_F_ITEMS];
   }
+  // a speculative worldgen pass launched behind this kernel as a programmatic
+  // dependent (it reads nothing this kernel writes) may start once every CTA
+  // of this grid is resident, i.e. after this kernel has its SMs
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #if GR_STEP_SMEM_CTX
   extern __shared__ __align__(16) unsigned char s_ctx_raw[];
   Ctx& e = reinterpret_cast<Ctx*>(s_ctx_raw)[threadIdx.x];

@@ -982,7 +982,22 @@ void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st) {
   int64_t max_items = (j.mode == 1 || j.mode == 3 ? j.out.cap : j.count) * (ext ? 9 : 1);
   int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * (j.ctas_per_sm > 0 ? j.ctas_per_sm
                                                                 : ext ? WT<true>::MINB : WT<false>::MINB));
+  if (j.max_ctas > 0) grid = std::min(grid, j.max_ctas);
   if (grid <= 0) return;
+  if (j.pdl) {   // starts once every CTA of the preceding kernel (k_step) is resident
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(ext ? WT<true>::THREADS : WT<false>::THREADS);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (ext) cudaLaunchKernelEx(&cfg, k_worldgen<true>, j);
+    else cudaLaunchKernelEx(&cfg, k_worldgen<false>, j);
+    return;
+  }
   if (ext) k_worldgen<true><<<grid, WT<true>::THREADS, 0, st>>>(j);
   else k_worldgen<false><<<grid, WT<false>::THREADS, 0, st>>>(j);
 }
