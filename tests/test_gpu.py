@@ -1189,9 +1189,12 @@ def test_reference_world_blob_installs_like_reference(torch_cuda, tag):
     assert not bad, f"installed fields differ from the reference: {bad}"
 
 
-@pytest.mark.parametrize("tier,obs_mode,n,spec", [("extended", "symbolic", 8192, "0"), ("extended", "pixels", 2048, "0"),
-                                                  ("classic", "symbolic", 4096, "1"), ("extended", "symbolic", 1024, "1")])
-def test_two_stream_step_equals_serialised_step(torch_cuda, monkeypatch, tier, obs_mode, n, spec):
+@pytest.mark.parametrize("tier,obs_mode,n,spec,pdl", [
+    ("extended", "symbolic", 8192, "0", "1"), ("extended", "pixels", 2048, "0", "1"),
+    ("classic", "symbolic", 4096, "1", "1"), ("extended", "symbolic", 1024, "1", "1"),
+    ("extended", "pixels", 2048, "1", "1"), ("classic", "pixels", 1024, "1", "1"),
+    ("extended", "symbolic", 2048, "1", "0"), ("extended", "none", 2048, "1", "0")])
+def test_two_stream_step_equals_serialised_step(torch_cuda, monkeypatch, tier, obs_mode, n, spec, pdl):
     """Race evidence for the two-stream step (compute-sanitizer is not available
     on this GPU pool): the step whose reset chain (compaction, worldgen,
     install, reset-env obs) runs on a side stream beside the main observation
@@ -1199,13 +1202,16 @@ def test_two_stream_step_equals_serialised_step(torch_cuda, monkeypatch, tier, o
     produces the same observations, rewards, dones and full state, step for
     step, as the same batch with everything serialised on one stream, kernel
     by kernel (GR_OVERLAP=0, GR_GRAPH=0, GR_SPEC=0).  Reset stress: every
-    episode ends within 10 steps, so every step runs the reset chain."""
+    episode ends within 10 steps, so every step runs the reset chain.  The
+    speculative pass runs either behind k_step as its programmatic dependent
+    with the obs writer forked off (pdl 1) or as its own graph root (pdl 0)."""
     from paper_2402_16801_b200 import GridrogueBatch
     from paper_2402_16801_b200.layout import field_shapes, FIELD_NAMES
     torch = torch_cuda
     monkeypatch.setenv("GR_SPEC", spec)
+    monkeypatch.setenv("GR_SPEC_PDL", pdl)
     fast = GridrogueBatch(n, tier, 9, obs_mode, 10)
-    for k, v in (("GR_OVERLAP", "0"), ("GR_GRAPH", "0"), ("GR_SPEC", "0")):
+    for k, v in (("GR_OVERLAP", "0"), ("GR_GRAPH", "0"), ("GR_SPEC", "0"), ("GR_SPEC_PDL", "0")):
         monkeypatch.setenv(k, v)
     slow = GridrogueBatch(n, tier, 9, obs_mode, 10)
     for b in (fast, slow):
