@@ -72,9 +72,6 @@ __global__ void k_selftest_argsort6(const float* keys, uint8_t* idx, int64_t n) 
 }
 
 // first invalid action (engine.py:715-717)
-// an empty kernel: the single root of a speculative step graph (see step_local)
-__global__ void k_fork_root() {}
-
 __global__ void k_validate(const int64_t* a, int64_t n, int na, unsigned long long* bad) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && (a[i] < 0 || a[i] >= na)) atomicMin(bad, (unsigned long long)i);
@@ -312,12 +309,9 @@ struct gr_env {
   int side_prio = 0;          // side stream priority (0 default, >0 lowest, <0 highest)
   bool graph_prio = true;     // GR_GRAPH_PRIO=0: step graphs instantiated without per-node priorities
   int install_parts = 1;      // CTAs per env in the pool install (GR_INSTALL_PARTS; 4 up to 16,384 extended envs)
-  bool fork_root = false;     // GR_FORK_ROOT=1: an empty root kernel before the speculative fork
-  int spec_ctas = 0;          // grid cap of the speculative worldgen pass (GR_SPEC_CTAS, 0 none)
   bool spec_pdl = true;       // GR_SPEC_PDL=0: the speculative pass as a second graph root on the side stream
   bool spec_main = false;     // this step's speculative pass runs behind k_step on the caller's stream
   cudaEvent_t ev_k = nullptr; // k_step complete (spec_pdl)
-  int spec_rem_ctas = 0;      // grid cap of the pool remainder after a speculative pass (GR_SPEC_REM_CTAS, 0 none)
   bool graphs = true;         // GR_GRAPH=0: launch the step kernel by kernel
   // speculative pool (one-shard steps): the side stream generates the first
   // spec_k worlds of this step's pool beside k_step, before the done count
@@ -488,9 +482,6 @@ int gr_create(const gr_config* cfg, gr_env** out) {
   if (const char* gp = getenv("GR_GRAPH_PRIO")) e->graph_prio = atoi(gp) != 0;
   e->install_parts = e->ext && cfg->n_envs <= 16384 ? 4 : 1;
   if (const char* ip = getenv("GR_INSTALL_PARTS")) e->install_parts = std::max(1, atoi(ip));
-  if (const char* sr = getenv("GR_SPEC_REM_CTAS")) e->spec_rem_ctas = std::max(0, atoi(sr));
-  if (const char* fr = getenv("GR_FORK_ROOT")) e->fork_root = atoi(fr) != 0;
-  if (const char* sc = getenv("GR_SPEC_CTAS")) e->spec_ctas = std::max(0, atoi(sc));
   // without observations the worldgen, not k_step, is the step's critical
   // path: there the speculative pass keeps its own root (worldgen first
   // pays: extended / classic obs-off 65,536 envs 335 / 774-833 M as a second
@@ -785,7 +776,6 @@ static int step_local(gr_env* e, const int64_t* actions_dev, float* reward_dev, 
     sj.pool_key = e->pool_key;
     sj.dstep = e->dstep;
     sj.wide = e->wg_wide;
-    sj.max_ctas = e->spec_ctas;
     a.defer_advance = 1;
     e->spec_pending = true;
     e->spec_main = e->spec_pdl;
@@ -874,9 +864,6 @@ static int step_finish(gr_env* e, const int32_t* exchange_all_dev, int32_t rank,
   j.max_attempts = e->wg_attempts;
   j.ctas_per_sm = e->wg_ctas;
   j.spec_k = spec ? e->spec_k : nullptr;   // only the slots the speculative pass did not make
-  // (usually none: a small grid, whose empty launch costs less on the
-  // small-batch critical path; a rare shortfall takes more items per CTA)
-  j.max_ctas = spec ? e->spec_rem_ctas : 0;
   j.wide = e->wg_wide;
   {
     PTimer t(e, PK_WORLDGEN, rs);

@@ -96,7 +96,6 @@ struct WorldJob {
   uint64_t pool_key;
   const unsigned long long* dstep;
   int wide;                      // extended tier: 512-thread CTAs (gr_world_wide.cu)
-  int max_ctas = 0;              // grid cap (0: none) -- the remainder after a speculative pass is usually empty
   int pdl = 0;                   // launch as a programmatic dependent of the preceding kernel in the stream
   int max_attempts = 16;         // worldgen.MAX_GEN_RETRIES (worldgen.py:36)
 };

@@ -982,7 +982,6 @@ void launch_worldgen(bool ext, const WorldJob& j, cudaStream_t st) {
   int64_t max_items = (j.mode == 1 || j.mode == 3 ? j.out.cap : j.count) * (ext ? 9 : 1);
   int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * (j.ctas_per_sm > 0 ? j.ctas_per_sm
                                                                 : ext ? WT<true>::MINB : WT<false>::MINB));
-  if (j.max_ctas > 0) grid = std::min(grid, j.max_ctas);
   if (grid <= 0) return;
   if (j.pdl) {   // starts once every CTA of the preceding kernel (k_step) is resident
     cudaLaunchConfig_t cfg{};
