@@ -688,7 +688,13 @@ struct TileSmem {
 #define GR_OBS_WIN_EARLY 1   // symbolic writer: next env's window loads issued before the scatter
 #endif
 template <bool EXT>
-__host__ __device__ constexpr int stage_warps() { return EXT ? 2 : 8; }
+#ifndef GR_CLS_WARPS
+#define GR_CLS_WARPS 4   // classic symbolic writer: warps (rows in flight) per CTA (4 x 8 CTAs/SM: 0.1378 -> 0.1370 ms/step at 65,536 envs against 8 x 4)
+#endif
+#ifndef GR_CLS_CTAS
+#define GR_CLS_CTAS 8    // classic symbolic writer: CTAs per SM (8 x 5, 4 x 10, 16 x 2 measured slower)
+#endif
+__host__ __device__ constexpr int stage_warps() { return EXT ? 2 : GR_CLS_WARPS; }
 // one stage = one whole row + up to 3 floats of alignment shift
 template <bool EXT>
 __host__ __device__ constexpr int stage_floats() { return EXT ? 8272 : 1352; }
@@ -909,7 +915,7 @@ void launch_symbolic(bool ext, const DS& S, const ObsArgs& a, cudaStream_t st) {
     const size_t smem = (size_t)NW * stage_floats<false>() * sizeof(float);
     static PerDeviceOnce once;
     once([&](int) { cudaFuncSetAttribute(k_symbolic_stage<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
-    const int grid = (int)std::min<int64_t>((a.n + NW - 1) / NW, (int64_t)sms * 4);
+    const int grid = (int)std::min<int64_t>((a.n + NW - 1) / NW, (int64_t)sms * GR_CLS_CTAS);
     k_symbolic_stage<false><<<grid, NW * 32, smem, st>>>(S, a);
   }
 }
