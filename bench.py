@@ -75,9 +75,18 @@ WORLD_BYTES = {"extended": 2 * 9 * 48 * 48, "classic": 2 * 64 * 64}
 # descriptor (gr_desc.cuh, read whole); pixels (k_pixels, after k_pixprep): frame written + the 848 /
 # 560 B per-env scratch read
 OBS_KERNEL_BYTES = {("extended", "symbolic"): 33072 + 99 + 255 + 256,
-                    ("classic", "symbolic"): 5380 + 63 + 256,
-                    ("extended", "pixels"): 42900 + 848,
-                    ("classic", "pixels"): 11907 + 560}
+                    ("classic", "symbolic"): 5380 + 63 + 256}
+
+
+def obs_kernel_bytes(tier: str, obs: str, tile_px: int | None) -> int:
+    """Bytes per env per launch of the observation writer; pixel frames are
+    ((view rows + 2) x px) x ((view cols + side panel) x px) x 3 (tiles.py:85-100)."""
+    if obs == "symbolic":
+        return OBS_KERNEL_BYTES[(tier, obs)]
+    ext = tier == "extended"
+    px = tile_px or (10 if ext else 7)
+    vr, vc, side = (9, 11, 2) if ext else (7, 9, 0)
+    return (vr + 2) * px * (vc + side) * px * 3 + (848 if ext else 560)
 
 
 def log(*a):
@@ -385,10 +394,10 @@ def main():
         # roofline of the dominant kernel (device-ms share of the step)
         dom = max(ktimes, key=lambda k: ktimes[k][0])
         dom_ms, dom_n = ktimes[dom]
-        if dom == "obs" and key in OBS_KERNEL_BYTES:
+        if dom == "obs" and args.obs in ("symbolic", "pixels"):
             # the main writer renders every env not reset this step; the reset
             # envs are rendered by a small launch after their install (obs_reset)
-            bytes_per_launch = int(OBS_KERNEL_BYTES[key] * (gb.n - resets_per_step))
+            bytes_per_launch = int(obs_kernel_bytes(args.tier, args.obs, args.tile_px) * (gb.n - resets_per_step))
         elif dom == "step":
             bytes_per_launch = STEP_KERNEL_BYTES[args.tier] * gb.n
         elif dom == "worldgen":

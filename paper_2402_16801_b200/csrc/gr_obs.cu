@@ -361,7 +361,12 @@ __global__ void __launch_bounds__(128) k_pixprep(DS S, ObsArgs a) {
 #define GR_PIX_STREAM_INC 1   // incremental (row, offset) walk in the chunk stream (0: divide per chunk)
 #endif
 template <bool EXT, int PX>
-__host__ __device__ constexpr int pix_threads() { return PG<EXT, PX>::FB >= 32768 ? 384 : 128; }
+// (end of round 2, 65,536 envs: classic 7 px with 96 threads 0.350 -> 0.343
+// ms per step; classic 10 px and extended 7 px lose with 96 or fewer, 64 and
+// 32 lose everywhere)
+__host__ __device__ constexpr int pix_threads() {
+  return !EXT && PX == 7 ? 96 : PG<EXT, PX>::FB >= 32768 ? 384 : 128;
+}
 
 template <bool EXT, int PX>
 __global__ void __launch_bounds__(pix_threads<EXT, PX>(), GR_PIX_MINB) k_pixels(DS S, ObsArgs a) {
