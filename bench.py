@@ -78,6 +78,25 @@ OBS_KERNEL_BYTES = {("extended", "symbolic"): 33072 + 99 + 255 + 256,
                     ("classic", "symbolic"): 5380 + 63 + 256}
 
 
+def pixel_class_row_bytes(tier: str, px: int) -> int:
+    """Bytes per frame of the compact pixel transfer: one row per row class
+    (the writer's row_class, gr_obs.cu: tile rows with / without insets and
+    gear bar, each vital bar, blank)."""
+    ext = tier == "extended"
+    vr, vc, side = (9, 11, 2) if ext else (7, 9, 0)
+    inset, ns = max(1, px // 4), (5 if ext else 4)
+    bar_h = max(2, (2 * px) // (ns + 1))
+    classes = set()
+    for y in range((vr + 2) * px):
+        if y < vr * px:
+            r, iy = divmod(y, px)
+            classes.add(r * 4 + (inset <= iy < px - inset) + 2 * (ext and r < 7 and 1 <= iy < px - 1))
+        else:
+            q = y - vr * px - 1
+            classes.add(vr * 4 + (q // bar_h if q >= 0 and q // bar_h < ns and q % bar_h < bar_h - 1 else 5))
+    return len(classes) * (vc + side) * px * 3
+
+
 def obs_kernel_bytes(tier: str, obs: str, tile_px: int | None) -> int:
     """Bytes per env per launch of the observation writer; pixel frames are
     ((view rows + 2) x px) x ((view cols + side panel) x px) x 3 (tiles.py:85-100)."""
@@ -477,6 +496,10 @@ def run_e2e(args, gb, env, world, rank, dist, t):
     acts = [pol.actions_at(t + k, n, env0=gb.cfg.env_offset) for k in range(steps * E2E_WINDOWS + 2)]
     small_d2h = n * (4 + 1 + gb.n_achievements + 4 + 1)   # reward, done, newly, time, floor
     obs_bytes = int(np.prod(gb.obs.shape[1:])) * gb.obs.element_size() * n
+    # the library's choice for host arrays (gr_create): the compact transfer
+    # unless disabled or below GR_HOST_COMPACT_MIN_MB of observations a step
+    compact = (os.environ.get("GR_HOST_COMPACT", "1") != "0"
+               and obs_bytes / 1048576.0 >= float(os.environ.get("GR_HOST_COMPACT_MIN_MB", "40")))
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -503,11 +526,15 @@ def run_e2e(args, gb, env, world, rank, dist, t):
         dense_env = BatchEnv.from_batch(gb, "dense")
         v_dense, ph_dense = run(dense_env, 0)
         dense_env.close()
-        if args.obs == "symbolic" and os.environ.get("GR_HOST_COMPACT", "1") != "0":
+        if args.obs == "symbolic" and compact:
             nb = (gb.obs.shape[1] + 31) // 32
             d2h_dense = n * nb * 4 + n * 8 + ph_dense["changed_words_per_step"] * 4 + small_d2h
             how = ("the observation travels packed (per row a non-zero bitmap + its values, gr_host_phase_times "
                    "words) and host threads expand it into the whole array (AVX-512 expand, streaming stores)")
+        elif args.obs == "pixels" and compact:
+            d2h_dense = n * pixel_class_row_bytes(args.tier, gb.tile_px) + small_d2h
+            how = ("the frames travel as one row per row class (rows of a class are byte-identical) and host "
+                   "threads replicate them into the whole array")
         else:
             d2h_dense = obs_bytes + small_d2h
             how = "D2H of the whole observation"
@@ -552,8 +579,10 @@ def run_e2e(args, gb, env, world, rank, dist, t):
     tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     dt = float(tt.item())
-    if args.obs == "symbolic" and os.environ.get("GR_HOST_COMPACT", "1") != "0":
+    if args.obs == "symbolic" and compact:
         d2h = n * ((gb.obs.shape[1] + 31) // 32) * 4 + n * 8 + ph["changed_words_per_step"] * 4 + small_d2h
+    elif args.obs == "pixels" and compact:
+        d2h = n * pixel_class_row_bytes(args.tier, gb.tile_px) + small_d2h
     else:
         d2h = obs_bytes + small_d2h
     return {"value": round(n * world * steps / dt, 1), "unit": UNIT, "h2d_bytes_per_step": n * 8,
